@@ -1,0 +1,102 @@
+"""Generate golden vectors from the REFERENCE implementation (`isattn`).
+
+Run in the build container, where /root/reference exists:
+
+    python tests/golden/make_golden.py
+
+For each case it generates inputs with the reference's own workload
+generator (`isattn.generate`, workload.py:127-144), rounds them to bf16
+values (the B200 path computes on bf16), runs the unmodified reference
+`isa_routing` / `isa_forward` (pipeline.py:302-316) and `full_attention`
+(reference.py:79-123), and stores the routing decisions and outputs in
+`tests/golden/<case>.npz`. Inputs are NOT stored: they are regenerated from
+the spec by `oracle.isa_oracle.workload` (a restatement of workload.py) and
+pinned by the stored checksums.
+
+The GPU box never runs this script (it has no /root/reference); the tests
+only read the committed .npz files.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+
+import isattn  # noqa: E402  (the reference)
+
+from oracle.isa_oracle import round_bf16  # noqa: E402
+
+CASES = [
+    # name, workload kind, B, H, S, D, l_src, l_ctx, seed, cfg overrides
+    ("cfg1_iid_s0", "iid-gaussian", 1, 2, 2048, 64, 1024, 1024, 0, {}),
+    ("cfg1_clustered_s1", "clustered", 1, 2, 2048, 64, 1024, 1024, 1, {}),
+    ("cfg1_lowrank_s2", "lowrank", 1, 2, 2048, 64, 1024, 1024, 2, {}),
+    ("ragged_iid_s3", "iid-gaussian", 1, 2, 2100, 64, 1000, 1100, 3, {"strict": False}),
+    ("d128_clustered_s4", "clustered", 1, 1, 2048, 128, 1024, 1024, 4, {}),
+    ("knobs_iid_s5", "iid-gaussian", 1, 2, 2048, 64, 1024, 1024, 5,
+     {"alpha_s": 0.25, "alpha_f": 0.25, "alpha_ns": 0.125}),
+    ("allsharp_iid_s6", "iid-gaussian", 1, 2, 2048, 64, 1024, 1024, 6, {"alpha_s": 1.0, "alpha_f": 0.0}),
+    ("allflat_exact_s7", "iid-gaussian", 1, 2, 2048, 64, 1024, 1024, 7,
+     {"alpha_s": 1.0, "alpha_f": 1.0, "alpha_ns": 1.0}),
+    ("srconly_s8", "clustered", 1, 2, 1024, 64, 1024, 0, 8, {}),
+    ("rawvar_clustered_s9", "clustered", 2, 1, 2048, 64, 1024, 1024, 9, {"softmax_first": False}),
+    ("ragged_clustered_s10", "clustered", 1, 2, 1500, 128, 900, 600, 10,
+     {"strict": False, "alpha_s": 0.5, "alpha_ns": 0.25}),
+    # routing-only cases (no stored output): larger T so the block mask has k > 1
+    ("mid_iid_s11", "iid-gaussian", 1, 2, 8192, 64, 4096, 4096, 11, {"_routing_only": True}),
+    ("mid_clustered_s12", "clustered", 1, 2, 8192, 128, 4096, 4096, 12, {"_routing_only": True}),
+    ("mid_lowrank_s13", "lowrank", 1, 1, 16384, 64, 8192, 8192, 13, {"_routing_only": True}),
+]
+
+IDENTITY = {"allsharp_iid_s6", "allflat_exact_s7"}
+
+
+def make_case(name, kind, B, H, S, D, l_src, l_ctx, seed, over):
+    spec = isattn.WorkloadSpec(batch=B, heads=H, seq_len=S, dim=D, l_src=l_src, l_ctx=l_ctx, kind=kind, seed=seed)
+    q, k, v, icl = isattn.generate(spec)
+    raw_sums = [float(x.astype(np.float64).sum()) for x in (q, k, v)]
+    q, k, v = (round_bf16(x) for x in (q, k, v))
+    over = dict(over)
+    routing_only = over.pop("_routing_only", False)
+    cfg = isattn.IsaConfig(**over)
+    t0 = time.perf_counter()
+    out, trace = isattn.isa_forward(q, k, v, icl, cfg)
+    t_isa = time.perf_counter() - t0
+    routing = isattn.isa_routing(q, k, v, icl, cfg)
+    payload = {
+        "selection": routing.selection.indices.astype(np.int64),
+        "sharp": routing.split.sharp.astype(np.int64),
+        "flat": routing.split.flat.astype(np.int64),
+        "sharpness": routing.split.sharpness.astype(np.float64),
+        "mask": (routing.mask.indices.astype(np.int64) if routing.mask is not None
+                 else np.zeros((B, H, 0, 0), np.int64)),
+        "input_sums": np.array([float(x.astype(np.float64).sum()) for x in (q, k, v)]),
+        "raw_input_sums": np.array(raw_sums),
+        "flops": np.array([trace.flops.exact_mas, trace.flops.taylor_mas, trace.flops.overhead_mas,
+                           trace.flops.dense_equivalent_mas], dtype=np.int64),
+    }
+    if not routing_only:
+        payload["out"] = out.astype(np.float32)
+    if name in IDENTITY:
+        payload["full"] = isattn.full_attention(q, k, v).astype(np.float32)
+    meta = {"name": name, "kind": kind, "B": B, "H": H, "S": S, "D": D, "l_src": l_src, "l_ctx": l_ctx,
+            "seed": seed, "cfg": over, "routing_only": routing_only, "ref_isa_seconds": t_isa,
+            "generator": "isattn.generate(WorkloadSpec(...)) then round to bf16"}
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), meta=json.dumps(meta), **payload)
+    print(f"{name}: isa_forward {t_isa:.2f}s  k_ctx={payload['selection'].shape[2]} "
+          f"n_flat={payload['flat'].shape[2]} k={payload['mask'].shape[3]}")
+
+
+if __name__ == "__main__":
+    only = set(sys.argv[1:])
+    for case in CASES:
+        if not only or case[0] in only:
+            make_case(*case)
