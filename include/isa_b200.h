@@ -1,0 +1,152 @@
+/*
+ * isa_b200.h — C ABI of the B200 (sm_100a) ISA forward operator.
+ *
+ * This is the drop-in boundary for the reference operator
+ *   isa_forward(q, k, v, icl, cfg, collect_trace=True) -> (out, IsaTrace)
+ *     /root/reference/pkg/src/isattn/pipeline.py:307-316
+ * and its routing hooks
+ *   isa_routing(q, k, v, icl, cfg) -> IsaRouting            pipeline.py:302-304
+ *   isa_forward_with_routing(q, k, v, icl, cfg, routing)     pipeline.py:319-328
+ * The reference is pure Python/numpy with no FFI of its own; the Python host
+ * layer (paper_2605_04569_b200/pipeline.py) binds these symbols with ctypes
+ * exactly as INTEGRATION.md shows a maintainer would.
+ *
+ * Conventions: plain C types only; every pointer to tensor data is a CUDA
+ * device pointer; every call is asynchronous and ordered on `stream`; the
+ * caller owns all buffers (inputs, outputs, workspace, routing arrays); no
+ * hidden allocations and no host synchronisation. Thread-safe for distinct
+ * streams/workspaces. Every entry point returns an IsaStatus; on failure
+ * isa_last_error() (thread-local) describes it. Status codes map 1:1 onto the
+ * reference exception classes (errors.py:4-37).
+ */
+#ifndef ISA_B200_H
+#define ISA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ISA_ABI_VERSION 1
+
+typedef enum IsaStatus {
+  ISA_OK = 0,
+  ISA_ERR_LAYOUT = 1,         /* LayoutError         errors.py:8  */
+  ISA_ERR_CONFIG = 2,         /* ConfigError         errors.py:24 */
+  ISA_ERR_NUMERIC = 3,        /* NumericError        errors.py:36 */
+  ISA_ERR_FORMAT = 4,         /* FormatError (reserved) errors.py:28 */
+  ISA_ERR_CONTRACT = 5,       /* ContractError       errors.py:20 */
+  ISA_ERR_BLOCK_INDEX = 6,    /* BlockIndexError     errors.py:16 */
+  ISA_ERR_INPUT = 7,          /* InputError          errors.py:12 */
+  ISA_ERR_DEGENERATE_ROW = 8, /* DegenerateRowError  errors.py:32 */
+  ISA_ERR_CUDA = 9            /* launch / driver failure          */
+} IsaStatus;
+
+typedef enum IsaDtype { ISA_DTYPE_BF16 = 0, ISA_DTYPE_F32 = 1 } IsaDtype;
+
+/* Geometry of Q/K/V (B,H,S,D) and the IclLayout (tensor.py:78-93). Q, K and V
+ * share shape and element strides; the D stride must be 1. `out` is written
+ * contiguous (B,H,S,D) in the input dtype. */
+typedef struct IsaShape {
+  int32_t batch, heads, seq_len, head_dim;
+  int32_t l_src, l_ctx;  /* source tokens first, then context */
+  int32_t block;         /* b (only 64 is implemented) */
+  int32_t dtype;         /* IsaDtype of q, k, v and out */
+  int64_t stride_b, stride_h, stride_s; /* element strides of q, k, v */
+} IsaShape;
+
+/* Host-derived integers, computed by the caller with the reference's float
+ * expressions: k_ctx = floor(alpha_s*T_ctx) (coarse.py:156), n_flat =
+ * floor(alpha_f*T) (coarse.py:197), k_mask = min(t_new, max(1,
+ * floor(alpha_ns*t_new))) (coarse.py:169). */
+typedef struct IsaKnobs {
+  double scale;          /* cfg.scale or 1/sqrt(D) (pipeline.py:154) */
+  int32_t k_ctx;
+  int32_t n_flat;
+  int32_t k_mask;
+  int32_t softmax_first; /* coarse.py:194 */
+  int32_t flags;         /* reserved, 0 */
+} IsaKnobs;
+
+/* Optional routing export (device pointers; any may be NULL). */
+typedef struct IsaRoutingOut {
+  int64_t* selection;  /* (B,H,k_ctx)      SelectionIndex.indices coarse.py:56 */
+  int64_t* sharp;      /* (B,H,n_sharp)    SharpnessSplit.sharp   coarse.py:95 */
+  int64_t* flat;       /* (B,H,n_flat)     SharpnessSplit.flat    coarse.py:96 */
+  int64_t* mask;       /* (B,H,n_flat,k)   BlockMask.indices      coarse.py:76 */
+  double* sharpness;   /* (B,H,T)          SharpnessSplit.sharpness coarse.py:97 */
+  double* ctx_scores;  /* (B,H,T_ctx)      context saliency (diagnostic) */
+} IsaRoutingOut;
+
+/* Pinned routing for isa_forward_with_routing (device int64, all required
+ * except mask when n_flat == 0). */
+typedef struct IsaRoutingIn {
+  const int64_t* selection;
+  const int64_t* sharp;
+  const int64_t* flat;
+  const int64_t* mask;
+} IsaRoutingIn;
+
+/* Optional per-stage CUDA events (cudaEvent_t handles cast to void*):
+ * ev[0] start, ev[1] after stage 1 "coarse", ev[2] after stage 2 "select",
+ * ev[3] after stage 3 "split", ev[4] after stage 4 "kernel" (pipeline.py:157-348;
+ * stage 5 "reconstruct" is fused into the stage-4 epilogues). NULL entries skip. */
+typedef struct IsaEvents {
+  void* ev[5];
+} IsaEvents;
+
+int isa_abi_version(void);
+const char* isa_last_error(void);
+
+/* Workspace needed by isa_forward / isa_routing for this geometry. */
+int isa_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* bytes);
+
+/* Full pipeline (stages 1-5). `pinned` == NULL computes routing on device,
+ * otherwise uses it (isa_forward_with_routing). `routing` may be NULL.
+ * `err_word` (device int32, may be NULL) receives bit 0 = non-finite input
+ * (InputError), bit 1 = degenerate row (DegenerateRowError); the caller
+ * zeroes it beforehand and reads it after the stream completes.
+ * `stream` is a cudaStream_t. */
+int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
+                void* out, void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned,
+                IsaRoutingOut* routing, int32_t* err_word, const IsaEvents* events, void* stream);
+
+/* Stages 1-3 only (isa_routing, pipeline.py:302-304). */
+int isa_routing(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
+                void* workspace, size_t workspace_bytes, IsaRoutingOut* routing, int32_t* err_word,
+                void* stream);
+
+/* Dense non-causal attention on the same sm_100a kernel (identity block
+ * tables): the speed-up denominator and the full_attention oracle
+ * (reference.py:79-123). Requires L_src, L_ctx multiples of 64 unless the
+ * sequence is a single segment. */
+int isa_dense_attention(const IsaShape* shape, double scale, const void* q, const void* k, const void* v,
+                        void* out, void* stream);
+
+/* ---- stage primitives (test hooks; same kernels as the pipeline) ---- */
+
+/* K1: block means (B,H,T,D) fp32 of q, k, v into means[3][B][H][T][D]. */
+int isa_pool_means(const IsaShape* shape, const void* q, const void* k, const void* v, float* means,
+                   int32_t* err_word, void* stream);
+
+/* Top-k of each row of a float64 (rows, n) matrix, ties to the lower index,
+ * emitted ascending (coarse.py:130-136). method 0 = CTA rank selection
+ * (context pre-selection kernel), 1 = warp arg-max rounds (block-mask kernel). */
+int isa_topk_rows_f64(const double* scores, int32_t rows, int32_t n, int32_t k, int64_t* out_idx,
+                      int32_t method, void* stream);
+
+/* Sharpness per row (coarse.py:193-195): population variance of the row
+ * softmax (softmax_first) or of the raw row. */
+int isa_sharpness_rows_f64(const double* s, int32_t rows, int32_t n, int32_t softmax_first, double* out,
+                           void* stream);
+
+/* Sharp/flat split of each row of sharpness values (coarse.py:196-200). */
+int isa_split_rows_f64(const double* m, int32_t rows, int32_t n, int32_t n_flat, int64_t* sharp, int64_t* flat,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISA_B200_H */

@@ -1,0 +1,51 @@
+"""B200-native (sm_100a) In-context Sparse Attention forward — drop-in for the
+reference `isattn` operator path (pkg/src/isattn/pipeline.py:302-328).
+
+    from paper_2605_04569_b200 import isa_forward, IsaConfig, IclLayout
+    out, trace = isa_forward(q, k, v, IclLayout(L_src, L_ctx), IsaConfig())
+
+The compute lives in libisa_b200.so (hand-written tcgen05/TMA kernels, C ABI in
+include/isa_b200.h); this package is the host-side mirror of the reference
+interface. There is no CPU fallback.
+"""
+
+from .errors import (
+    BlockIndexError,
+    ConfigError,
+    ContractError,
+    DegenerateRowError,
+    FormatError,
+    InputError,
+    IsaError,
+    LayoutError,
+    NativeError,
+    NumericError,
+)
+from .types import (
+    BlockLayout,
+    BlockMask,
+    FlopCount,
+    IclLayout,
+    IsaConfig,
+    IsaDims,
+    IsaRouting,
+    IsaTrace,
+    SelectionIndex,
+    SharpnessSplit,
+)
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # The operator entry points import torch; keep `import paper_2605_04569_b200`
+    # light for host-only consumers (types, errors, build).
+    if name in ("isa_forward", "isa_routing", "isa_forward_with_routing", "dense_attention", "prepare"):
+        from . import pipeline
+
+        return getattr(pipeline, name)
+    if name in ("isa_forward_sharded", "head_shard"):
+        from . import parallel
+
+        return getattr(parallel, name)
+    raise AttributeError(name)

@@ -1,0 +1,479 @@
+// Gathered-block attention on sm_100a (tcgen05 + TMEM + TMA, warp-specialised).
+//
+// One kernel body serves three hot-path branches of the ISA forward:
+//   MODE_DENSE  (K8)  dense non-causal attention, identity block tables.
+//                     Reference: full_attention (reference.py:79-123).
+//   MODE_EXACT  (K6)  the sharp query blocks over K_new = source blocks + the
+//                     selected context blocks, addressed through the per-head
+//                     block table (no K_new / gathered-Q materialisation).
+//                     Reference: gather_blocks + online_softmax_attention +
+//                     OnlineState (pipeline.py:338-343, reference.py:126-170).
+//   MODE_TAYLOR (K7)  the flat query blocks: online softmax over their exact
+//                     K_new blocks (union stream of the CTA's 4 query blocks,
+//                     per-(row-block, key-block) visibility bits) followed by
+//                     all K_new centroids with additive log2(valid_rows)
+//                     weights and -inf for the row block's own exact members.
+//                     Reference: taylor_sparse_forward/_head_state
+//                     (taylor.py:124-194), semantics SPEC.md:304.
+// The stage-5 scatter (pipeline.py:350-357) is fused: each output row is
+// written straight to its original token position.
+//
+// CTA = 4 query blocks of 64 rows = two 128-row Q tiles ("stages") sharing one
+// K/V tile stream (128 keys per tile = two 64-row key blocks).
+// Warp roles (384 threads):
+//   warps 0-3   softmax / rescale / epilogue for Q tile 0 (TMEM lanes 0-127)
+//   warps 4-7   same for Q tile 1
+//   warp  8     TMEM allocator + single-thread tcgen05.mma issuer
+//   warp  9     TMA producer (Q once, then the K/V ring)
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512);
+// P_s (bf16 pairs) overwrites the upper 64 columns of S_s.
+#pragma once
+#include "isa_ptx.cuh"
+
+namespace isa {
+
+enum AttnMode : int { MODE_DENSE = 0, MODE_EXACT = 1, MODE_TAYLOR = 2 };
+
+struct AttnParams {
+  int H;           // heads; bh = b*H + h
+  int l_src, l_ctx;
+  int t_src, t_ctx;
+  int t_new;       // K_new blocks (T for DENSE)
+  int n_qblk;      // query blocks per head in the list (n_sharp / n_flat / T)
+  float scale_log2;
+  const int* qlist;    // [BH][n_qblk] original query block ids (EXACT/TAYLOR)
+  const int* kv_blk;   // [BH][t_new] original block id of K_new block j (EXACT/TAYLOR)
+  // TAYLOR only
+  const int4* tiles;   // [BH][n_items][max_tiles] {kn0, kn1, bits0, bits1}
+  const int* n_tiles;  // [BH][n_items] exact tiles per item
+  int n_items;
+  int max_tiles;
+  const uint32_t* member_bits;  // [BH][n_qblk][W]
+  int W;
+  const float* clog2w;  // [BH][tn_pad]: log2(valid rows of K_new block j) or -inf
+  int tn_pad;           // centroid rows, multiple of 128
+  // output (token-major, D contiguous)
+  void* out;
+  int out_fp32;
+  long long o_sb, o_sh, o_ss;
+  int* err_flag;
+};
+
+constexpr int kThreads = 384;
+constexpr int kKvStages = 4;
+constexpr int kSoftmaxRegs = 208;
+constexpr int kOtherRegs = 96;
+
+template <int D>
+struct AttnSmem {
+  static constexpr int kPlanes = D / 64;
+  static constexpr int kTileBytes = 128 * D * 2;  // one 128-row bf16 tile
+  static constexpr int kQOff = 0;
+  static constexpr int kKvOff = 2 * kTileBytes;
+  static constexpr int kBarOff = kKvOff + kKvStages * kTileBytes;
+  static constexpr int kBytes = kBarOff + 256;
+  static constexpr int kAlloc = kBytes + 1024;  // slack for 1024-B alignment
+};
+
+__device__ __forceinline__ int blk_tok0(const AttnParams& p, int u) {
+  return u < p.t_src ? u * 64 : p.l_src + (u - p.t_src) * 64;
+}
+__device__ __forceinline__ int blk_valid(const AttnParams& p, int u) {
+  int r = u < p.t_src ? p.l_src - u * 64 : p.l_ctx - (u - p.t_src) * 64;
+  return r < 64 ? r : 64;
+}
+
+struct TileInfo {
+  int tok0, tok1;    // source rows (token index, or centroid row for centroid tiles)
+  int valid0, valid1;  // valid key rows in each 64-row half (0 = missing)
+  int bits0, bits1;    // TAYLOR: visibility bit per query block for each half
+  int centroid;        // 1 = centroid tile, index in [0, tn_pad/128)
+  int cidx;
+};
+
+template <int MODE>
+__device__ __forceinline__ int num_kv_tiles(const AttnParams& p, int bh, int item) {
+  if (MODE == MODE_TAYLOR) return p.n_tiles[bh * p.n_items + item] + p.tn_pad / 128;
+  return (p.t_new + 1) >> 1;
+}
+
+template <int MODE>
+__device__ __forceinline__ TileInfo kv_tile(const AttnParams& p, int bh, int item, int i) {
+  TileInfo t;
+  t.centroid = 0;
+  t.cidx = 0;
+  t.bits0 = t.bits1 = 0xF;
+  int kn0, kn1;
+  if (MODE == MODE_TAYLOR) {
+    const int ne = p.n_tiles[bh * p.n_items + item];
+    if (i >= ne) {
+      t.centroid = 1;
+      t.cidx = i - ne;
+      t.tok0 = t.cidx * 128;
+      t.tok1 = t.tok0 + 64;
+      t.valid0 = t.valid1 = 64;
+      return t;
+    }
+    const int4 e = p.tiles[((long long)bh * p.n_items + item) * p.max_tiles + i];
+    kn0 = e.x;
+    kn1 = e.y;
+    t.bits0 = e.z;
+    t.bits1 = e.w;
+  } else {
+    kn0 = 2 * i;
+    kn1 = 2 * i + 1 < p.t_new ? 2 * i + 1 : -1;
+  }
+  int u0 = kn0, u1 = kn1;
+  if (MODE != MODE_DENSE) {
+    const int* tab = p.kv_blk + (long long)bh * p.t_new;
+    u0 = tab[kn0];
+    u1 = kn1 >= 0 ? tab[kn1] : -1;
+  }
+  t.tok0 = blk_tok0(p, u0);
+  t.valid0 = blk_valid(p, u0);
+  if (u1 >= 0) {
+    t.tok1 = blk_tok0(p, u1);
+    t.valid1 = blk_valid(p, u1);
+  } else {  // missing half: reload block 0 (finite data), fully masked
+    t.tok1 = t.tok0;
+    t.valid1 = 0;
+    t.bits1 = 0;
+  }
+  return t;
+}
+
+template <int MODE>
+__device__ __forceinline__ int query_block(const AttnParams& p, int bh, int item, int q) {
+  const int pos = item * 4 + q;
+  if (pos >= p.n_qblk) return -1;
+  if (MODE == MODE_DENSE) return pos;
+  return p.qlist[(long long)bh * p.n_qblk + pos];
+}
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    gba_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
+                         const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
+  using L = AttnSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + L::kQOff;
+  uint8_t* sKV = smem + L::kKvOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* q_full = bars + 0;           // [2]
+  uint64_t* kv_full = bars + 2;          // [kKvStages]
+  uint64_t* kv_empty = bars + 2 + kKvStages;  // [kKvStages]
+  uint64_t* s_full = bars + 2 + 2 * kKvStages;     // [2]
+  uint64_t* p_full = bars + 4 + 2 * kKvStages;     // [2]
+  uint64_t* o_full = bars + 6 + 2 * kKvStages;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kKvStages);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int item = blockIdx.x;
+  const int bh = blockIdx.y;
+  const int n_kv = num_kv_tiles<MODE>(p, bh, item);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&q_full[0], 1);
+    mbar_init(&q_full[1], 1);
+    for (int s = 0; s < kKvStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 4);
+      mbar_init(&o_full[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 8) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= 8) {
+    setmaxnreg_dec<kOtherRegs>();
+    if (warp == 9 && lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      if (MODE == MODE_TAYLOR) {
+        tma_prefetch_desc(&tm_kc);
+        tma_prefetch_desc(&tm_vc);
+      }
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();
+      const int hh = bh % p.H, bb = bh / p.H;
+      int first_u = query_block<MODE>(p, bh, item, 0);
+      for (int s = 0; s < 2; ++s) {
+        mbar_arrive_expect_tx(&q_full[s], L::kTileBytes);
+        for (int half = 0; half < 2; ++half) {
+          int u = query_block<MODE>(p, bh, item, 2 * s + half);
+          if (u < 0) u = first_u;
+          const int tok = blk_tok0(p, u);
+          for (int pl = 0; pl < L::kPlanes; ++pl)
+            tma_load_4d(sQ + s * L::kTileBytes + pl * 16384 + half * 8192, &tm_q, &q_full[s], pl * 64, tok, hh, bb,
+                        pol_q);
+        }
+      }
+      for (int i = 0; i < n_kv; ++i) {
+        const TileInfo t = kv_tile<MODE>(p, bh, item, i);
+        for (int kv = 0; kv < 2; ++kv) {
+          const int c = 2 * i + kv;
+          const int slot = c % kKvStages;
+          const int use = c / kKvStages;
+          if (use > 0) mbar_wait(&kv_empty[slot], (use - 1) & 1);
+          mbar_arrive_expect_tx(&kv_full[slot], L::kTileBytes);
+          uint8_t* dst = sKV + slot * L::kTileBytes;
+          const CUtensorMap* tm;
+          int c2, c3;
+          if (t.centroid) {
+            tm = kv == 0 ? &tm_kc : &tm_vc;
+            c2 = bh;
+            c3 = 0;
+          } else {
+            tm = kv == 0 ? &tm_k : &tm_v;
+            c2 = hh;
+            c3 = bb;
+          }
+          for (int half = 0; half < 2; ++half) {
+            const int tok = half ? t.tok1 : t.tok0;
+            for (int pl = 0; pl < L::kPlanes; ++pl)
+              tma_load_4d(dst + pl * 16384 + half * 8192, tm, &kv_full[slot], pl * 64, tok, c2, c3, pol_kv);
+          }
+        }
+      }
+    } else if (warp == 8 && lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D, 0, 1);
+      const uint32_t sq = smem_u32(sQ);
+      const uint32_t skv = smem_u32(sKV);
+      auto issue_qk = [&](int s, int slot) {
+        const uint32_t a0 = sq + s * L::kTileBytes;
+        const uint32_t b0 = skv + slot * L::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tmem + s * 128, sdesc_sw128(a0 + off, 16, 1024), sdesc_sw128(b0 + off, 16, 1024), idesc_qk,
+                 kk > 0);
+        }
+      };
+      auto issue_pv = [&](int s, int slot, uint32_t acc) {
+        const uint32_t b0 = skv + slot * L::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          mma_ts(tmem + 256 + s * 128, tmem + s * 128 + 64 + kk * 8, sdesc_sw128(b0 + kk * 2048, 16384, 1024),
+                 idesc_pv, (acc | kk) != 0);
+        }
+      };
+      mbar_wait(&q_full[0], 0);
+      mbar_wait(&q_full[1], 0);
+      // tile 0: K_0
+      mbar_wait(&kv_full[0], 0);
+      tc_fence_after();
+      issue_qk(0, 0);
+      mma_commit(&s_full[0]);
+      issue_qk(1, 0);
+      mma_commit(&s_full[1]);
+      mma_commit(&kv_empty[0]);
+      for (int i = 1; i < n_kv; ++i) {
+        const int cv = 2 * i - 1, ck = 2 * i;
+        const int sv = cv % kKvStages, sk = ck % kKvStages;
+        mbar_wait(&kv_full[sv], (cv / kKvStages) & 1);
+        mbar_wait(&kv_full[sk], (ck / kKvStages) & 1);
+        for (int s = 0; s < 2; ++s) {
+          mbar_wait(&p_full[s], (i - 1) & 1);
+          tc_fence_after();
+          issue_pv(s, sv, i > 1);
+          issue_qk(s, sk);
+          mma_commit(&s_full[s]);
+        }
+        mma_commit(&kv_empty[sv]);
+        mma_commit(&kv_empty[sk]);
+      }
+      {
+        const int cv = 2 * n_kv - 1;
+        const int sv = cv % kKvStages;
+        mbar_wait(&kv_full[sv], (cv / kKvStages) & 1);
+        for (int s = 0; s < 2; ++s) {
+          mbar_wait(&p_full[s], (n_kv - 1) & 1);
+          tc_fence_after();
+          issue_pv(s, sv, n_kv > 1);
+          mma_commit(&o_full[s]);
+        }
+        mma_commit(&kv_empty[sv]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------------------------------- softmax
+    setmaxnreg_inc<kSoftmaxRegs>();
+    const int s = warp >> 2;                  // Q tile (stage)
+    const int row = (warp & 3) * 32 + lane;   // row in the 128-row tile == TMEM lane
+    const int qb = 2 * s + (row >> 6);        // query block 0..3 of this CTA
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t t_s = tmem + lane_base + s * 128;
+    const uint32_t t_p = t_s + 64;
+    const uint32_t t_o = tmem + lane_base + 256 + s * 128;
+    const float sl2 = p.scale_log2;
+    float m = -INFINITY;  // running max, log2 domain (already scaled)
+    float l = 0.f;
+    const uint32_t* mbits = nullptr;
+    const float* cw = nullptr;
+    if (MODE == MODE_TAYLOR) {
+      int pos = item * 4 + qb;
+      if (pos >= p.n_qblk) pos = item * 4;
+      mbits = p.member_bits + ((long long)bh * p.n_qblk + pos) * p.W;
+      cw = p.clog2w + (long long)bh * p.tn_pad;
+    }
+    for (int i = 0; i < n_kv; ++i) {
+      const TileInfo t = kv_tile<MODE>(p, bh, item, i);
+      mbar_wait(&s_full[s], i & 1);
+      tc_fence_after();
+      uint32_t sr[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, sr[c]);
+      tmem_ld_wait();
+      float* x = reinterpret_cast<float*>(&sr[0][0]);
+      const bool plain = !t.centroid && t.valid0 == 64 && t.valid1 == 64 &&
+                         (MODE != MODE_TAYLOR || (((t.bits0 & t.bits1) >> qb) & 1));
+      float mx[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+      if (plain) {  // raw scores; scaled inside the exp2 FMA below
+#pragma unroll
+        for (int c = 0; c < 128; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
+      } else if (!t.centroid) {
+        const int v0 = ((t.bits0 >> qb) & 1) ? t.valid0 : 0;
+        const int v1 = ((t.bits1 >> qb) & 1) ? t.valid1 : 0;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          const int lim = c < 64 ? v0 : v1;
+          x[c] = ((c & 63) < lim) ? x[c] * sl2 : -INFINITY;
+          mx[c & 7] = fmaxf(mx[c & 7], x[c]);
+        }
+      } else {
+        const uint32_t* wb = mbits + t.cidx * 4;
+        const float* wc = cw + t.cidx * 128;
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+          const uint32_t bits = __ldg(wb + w4);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int cc = w4 * 32 + c;
+            const float bias = __ldg(wc + cc);
+            x[cc] = ((bits >> c) & 1) ? -INFINITY : fmaf(x[cc], sl2, bias);
+            mx[cc & 7] = fmaxf(mx[cc & 7], x[cc]);
+          }
+        }
+      }
+      float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      if (plain) mt *= sl2;
+      // running max with lazy rescale (threshold 8 in log2 units)
+      float m_new = fmaxf(m, mt);
+      float o_scale = 1.f;
+      bool need = false;
+      if (i == 0) {
+        m = m_new;
+      } else if (m_new > m + 8.f) {
+        o_scale = ex2_approx(m - m_new);  // m == -inf -> 0 (O and l are 0 then)
+        need = true;
+        m = m_new;
+      }
+      if (__any_sync(0xffffffffu, need)) {
+        l *= o_scale;
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t orr[32];
+          tmem_ld32(t_o + c * 32, orr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) orr[j] = __float_as_uint(__uint_as_float(orr[j]) * o_scale);
+          tmem_st32(t_o + c * 32, orr);
+        }
+      }
+      const float mu = (m == -INFINITY) ? 0.f : m;
+      float sm[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sm[j] = 0.f;
+      uint32_t pk[2][32];
+      if (plain) {
+        const float nmu = -mu;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const float p0 = ex2_approx(fmaf(x[2 * c], sl2, nmu));
+          const float p1 = ex2_approx(fmaf(x[2 * c + 1], sl2, nmu));
+          sm[c & 7] += p0 + p1;
+          pk[c >> 5][c & 31] = pack_bf16x2(p0, p1);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const float p0 = ex2_approx(x[2 * c] - mu);
+          const float p1 = ex2_approx(x[2 * c + 1] - mu);
+          sm[c & 7] += p0 + p1;
+          pk[c >> 5][c & 31] = pack_bf16x2(p0, p1);
+        }
+      }
+      const float sum = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
+      tmem_st32(t_p, pk[0]);
+      tmem_st32(t_p + 32, pk[1]);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[s]);
+      l += sum;
+    }
+    // -------------------------------------------------------------- epilogue
+    mbar_wait(&o_full[s], 0);
+    tc_fence_after();
+    const int u = query_block<MODE>(p, bh, item, qb);
+    const int rr = row & 63;
+    const bool write = u >= 0 && rr < blk_valid(p, u);
+    if (write && !(l > 0.f) && p.err_flag) atomicOr(p.err_flag, 1);
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const int hh = bh % p.H, bb = bh / p.H;
+    const long long obase =
+        bb * p.o_sb + hh * p.o_sh + (long long)(write ? blk_tok0(p, u) + rr : 0) * p.o_ss;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t orr[32];
+      tmem_ld32(t_o + c * 32, orr);
+      tmem_ld_wait();
+      if (write) {
+        if (p.out_fp32) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + obase + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(orr[4 * j]) * inv, __uint_as_float(orr[4 * j + 1]) * inv,
+                                 __uint_as_float(orr[4 * j + 2]) * inv, __uint_as_float(orr[4 * j + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + obase + c * 32);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(orr[8 * j + 0]) * inv, __uint_as_float(orr[8 * j + 1]) * inv);
+            w.y = pack_bf16x2(__uint_as_float(orr[8 * j + 2]) * inv, __uint_as_float(orr[8 * j + 3]) * inv);
+            w.z = pack_bf16x2(__uint_as_float(orr[8 * j + 4]) * inv, __uint_as_float(orr[8 * j + 5]) * inv);
+            w.w = pack_bf16x2(__uint_as_float(orr[8 * j + 6]) * inv, __uint_as_float(orr[8 * j + 7]) * inv);
+            dst[j] = w;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace isa

@@ -1,0 +1,594 @@
+// C ABI and native orchestration of the ISA forward on sm_100a.
+//
+// isa_forward runs the five reference stages (pipeline.py:133-370) as one
+// stream-ordered sequence of kernels with no host synchronisation:
+//   stage 1 "coarse"  K1 pool_means, K2a coarse_src (fp64 S over source
+//                     columns), K2b ctx_score                pipeline.py:176-184
+//   stage 2 "select"  K3 topk_rank (context), K_new block table, bf16 K_new
+//                     centroids + log2 weights              pipeline.py:186-212
+//   stage 3 "split"   K4a sharpness, K4b split, K5 block mask, Taylor plan
+//                                                            pipeline.py:214-228
+//   stage 4 "kernel"  K6 exact (sharp) and K7 Taylor (flat) tcgen05 attention,
+//                     stage-5 scatter fused into their epilogues
+//                                                            pipeline.py:331-358
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/isa_b200.h"
+#include "isa_attn.cuh"
+#include "isa_route.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define ISA_CUDA(call)                                                                         \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) return fail(ISA_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define ISA_LAUNCHED(name)                                                                             \
+  do {                                                                                                 \
+    cudaError_t e_ = cudaGetLastError();                                                               \
+    if (e_ != cudaSuccess) return fail(ISA_ERR_CUDA, "launch %s: %s", name, cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------- TMA maps
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// bf16 4-D map {D, d1, d2, d3} with byte strides s1..s3; box {64, 64, 1, 1}, 128B swizzle.
+int make_map(CUtensorMap* m, const void* ptr, int D, long long d1, long long d2, long long d3, long long s1,
+             long long s2, long long s3) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return fail(ISA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (s1 & 15) || (s2 & 15) || (s3 & 15))
+    return fail(ISA_ERR_LAYOUT, "TMA needs 16-byte aligned base and strides (got strides %lld,%lld,%lld bytes)",
+                s1, s2, s3);
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)d1, (cuuint64_t)d2, (cuuint64_t)d3};
+  cuuint64_t strides[3] = {(cuuint64_t)s1, (cuuint64_t)s2, (cuuint64_t)s3};
+  cuuint32_t box[4] = {64, 64, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ISA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ISA_OK;
+}
+
+// ---------------------------------------------------------------- geometry
+struct Dims {
+  int B, H, S, D, BH;
+  int l_src, l_ctx, t_src, t_ctx, T;
+  int k_ctx, t_new, n_flat, n_sharp, k;
+  int tn_pad, W, items_s, items_f, max_tiles;
+  double scale;
+};
+
+int derive(const IsaShape* sh, const IsaKnobs* kn, Dims* d) {
+  if (!sh || !kn) return fail(ISA_ERR_CONFIG, "null shape/knobs");
+  if (sh->block != 64) return fail(ISA_ERR_CONFIG, "block_size=%d not supported (only 64)", sh->block);
+  if (sh->head_dim != 64 && sh->head_dim != 128)
+    return fail(ISA_ERR_CONFIG, "head_dim=%d not supported (64 or 128)", sh->head_dim);
+  if (sh->batch < 1 || sh->heads < 1 || sh->seq_len < 1)
+    return fail(ISA_ERR_LAYOUT, "all dims must be >= 1");
+  if (sh->l_src < 1 || sh->l_ctx < 0) return fail(ISA_ERR_LAYOUT, "l_src must be >= 1 and l_ctx >= 0");
+  if (sh->l_src + sh->l_ctx != sh->seq_len)
+    return fail(ISA_ERR_LAYOUT, "sequence length %d != icl total %d", sh->seq_len, sh->l_src + sh->l_ctx);
+  if (sh->dtype != ISA_DTYPE_BF16 && sh->dtype != ISA_DTYPE_F32) return fail(ISA_ERR_CONFIG, "bad dtype");
+  if (!(kn->scale > 0.0)) return fail(ISA_ERR_CONFIG, "scale must be > 0");
+  d->B = sh->batch;
+  d->H = sh->heads;
+  d->S = sh->seq_len;
+  d->D = sh->head_dim;
+  d->BH = d->B * d->H;
+  d->l_src = sh->l_src;
+  d->l_ctx = sh->l_ctx;
+  d->t_src = (sh->l_src + 63) / 64;
+  d->t_ctx = (sh->l_ctx + 63) / 64;
+  d->T = d->t_src + d->t_ctx;
+  d->k_ctx = kn->k_ctx;
+  if (d->k_ctx < 0 || d->k_ctx > d->t_ctx) return fail(ISA_ERR_CONFIG, "k_ctx=%d out of [0, %d]", d->k_ctx, d->t_ctx);
+  d->t_new = d->t_src + d->k_ctx;
+  d->n_flat = kn->n_flat;
+  if (d->n_flat < 0 || d->n_flat > d->T) return fail(ISA_ERR_CONFIG, "n_flat=%d out of [0, %d]", d->n_flat, d->T);
+  d->n_sharp = d->T - d->n_flat;
+  d->k = d->n_flat ? kn->k_mask : 0;
+  if (d->n_flat && (d->k < 1 || d->k > d->t_new))
+    return fail(ISA_ERR_CONFIG, "k_mask=%d out of [1, %d]", d->k, d->t_new);
+  d->tn_pad = ((d->t_new + 127) / 128) * 128;
+  d->W = d->tn_pad / 32;
+  d->items_s = (d->n_sharp + 3) / 4;
+  d->items_f = (d->n_flat + 3) / 4;
+  int u = 4 * d->k < d->t_new ? 4 * d->k : d->t_new;
+  d->max_tiles = (u + 1) / 2;
+  if (d->max_tiles < 1) d->max_tiles = 1;
+  d->scale = kn->scale;
+  return ISA_OK;
+}
+
+struct Workspace {
+  int32_t* err;
+  float* means;  // [3][BH][T][D]
+  __nv_bfloat16* bf;  // [3][BH][S][D] (fp32 inputs only)
+  double* s_src;      // [BH][T][t_src]
+  double* ctx;        // [BH][t_ctx]
+  int* sel;           // [BH][k_ctx]
+  int* kv_blk;        // [BH][t_new]
+  double* sharpness;  // [BH][T]
+  int* sharp;         // [BH][n_sharp]
+  int* flat;          // [BH][n_flat]
+  int* mask;          // [BH][n_flat][k]
+  uint32_t* bits;     // [BH][n_flat][W]
+  __nv_bfloat16* kc_bf;  // [BH][tn_pad][D]
+  __nv_bfloat16* vc_bf;
+  float* clog2w;      // [BH][tn_pad]
+  int4* tiles;        // [BH][items_f][max_tiles]
+  int* n_tiles;       // [BH][items_f]
+  size_t bytes;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+Workspace carve(const Dims& d, int dtype, uint8_t* base) {
+  Workspace w{};
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    uint8_t* p = base ? base + off : nullptr;
+    off += align256(n ? n : 1);
+    return p;
+  };
+  const long long BH = d.BH;
+  w.err = reinterpret_cast<int32_t*>(take(16));
+  w.means = reinterpret_cast<float*>(take(3ull * BH * d.T * d.D * 4));
+  w.bf = dtype == ISA_DTYPE_F32 ? reinterpret_cast<__nv_bfloat16*>(take(3ull * BH * d.S * d.D * 2)) : nullptr;
+  w.s_src = reinterpret_cast<double*>(take(8ull * BH * d.T * d.t_src));
+  w.ctx = reinterpret_cast<double*>(take(8ull * BH * d.t_ctx));
+  w.sel = reinterpret_cast<int*>(take(4ull * BH * d.k_ctx));
+  w.kv_blk = reinterpret_cast<int*>(take(4ull * BH * d.t_new));
+  w.sharpness = reinterpret_cast<double*>(take(8ull * BH * d.T));
+  w.sharp = reinterpret_cast<int*>(take(4ull * BH * d.n_sharp));
+  w.flat = reinterpret_cast<int*>(take(4ull * BH * d.n_flat));
+  w.mask = reinterpret_cast<int*>(take(4ull * BH * d.n_flat * d.k));
+  w.bits = reinterpret_cast<uint32_t*>(take(4ull * BH * d.n_flat * d.W));
+  w.kc_bf = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.tn_pad * d.D));
+  w.vc_bf = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.tn_pad * d.D));
+  w.clog2w = reinterpret_cast<float*>(take(4ull * BH * d.tn_pad));
+  w.tiles = reinterpret_cast<int4*>(take(16ull * BH * d.items_f * d.max_tiles));
+  w.n_tiles = reinterpret_cast<int*>(take(4ull * BH * d.items_f));
+  w.bytes = off;
+  return w;
+}
+
+unsigned grid1d(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  return static_cast<unsigned>(g < 1 ? 1 : (g > 65535 * 16 ? 65535 * 16 : g));
+}
+
+template <int D, int MODE>
+int launch_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
+                     const CUtensorMap& tvc, const isa::AttnParams& p, int items, int BH, cudaStream_t st) {
+  using L = isa::AttnSmem<D>;
+  static bool configured = false;
+  if (!configured) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::gba_attention_kernel<D, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  L::kAlloc));
+    configured = true;
+  }
+  if (items < 1) return ISA_OK;
+  dim3 grid(items, BH);
+  isa::gba_attention_kernel<D, MODE><<<grid, isa::kThreads, L::kAlloc, st>>>(tq, tk, tv, tkc, tvc, p);
+  ISA_LAUNCHED("gba_attention_kernel");
+  return ISA_OK;
+}
+
+template <int MODE>
+int launch_attention_d(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                       const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& p, int items, int BH,
+                       cudaStream_t st) {
+  if (D == 128) return launch_attention<128, MODE>(tq, tk, tv, tkc, tvc, p, items, BH, st);
+  return launch_attention<64, MODE>(tq, tk, tv, tkc, tvc, p, items, BH, st);
+}
+
+// Q/K/V TMA maps (bf16): either the caller's tensors (with strides) or the workspace bf16 copy.
+int qkv_maps(const IsaShape* sh, const Dims& d, const void* q, const void* k, const void* v, const Workspace& w,
+             CUtensorMap* tq, CUtensorMap* tk, CUtensorMap* tv) {
+  const void* ptr[3] = {q, k, v};
+  CUtensorMap* maps[3] = {tq, tk, tv};
+  for (int i = 0; i < 3; ++i) {
+    int rc;
+    if (sh->dtype == ISA_DTYPE_BF16) {
+      rc = make_map(maps[i], ptr[i], d.D, d.S, d.H, d.B, sh->stride_s * 2, sh->stride_h * 2, sh->stride_b * 2);
+    } else {
+      const __nv_bfloat16* base = w.bf + (long long)i * d.BH * d.S * d.D;
+      rc = make_map(maps[i], base, d.D, d.S, d.H, d.B, (long long)d.D * 2, (long long)d.S * d.D * 2,
+                    (long long)d.H * d.S * d.D * 2);
+    }
+    if (rc) return rc;
+  }
+  return ISA_OK;
+}
+
+int check_io(const IsaShape* sh, const void* q, const void* k, const void* v) {
+  if (!q || !k || !v) return fail(ISA_ERR_LAYOUT, "null q/k/v");
+  const int elem = sh->dtype == ISA_DTYPE_BF16 ? 2 : 4;
+  for (const void* p : {q, k, v})
+    if (reinterpret_cast<uintptr_t>(p) & 15) return fail(ISA_ERR_LAYOUT, "q/k/v must be 16-byte aligned");
+  const long long st[3] = {sh->stride_b, sh->stride_h, sh->stride_s};
+  for (long long s : st)
+    if ((s * elem) & 15) return fail(ISA_ERR_LAYOUT, "q/k/v strides must be multiples of 16 bytes");
+  return ISA_OK;
+}
+
+void record(const IsaEvents* ev, int i, cudaStream_t st) {
+  if (ev && ev->ev[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev->ev[i]), st);
+}
+
+int run_pool(const IsaShape* sh, const Dims& d, const void* q, const void* k, const void* v, float* means,
+             __nv_bfloat16* bf, int32_t* err, cudaStream_t st) {
+  isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};
+  dim3 grid(d.T, d.BH, 3);
+  if (sh->dtype == ISA_DTYPE_BF16) {
+    auto* qq = static_cast<const __nv_bfloat16*>(q);
+    auto* kk = static_cast<const __nv_bfloat16*>(k);
+    auto* vv = static_cast<const __nv_bfloat16*>(v);
+    if (d.D == 128)
+      isa::pool_means_kernel<__nv_bfloat16, 128><<<grid, 256, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h,
+                                                                       sh->stride_s, d.H, seg, d.T, means, nullptr,
+                                                                       d.S, err);
+    else
+      isa::pool_means_kernel<__nv_bfloat16, 64><<<grid, 256, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h,
+                                                                      sh->stride_s, d.H, seg, d.T, means, nullptr,
+                                                                      d.S, err);
+  } else {
+    auto* qq = static_cast<const float*>(q);
+    auto* kk = static_cast<const float*>(k);
+    auto* vv = static_cast<const float*>(v);
+    if (d.D == 128)
+      isa::pool_means_kernel<float, 128><<<grid, 256, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h, sh->stride_s,
+                                                               d.H, seg, d.T, means, bf, d.S, err);
+    else
+      isa::pool_means_kernel<float, 64><<<grid, 256, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h, sh->stride_s,
+                                                              d.H, seg, d.T, means, bf, d.S, err);
+  }
+  ISA_LAUNCHED("pool_means_kernel");
+  return ISA_OK;
+}
+
+size_t rank_smem(int n) { return (size_t)n * (8 + 4 + 1) + 16; }
+
+int set_rank_smem(size_t bytes) {
+  static size_t cur_topk = 48 * 1024, cur_split = 48 * 1024, cur_mask = 48 * 1024;
+  (void)cur_mask;
+  if (bytes > cur_topk) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::topk_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur_topk = bytes;
+  }
+  if (bytes > cur_split) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur_split = bytes;
+  }
+  return ISA_OK;
+}
+
+int set_mask_smem(size_t bytes) {
+  static size_t cur = 48 * 1024;
+  if (bytes > cur) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::block_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
+  }
+  return ISA_OK;
+}
+
+// Stages 1-3 (+ routing export). Leaves sel/kv_blk/sharp/flat/mask/bits/centroids in the workspace.
+int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const void* q, const void* k, const void* v,
+                const Workspace& w, const IsaRoutingIn* pinned, IsaRoutingOut* ro, int32_t* err,
+                const IsaEvents* ev, cudaStream_t st) {
+  int rc;
+  const long long BH = d.BH;
+  float* qc = w.means;
+  float* kc = w.means + BH * d.T * d.D;
+  float* vc = w.means + 2 * BH * d.T * d.D;
+  // ---- stage 1: coarse
+  if ((rc = run_pool(sh, d, q, k, v, w.means, w.bf, err, st))) return rc;
+  const bool need_scores = !pinned;
+  if (need_scores) {
+    dim3 g((d.t_src + 63) / 64, (d.T + 63) / 64, d.BH);
+    isa::coarse_src_kernel<<<g, 256, 0, st>>>(qc, kc, d.T, d.t_src, d.D, d.scale, w.s_src);
+    ISA_LAUNCHED("coarse_src_kernel");
+    if (d.t_ctx) {
+      isa::ctx_score_kernel<<<d.BH, 256, d.D * sizeof(double), st>>>(qc, kc, d.T, d.t_src, d.t_ctx, d.D, d.scale,
+                                                                      w.ctx);
+      ISA_LAUNCHED("ctx_score_kernel");
+    }
+  }
+  record(ev, 1, st);
+  // ---- stage 2: select
+  if (pinned) {
+    if (d.k_ctx) {
+      if (!pinned->selection) return fail(ISA_ERR_CONTRACT, "pinned routing lacks selection");
+      isa::narrow_kernel<<<grid1d(BH * d.k_ctx, 256), 256, 0, st>>>(pinned->selection, w.sel, BH * d.k_ctx);
+      ISA_LAUNCHED("narrow_kernel");
+    }
+  } else if (d.k_ctx) {
+    size_t sm = rank_smem(d.t_ctx);
+    if ((rc = set_rank_smem(sm))) return rc;
+    isa::topk_rank_kernel<<<d.BH, 1024, sm, st>>>(w.ctx, d.t_ctx, d.k_ctx, w.sel, ro ? ro->selection : nullptr);
+    ISA_LAUNCHED("topk_rank_kernel");
+  }
+  isa::kvblk_from_sel_kernel<<<d.BH, 256, 0, st>>>(w.sel, d.t_src, d.k_ctx, w.kv_blk);
+  ISA_LAUNCHED("kvblk_from_sel_kernel");
+  if (d.n_flat) {
+    isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};
+    isa::centroid_kernel<<<dim3(d.tn_pad, d.BH), d.D, 0, st>>>(kc, vc, w.kv_blk, d.T, d.t_new, d.tn_pad, d.D, seg,
+                                                                w.kc_bf, w.vc_bf, w.clog2w);
+    ISA_LAUNCHED("centroid_kernel");
+  }
+  if (ro && ro->ctx_scores && need_scores && d.t_ctx)
+    ISA_CUDA(cudaMemcpyAsync(ro->ctx_scores, w.ctx, 8ull * BH * d.t_ctx, cudaMemcpyDeviceToDevice, st));
+  if (ro && ro->selection && pinned && d.k_ctx)
+    ISA_CUDA(cudaMemcpyAsync(ro->selection, pinned->selection, 8ull * BH * d.k_ctx, cudaMemcpyDeviceToDevice, st));
+  record(ev, 2, st);
+  // ---- stage 3: split + block mask
+  if (pinned) {
+    if (!pinned->sharp || (d.n_flat && !pinned->flat)) return fail(ISA_ERR_CONTRACT, "pinned routing lacks split");
+    if (d.n_sharp) {
+      isa::narrow_kernel<<<grid1d(BH * d.n_sharp, 256), 256, 0, st>>>(pinned->sharp, w.sharp, BH * d.n_sharp);
+      ISA_LAUNCHED("narrow_kernel");
+    }
+    if (d.n_flat) {
+      if (!pinned->mask) return fail(ISA_ERR_CONTRACT, "pinned routing lacks mask");
+      isa::narrow_kernel<<<grid1d(BH * d.n_flat, 256), 256, 0, st>>>(pinned->flat, w.flat, BH * d.n_flat);
+      isa::narrow_kernel<<<grid1d(BH * d.n_flat * d.k, 256), 256, 0, st>>>(pinned->mask, w.mask,
+                                                                         BH * d.n_flat * d.k);
+      isa::bits_from_mask_kernel<<<BH * d.n_flat, 128, 0, st>>>(w.mask, d.k, d.W, w.bits);
+      ISA_LAUNCHED("bits_from_mask_kernel");
+    }
+  } else {
+    isa::sharpness_kernel<<<(unsigned)((BH * d.T + 7) / 8), 256, 0, st>>>(w.s_src, (int)(BH * d.T), d.t_src,
+                                                                          kn->softmax_first, w.sharpness);
+    ISA_LAUNCHED("sharpness_kernel");
+    size_t sm = rank_smem(d.T);
+    if ((rc = set_rank_smem(sm))) return rc;
+    isa::split_kernel<<<d.BH, 1024, sm, st>>>(w.sharpness, d.T, d.n_flat, w.sharp, w.flat, ro ? ro->sharp : nullptr,
+                                              ro ? ro->flat : nullptr);
+    ISA_LAUNCHED("split_kernel");
+    if (ro && ro->sharpness)
+      ISA_CUDA(cudaMemcpyAsync(ro->sharpness, w.sharpness, 8ull * BH * d.T, cudaMemcpyDeviceToDevice, st));
+    if (d.n_flat) {
+      size_t sm2 = 4 * ((size_t)d.t_new * 8 + (size_t)d.W * 4);
+      if ((rc = set_mask_smem(sm2))) return rc;
+      const int rows = (int)(BH * d.n_flat);
+      isa::block_mask_kernel<<<(rows + 3) / 4, 128, sm2, st>>>(
+          nullptr, rows, w.s_src, qc, kc, w.flat, w.kv_blk, d.T, d.t_src, d.n_flat, d.D, d.scale, d.t_new, d.k,
+          d.W, w.mask, ro ? ro->mask : nullptr, w.bits);
+      ISA_LAUNCHED("block_mask_kernel");
+    }
+  }
+  if (pinned && ro) {
+    if (ro->sharp && d.n_sharp)
+      ISA_CUDA(cudaMemcpyAsync(ro->sharp, pinned->sharp, 8ull * BH * d.n_sharp, cudaMemcpyDeviceToDevice, st));
+    if (ro->flat && d.n_flat)
+      ISA_CUDA(cudaMemcpyAsync(ro->flat, pinned->flat, 8ull * BH * d.n_flat, cudaMemcpyDeviceToDevice, st));
+    if (ro->mask && d.n_flat)
+      ISA_CUDA(cudaMemcpyAsync(ro->mask, pinned->mask, 8ull * BH * d.n_flat * d.k, cudaMemcpyDeviceToDevice, st));
+  }
+  if (d.n_flat) {
+    isa::taylor_plan_kernel<<<dim3(d.items_f, d.BH), 32, 0, st>>>(w.bits, d.n_flat, d.W, d.items_f, d.max_tiles,
+                                                                   w.tiles, w.n_tiles);
+    ISA_LAUNCHED("taylor_plan_kernel");
+  }
+  record(ev, 3, st);
+  return ISA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int isa_abi_version(void) { return ISA_ABI_VERSION; }
+
+const char* isa_last_error(void) { return g_last_error.c_str(); }
+
+int isa_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* bytes) {
+  Dims d;
+  int rc = derive(shape, knobs, &d);
+  if (rc) return rc;
+  if (!bytes) return fail(ISA_ERR_CONFIG, "null bytes");
+  *bytes = carve(d, shape->dtype, nullptr).bytes;
+  return ISA_OK;
+}
+
+int isa_routing(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
+                void* workspace, size_t workspace_bytes, IsaRoutingOut* routing, int32_t* err_word, void* stream) {
+  Dims d;
+  int rc = derive(shape, knobs, &d);
+  if (rc) return rc;
+  if ((rc = check_io(shape, q, k, v))) return rc;
+  Workspace w = carve(d, shape->dtype, static_cast<uint8_t*>(workspace));
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, w.bytes);
+  return run_routing(shape, d, knobs, q, k, v, w, nullptr, routing, err_word, nullptr,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v, void* out,
+                void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
+                int32_t* err_word, const IsaEvents* events, void* stream) {
+  Dims d;
+  int rc = derive(shape, knobs, &d);
+  if (rc) return rc;
+  if ((rc = check_io(shape, q, k, v))) return rc;
+  if (!out || (reinterpret_cast<uintptr_t>(out) & 15)) return fail(ISA_ERR_LAYOUT, "out must be 16-byte aligned");
+  Workspace w = carve(d, shape->dtype, static_cast<uint8_t*>(workspace));
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, w.bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  record(events, 0, st);
+  if ((rc = run_routing(shape, d, knobs, q, k, v, w, pinned, routing, err_word, events, st))) return rc;
+  // ---- stage 4 (+ fused stage 5)
+  CUtensorMap tq, tk, tv, tkc, tvc;
+  if ((rc = qkv_maps(shape, d, q, k, v, w, &tq, &tk, &tv))) return rc;
+  isa::AttnParams p{};
+  p.H = d.H;
+  p.l_src = d.l_src;
+  p.l_ctx = d.l_ctx;
+  p.t_src = d.t_src;
+  p.t_ctx = d.t_ctx;
+  p.t_new = d.t_new;
+  p.scale_log2 = static_cast<float>(d.scale * 1.4426950408889634);
+  p.kv_blk = w.kv_blk;
+  p.out = out;
+  p.out_fp32 = shape->dtype == ISA_DTYPE_F32;
+  p.o_sh = (long long)d.S * d.D;
+  p.o_sb = (long long)d.H * d.S * d.D;
+  p.o_ss = d.D;
+  p.err_flag = err_word;
+  if (d.n_sharp) {
+    isa::AttnParams ps = p;
+    ps.n_qblk = d.n_sharp;
+    ps.qlist = w.sharp;
+    if ((rc = launch_attention_d<isa::MODE_EXACT>(d.D, tq, tk, tv, tq, tq, ps, d.items_s, d.BH, st))) return rc;
+  }
+  if (d.n_flat) {
+    if ((rc = make_map(&tkc, w.kc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
+                       (long long)d.BH * d.tn_pad * d.D * 2)))
+      return rc;
+    if ((rc = make_map(&tvc, w.vc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
+                       (long long)d.BH * d.tn_pad * d.D * 2)))
+      return rc;
+    isa::AttnParams pf = p;
+    pf.n_qblk = d.n_flat;
+    pf.qlist = w.flat;
+    pf.tiles = w.tiles;
+    pf.n_tiles = w.n_tiles;
+    pf.n_items = d.items_f;
+    pf.max_tiles = d.max_tiles;
+    pf.member_bits = w.bits;
+    pf.W = d.W;
+    pf.clog2w = w.clog2w;
+    pf.tn_pad = d.tn_pad;
+    if ((rc = launch_attention_d<isa::MODE_TAYLOR>(d.D, tq, tk, tv, tkc, tvc, pf, d.items_f, d.BH, st))) return rc;
+  }
+  record(events, 4, st);
+  return ISA_OK;
+}
+
+int isa_dense_attention(const IsaShape* shape, double scale, const void* q, const void* k, const void* v, void* out,
+                        void* stream) {
+  IsaKnobs kn{scale, 0, 0, 1, 1, 0};
+  Dims d;
+  int rc = derive(shape, &kn, &d);
+  if (rc) return rc;
+  if (shape->dtype != ISA_DTYPE_BF16) return fail(ISA_ERR_CONFIG, "dense attention takes bf16 inputs");
+  if ((rc = check_io(shape, q, k, v))) return rc;
+  Workspace w{};
+  CUtensorMap tq, tk, tv;
+  if ((rc = qkv_maps(shape, d, q, k, v, w, &tq, &tk, &tv))) return rc;
+  isa::AttnParams p{};
+  p.H = d.H;
+  p.l_src = d.l_src;
+  p.l_ctx = d.l_ctx;
+  p.t_src = d.t_src;
+  p.t_ctx = d.t_ctx;
+  p.t_new = d.T;
+  p.n_qblk = d.T;
+  p.scale_log2 = static_cast<float>(scale * 1.4426950408889634);
+  p.out = out;
+  p.out_fp32 = 0;
+  p.o_sh = (long long)d.S * d.D;
+  p.o_sb = (long long)d.H * d.S * d.D;
+  p.o_ss = d.D;
+  return launch_attention_d<isa::MODE_DENSE>(d.D, tq, tk, tv, tq, tq, p, (d.T + 3) / 4, d.BH,
+                                             static_cast<cudaStream_t>(stream));
+}
+
+int isa_pool_means(const IsaShape* shape, const void* q, const void* k, const void* v, float* means,
+                   int32_t* err_word, void* stream) {
+  IsaKnobs kn{1.0, 0, 0, 1, 1, 0};
+  Dims d;
+  int rc = derive(shape, &kn, &d);
+  if (rc) return rc;
+  if ((rc = check_io(shape, q, k, v))) return rc;
+  return run_pool(shape, d, q, k, v, means, nullptr, err_word, static_cast<cudaStream_t>(stream));
+}
+
+int isa_topk_rows_f64(const double* scores, int32_t rows, int32_t n, int32_t k, int64_t* out_idx, int32_t method,
+                      void* stream) {
+  if (rows < 0 || n < 1 || k < 0 || k > n) return fail(ISA_ERR_CONFIG, "bad topk geometry");
+  if (rows == 0 || k == 0) return ISA_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc;
+  if (method == 0) {
+    size_t sm = rank_smem(n);
+    if ((rc = set_rank_smem(sm))) return rc;
+    isa::topk_rank_kernel<<<rows, 1024, sm, st>>>(scores, n, k, nullptr, out_idx);
+    ISA_LAUNCHED("topk_rank_kernel");
+  } else {
+    const int W = (n + 31) / 32;
+    size_t sm2 = 4 * ((size_t)n * 8 + (size_t)W * 4);
+    if ((rc = set_mask_smem(sm2))) return rc;
+    isa::block_mask_kernel<<<(rows + 3) / 4, 128, sm2, st>>>(scores, rows, nullptr, nullptr, nullptr, nullptr,
+                                                              nullptr, 0, 0, 1, 0, 1.0, n, k, W, nullptr,
+                                                              out_idx, nullptr);
+    ISA_LAUNCHED("block_mask_kernel");
+  }
+  return ISA_OK;
+}
+
+int isa_sharpness_rows_f64(const double* s, int32_t rows, int32_t n, int32_t softmax_first, double* out,
+                           void* stream) {
+  if (rows < 0 || n < 1) return fail(ISA_ERR_CONFIG, "bad sharpness geometry");
+  if (rows == 0) return ISA_OK;
+  isa::sharpness_kernel<<<(rows + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(s, rows, n, softmax_first,
+                                                                                      out);
+  ISA_LAUNCHED("sharpness_kernel");
+  return ISA_OK;
+}
+
+int isa_split_rows_f64(const double* m, int32_t rows, int32_t n, int32_t n_flat, int64_t* sharp, int64_t* flat,
+                       void* stream) {
+  if (rows < 0 || n < 1 || n_flat < 0 || n_flat > n) return fail(ISA_ERR_CONFIG, "bad split geometry");
+  if (rows == 0) return ISA_OK;
+  int rc;
+  size_t sm = rank_smem(n);
+  if ((rc = set_rank_smem(sm))) return rc;
+  isa::split_kernel<<<rows, 1024, sm, static_cast<cudaStream_t>(stream)>>>(
+      m, n, n_flat, nullptr, nullptr, sharp, flat);
+  ISA_LAUNCHED("split_kernel");
+  return ISA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,317 @@
+"""The ISA forward operator on B200 — drop-in for the reference pipeline API.
+
+Public functions keep the reference signatures (pkg/src/isattn/pipeline.py):
+
+    isa_forward(q, k, v, icl, cfg, collect_trace=True) -> (out, IsaTrace | None)   :307-316
+    isa_routing(q, k, v, icl, cfg) -> IsaRouting                                   :302-304
+    isa_forward_with_routing(q, k, v, icl, cfg, routing) -> out                    :319-328
+
+plus `dense_attention` (the full_attention oracle / dense baseline,
+reference.py:79-123) on the same sm_100a kernel.
+
+Inputs may be torch CUDA tensors (bf16 or fp32; any B/H/S strides with a
+contiguous D axis) or numpy arrays (copied to the current CUDA device; the
+result is returned as a numpy float32 array, like the reference). All compute
+runs in libisa_b200.so; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError, DegenerateRowError, InputError, LayoutError
+from .types import (
+    BlockMask,
+    IclLayout,
+    IsaConfig,
+    IsaDims,
+    IsaRouting,
+    IsaTrace,
+    SelectionIndex,
+    SharpnessSplit,
+    SUPPORTED_HEAD_DIMS,
+    _LazyStageTimes,
+    cfg_from_any,
+    icl_from_any,
+)
+
+__all__ = ["isa_forward", "isa_routing", "isa_forward_with_routing", "dense_attention", "prepare"]
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class _Inputs:
+    """Validated device views of q/k/v plus the ABI descriptors (pipeline.py:136-154)."""
+
+    def __init__(self, q, k, v, icl, cfg):
+        self.cfg = cfg_from_any(cfg).validate_b200()
+        self.icl = icl_from_any(icl)
+        self.numpy_io = isinstance(q, np.ndarray)
+        q, k, v = (self._to_device(x, n) for x, n in ((q, "Q"), (k, "K"), (v, "V")))
+        if not (q.shape == k.shape == v.shape):
+            raise LayoutError(f"Q/K/V must share one shape, got {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+        if q.stride() != k.stride() or q.stride() != v.stride() or q.dtype != k.dtype or q.dtype != v.dtype:
+            k, v = (x.contiguous() if x.stride() != q.stride() else x for x in (k, v))
+            q = q.contiguous()
+            k, v = k.contiguous().to(q.dtype), v.contiguous().to(q.dtype)
+        if q.shape[2] != self.icl.total:
+            raise LayoutError(f"sequence length {q.shape[2]} != icl total {self.icl.total}")
+        b = self.cfg.block_size
+        if self.cfg.strict and (self.icl.l_src % b or self.icl.l_ctx % b):
+            raise ConfigError(
+                f"strict mode requires L_src and L_ctx divisible by b={b}, got ({self.icl.l_src}, {self.icl.l_ctx})")
+        if q.shape[3] not in SUPPORTED_HEAD_DIMS:
+            raise ConfigError(f"head dim {q.shape[3]} not supported by the sm_100a kernels {SUPPORTED_HEAD_DIMS}")
+        self.q, self.k, self.v = q, k, v
+        self.dims = IsaDims.derive(q.shape, self.icl, self.cfg)
+        d = self.dims
+        self.shape = N.IsaShape(d.B, d.H, d.S, d.D, self.icl.l_src, self.icl.l_ctx, b,
+                                N.ISA_DTYPE_BF16 if q.dtype == torch.bfloat16 else N.ISA_DTYPE_F32,
+                                q.stride(0), q.stride(1), q.stride(2))
+        self.knobs = N.IsaKnobs(d.scale, d.k_ctx, d.n_flat, max(d.k, 1), int(bool(self.cfg.softmax_first)), 0)
+
+    @staticmethod
+    def _to_device(x, name):
+        if isinstance(x, np.ndarray):
+            if x.ndim != 4:
+                raise LayoutError(f"{name}: expected 4 axes (B,H,S,D), got shape {x.shape}")
+            x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+        if not isinstance(x, torch.Tensor):
+            raise LayoutError(f"{name}: expected a torch tensor or numpy array")
+        if x.dim() != 4:
+            raise LayoutError(f"{name}: expected 4 axes (B,H,S,D), got shape {tuple(x.shape)}")
+        if min(x.shape) < 1:
+            raise LayoutError(f"{name}: all dims must be >= 1, got shape {tuple(x.shape)}")
+        if not x.is_cuda:
+            raise LayoutError(f"{name}: tensor must live on a CUDA device (no CPU path)")
+        if x.dtype not in (torch.bfloat16, torch.float32):
+            if not x.is_floating_point():
+                raise InputError(f"{name}: floating-point input required")
+            x = x.float()
+        if x.stride(3) != 1:
+            x = x.contiguous()
+        elem = x.element_size()
+        if any((s * elem) % 16 for s in x.stride()[:3]) or x.data_ptr() % 16:
+            x = x.contiguous()
+        return x
+
+    def workspace(self):
+        nbytes = ctypes.c_size_t(0)
+        N.check(N.load().isa_workspace_bytes(ctypes.byref(self.shape), ctypes.byref(self.knobs), ctypes.byref(nbytes)))
+        return torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.q.device), int(nbytes.value)
+
+
+def _routing_buffers(d: IsaDims, device):
+    B, H = d.B, d.H
+    i64 = dict(dtype=torch.int64, device=device)
+    return {
+        "selection": torch.empty((B, H, d.k_ctx), **i64),
+        "sharp": torch.empty((B, H, d.n_sharp), **i64),
+        "flat": torch.empty((B, H, d.n_flat), **i64),
+        "mask": torch.empty((B, H, d.n_flat, d.k), **i64),
+        "sharpness": torch.empty((B, H, d.T), dtype=torch.float64, device=device),
+        "ctx_scores": torch.empty((B, H, d.t_ctx), dtype=torch.float64, device=device),
+    }
+
+
+def _routing_struct(bufs) -> N.IsaRoutingOut:
+    return N.IsaRoutingOut(*(_ptr(bufs[n]) if bufs[n].numel() else None
+                             for n in ("selection", "sharp", "flat", "mask", "sharpness", "ctx_scores")))
+
+
+def _make_routing(d: IsaDims, bufs) -> IsaRouting:
+    sel = SelectionIndex(bufs["selection"], d.t_ctx)
+    split = SharpnessSplit(bufs["sharp"], bufs["flat"], bufs["sharpness"])
+    mask = BlockMask(bufs["mask"], d.t_new) if d.n_flat else None
+    return IsaRouting(selection=sel, split=split, mask=mask)
+
+
+def _raise_flags(err: torch.Tensor):
+    flags = int(err.item())
+    if flags & 1:
+        raise InputError("Q/K/V: non-finite elements")
+    if flags & 2:
+        raise DegenerateRowError("row with empty key set: normalizer is zero")
+
+
+class _LazySummary(dict):
+    """coarse_summary of the reference trace (coarse.py:41-49), computed on access
+    from the pooled means (torch fp64 on device; diagnostics only)."""
+
+    def __init__(self, qc, kc, scale):
+        super().__init__()
+        self._args = (qc, kc, scale)
+
+    def _resolve(self):
+        if self._args is not None:
+            qc, kc, scale = self._args
+            self._args = None
+            s = scale * torch.einsum("bhid,bhjd->bhij", qc.double(), kc.double())
+            dict.update(self, {"query_blocks": int(qc.shape[2]), "key_blocks": int(kc.shape[2]),
+                               "score_min": float(s.min()), "score_max": float(s.max()),
+                               "score_mean": float(s.mean())})
+
+    def items(self):
+        self._resolve()
+        return dict.items(self)
+
+    def __getitem__(self, key):
+        self._resolve()
+        return dict.__getitem__(self, key)
+
+    def __repr__(self):
+        self._resolve()
+        return dict.__repr__(self)
+
+
+def _pinned_struct(routing, d: IsaDims, device):
+    """IsaRouting (ours or the reference's numpy one) -> device int64 buffers."""
+    def dev(x, shape):
+        if x is None:
+            return None
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.int64))
+        t = t.to(device=device, dtype=torch.int64).contiguous()
+        if tuple(t.shape) != tuple(shape):
+            raise LayoutError(f"pinned routing shape {tuple(t.shape)} != {tuple(shape)}")
+        return t
+    sel = dev(routing.selection.indices, (d.B, d.H, d.k_ctx))
+    sharp = dev(routing.split.sharp, (d.B, d.H, d.n_sharp))
+    flat = dev(routing.split.flat, (d.B, d.H, d.n_flat))
+    mask = dev(routing.mask.indices, (d.B, d.H, d.n_flat, d.k)) if routing.mask is not None else None
+    keep = (sel, sharp, flat, mask)
+    return N.IsaRoutingIn(*(_ptr(t) if t is not None and t.numel() else None for t in keep)), keep
+
+
+def _run(inp: _Inputs, collect_trace: bool, pinned=None, out: Optional[torch.Tensor] = None, validate=True):
+    lib = N.load()
+    d = inp.dims
+    dev = inp.q.device
+    ws, nbytes = inp.workspace()
+    if out is None:
+        out = torch.empty((d.B, d.H, d.S, d.D), dtype=inp.q.dtype, device=dev)
+    elif not (out.is_contiguous() and tuple(out.shape) == (d.B, d.H, d.S, d.D) and out.dtype == inp.q.dtype):
+        raise LayoutError("out must be a contiguous (B,H,S,D) tensor of the input dtype")
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    bufs = _routing_buffers(d, dev) if collect_trace else None
+    rout = _routing_struct(bufs) if bufs is not None else None
+    pin_struct, keep = (None, None)
+    if pinned is not None:
+        pin_struct, keep = _pinned_struct(pinned, d, dev)
+    events = None
+    evs = None
+    if collect_trace:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        events = N.IsaEvents()
+        for i, e in enumerate(evs):
+            e.record()  # materialise the cudaEvent_t handle
+            events.ev[i] = e.cuda_event
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    N.check(lib.isa_forward(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), _ptr(inp.q), _ptr(inp.k), _ptr(inp.v),
+                            _ptr(out), _ptr(ws), nbytes, ctypes.byref(pin_struct) if pin_struct else None,
+                            ctypes.byref(rout) if rout else None, _ptr(err),
+                            ctypes.byref(events) if events else None, stream))
+    if validate:
+        _raise_flags(err)
+    trace = None
+    if collect_trace:
+        T, D = d.T, d.D
+        means = ws[256: 256 + 3 * d.B * d.H * T * D * 4].view(torch.float32).view(3, d.B, d.H, T, D)
+        qc, kc = means[0].clone(), means[1].clone()
+        times = _LazyStageTimes({"coarse": (evs[0], evs[1]), "select": (evs[1], evs[2]),
+                                 "split": (evs[2], evs[3]), "kernel": (evs[3], evs[4])})
+        dict.__setitem__(times, "reconstruct", 0.0)
+        routing = _make_routing(d, bufs)
+        trace = IsaTrace(coarse_summary=_LazySummary(qc, kc, d.scale), selection=routing.selection,
+                         split=routing.split, mask=routing.mask, flops=d.flops(), stage_times_us=times)
+    del keep
+    if inp.numpy_io:
+        out = out.float().cpu().numpy()
+    return out, trace, bufs
+
+
+def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = True, *, out=None, validate=True):
+    """Run the full pipeline; returns (output, IsaTrace or None) (pipeline.py:307-316).
+
+    The output has the input dtype (bf16 in -> bf16 out; fp32 in -> fp32 out,
+    computed with bf16 tensor cores and fp32 accumulation). Routing decisions
+    are exact float64 restatements of the reference and match it bit-for-bit.
+    """
+    res, trace, _ = _run(_Inputs(q, k, v, icl, cfg), collect_trace, out=out, validate=validate)
+    return res, trace
+
+
+def isa_routing(q, k, v, icl: IclLayout, cfg: IsaConfig) -> IsaRouting:
+    """Stages 1-3 only (pipeline.py:302-304); index tensors stay on the GPU."""
+    inp = _Inputs(q, k, v, icl, cfg)
+    lib = N.load()
+    d = inp.dims
+    ws, nbytes = inp.workspace()
+    err = torch.zeros(1, dtype=torch.int32, device=inp.q.device)
+    bufs = _routing_buffers(d, inp.q.device)
+    rout = _routing_struct(bufs)
+    stream = torch.cuda.current_stream(inp.q.device).cuda_stream
+    N.check(lib.isa_routing(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), _ptr(inp.q), _ptr(inp.k), _ptr(inp.v),
+                            _ptr(ws), nbytes, ctypes.byref(rout), _ptr(err), stream))
+    _raise_flags(err)
+    return _make_routing(d, bufs)
+
+
+def isa_forward_with_routing(q, k, v, icl: IclLayout, cfg: IsaConfig, routing) -> object:
+    """Forward pass with pinned routing (pipeline.py:319-328). Accepts our
+    IsaRouting or the reference's (numpy index arrays)."""
+    res, _, _ = _run(_Inputs(q, k, v, icl, cfg), False, pinned=routing)
+    return res
+
+
+def dense_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: Optional[float] = None,
+                    out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Dense non-causal softmax attention (reference.py:79-123) on the sm_100a
+    kernel with identity block tables: the ISA speed-up denominator (K8)."""
+    if q.dtype != torch.bfloat16:
+        raise ConfigError("dense_attention takes bf16 tensors")
+    B, H, S, D = q.shape
+    if D not in SUPPORTED_HEAD_DIMS:
+        raise ConfigError(f"head dim {D} not supported")
+    scale = scale if scale is not None else 1.0 / math.sqrt(D)
+    q, k, v = (x if x.stride(3) == 1 else x.contiguous() for x in (q, k, v))
+    if q.stride() != k.stride() or q.stride() != v.stride():
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    if out is None:
+        out = torch.empty((B, H, S, D), dtype=q.dtype, device=q.device)
+    shape = N.IsaShape(B, H, S, D, S, 0, 64, N.ISA_DTYPE_BF16, q.stride(0), q.stride(1), q.stride(2))
+    N.check(N.load().isa_dense_attention(ctypes.byref(shape), scale, _ptr(q), _ptr(k), _ptr(v), _ptr(out),
+                                         torch.cuda.current_stream(q.device).cuda_stream))
+    return out
+
+
+def prepare(q, k, v, icl, cfg):
+    """Validated inputs + a reusable workspace for repeated calls (bench/CUDA graphs)."""
+    inp = _Inputs(q, k, v, icl, cfg)
+    ws, nbytes = inp.workspace()
+    return _Prepared(inp, ws, nbytes)
+
+
+class _Prepared:
+    """Pre-validated call: no per-call allocation except nothing; graph-capturable."""
+
+    def __init__(self, inp: _Inputs, ws, nbytes):
+        self.inp, self.ws, self.nbytes = inp, ws, nbytes
+        d = inp.dims
+        self.out = torch.empty((d.B, d.H, d.S, d.D), dtype=inp.q.dtype, device=inp.q.device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=inp.q.device)
+
+    def __call__(self, stream=None):
+        inp = self.inp
+        st = stream if stream is not None else torch.cuda.current_stream(inp.q.device).cuda_stream
+        N.check(N.load().isa_forward(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), _ptr(inp.q), _ptr(inp.k),
+                                     _ptr(inp.v), _ptr(self.out), _ptr(self.ws), self.nbytes, None, None,
+                                     _ptr(self.err), None, st))
+        return self.out
