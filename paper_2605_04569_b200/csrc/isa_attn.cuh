@@ -50,8 +50,8 @@ struct AttnParams {
   int max_tiles;
   const uint32_t* member_bits;  // [BH][n_qblk][W]
   int W;
-  const float* clog2w;  // [BH][tn_pad]: log2(valid rows of K_new block j) or -inf
-  int tn_pad;           // centroid rows, multiple of 128
+  const int* ctx_short_j;  // [BH]: K_new index of the selected short context block or -1
+  int tn_pad;              // centroid rows, multiple of 128
   // output (token-major, D contiguous)
   void* out;
   int out_fp32;
@@ -63,6 +63,7 @@ constexpr int kThreads = 384;
 constexpr int kKvStages = 4;
 constexpr int kSoftmaxRegs = 208;
 constexpr int kOtherRegs = 96;
+constexpr int kLdCols = 16;  // tcgen05.ld width (columns) for the S row
 
 template <int D>
 struct AttnSmem {
@@ -197,28 +198,34 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp >= 8) {
     setmaxnreg_dec<kOtherRegs>();
-    if (warp == 9 && lane == 0) {
+    if (warp == 9) {
       // ------------------------------------------------------------ TMA producer
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
-      if (MODE == MODE_TAYLOR) {
-        tma_prefetch_desc(&tm_kc);
-        tma_prefetch_desc(&tm_vc);
+      // The whole warp walks the schedule (uniform values); one lane issues.
+      const bool leader = elect_one();
+      if (leader) {
+        tma_prefetch_desc(&tm_q);
+        tma_prefetch_desc(&tm_k);
+        tma_prefetch_desc(&tm_v);
+        if (MODE == MODE_TAYLOR) {
+          tma_prefetch_desc(&tm_kc);
+          tma_prefetch_desc(&tm_vc);
+        }
       }
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
       const int hh = bh % p.H, bb = bh / p.H;
-      int first_u = query_block<MODE>(p, bh, item, 0);
-      for (int s = 0; s < 2; ++s) {
-        mbar_arrive_expect_tx(&q_full[s], L::kTileBytes);
-        for (int half = 0; half < 2; ++half) {
-          int u = query_block<MODE>(p, bh, item, 2 * s + half);
-          if (u < 0) u = first_u;
-          const int tok = blk_tok0(p, u);
-          for (int pl = 0; pl < L::kPlanes; ++pl)
-            tma_load_4d(sQ + s * L::kTileBytes + pl * 16384 + half * 8192, &tm_q, &q_full[s], pl * 64, tok, hh, bb,
-                        pol_q);
+      const int first_u = query_block<MODE>(p, bh, item, 0);
+      if (leader) {
+        for (int s = 0; s < 2; ++s) {
+          mbar_arrive_expect_tx(&q_full[s], L::kTileBytes);
+          for (int half = 0; half < 2; ++half) {
+            int u = query_block<MODE>(p, bh, item, 2 * s + half);
+            if (u < 0) u = first_u;
+            const int tok = blk_tok0(p, u);
+            for (int pl = 0; pl < L::kPlanes; ++pl)
+              tma_load_4d(sQ + s * L::kTileBytes + pl * 16384 + half * 8192, &tm_q, &q_full[s], pl * 64, tok, hh,
+                          bb, pol_q);
+          }
         }
       }
       for (int i = 0; i < n_kv; ++i) {
@@ -228,74 +235,92 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int slot = c % kKvStages;
           const int use = c / kKvStages;
           if (use > 0) mbar_wait(&kv_empty[slot], (use - 1) & 1);
-          mbar_arrive_expect_tx(&kv_full[slot], L::kTileBytes);
-          uint8_t* dst = sKV + slot * L::kTileBytes;
-          const CUtensorMap* tm;
-          int c2, c3;
-          if (t.centroid) {
-            tm = kv == 0 ? &tm_kc : &tm_vc;
-            c2 = bh;
-            c3 = 0;
-          } else {
-            tm = kv == 0 ? &tm_k : &tm_v;
-            c2 = hh;
-            c3 = bb;
-          }
-          for (int half = 0; half < 2; ++half) {
-            const int tok = half ? t.tok1 : t.tok0;
-            for (int pl = 0; pl < L::kPlanes; ++pl)
-              tma_load_4d(dst + pl * 16384 + half * 8192, tm, &kv_full[slot], pl * 64, tok, c2, c3, pol_kv);
+          __syncwarp();
+          if (leader) {
+            mbar_arrive_expect_tx(&kv_full[slot], L::kTileBytes);
+            uint8_t* dst = sKV + slot * L::kTileBytes;
+            const CUtensorMap* tm;
+            int c2, c3;
+            if (t.centroid) {
+              tm = kv == 0 ? &tm_kc : &tm_vc;
+              c2 = bh;
+              c3 = 0;
+            } else {
+              tm = kv == 0 ? &tm_k : &tm_v;
+              c2 = hh;
+              c3 = bb;
+            }
+            for (int half = 0; half < 2; ++half) {
+              const int tok = half ? t.tok1 : t.tok0;
+              for (int pl = 0; pl < L::kPlanes; ++pl)
+                tma_load_4d(dst + pl * 16384 + half * 8192, tm, &kv_full[slot], pl * 64, tok, c2, c3, pol_kv);
+            }
+            progress(0, c + 1);
           }
         }
       }
-    } else if (warp == 8 && lane == 0) {
+    } else if (warp == 8) {
       // ------------------------------------------------------------ MMA issuer
+      // Whole warp waits; one elected lane issues tcgen05.mma / commit.
       constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D, 0, 1);
       const uint32_t sq = smem_u32(sQ);
       const uint32_t skv = smem_u32(sKV);
+      const bool leader = elect_one();
       auto issue_qk = [&](int s, int slot) {
-        const uint32_t a0 = sq + s * L::kTileBytes;
-        const uint32_t b0 = skv + slot * L::kTileBytes;
+        if (leader) {
+          const uint32_t a0 = sq + s * L::kTileBytes;
+          const uint32_t b0 = skv + slot * L::kTileBytes;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma_ss(tmem + s * 128, sdesc_sw128(a0 + off, 16, 1024), sdesc_sw128(b0 + off, 16, 1024), idesc_qk,
-                 kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma_ss(tmem + s * 128, sdesc_sw128(a0 + off, 16, 1024), sdesc_sw128(b0 + off, 16, 1024), idesc_qk,
+                   kk > 0);
+          }
         }
+        __syncwarp();
       };
       auto issue_pv = [&](int s, int slot, uint32_t acc) {
-        const uint32_t b0 = skv + slot * L::kTileBytes;
+        if (leader) {
+          const uint32_t b0 = skv + slot * L::kTileBytes;
+          const uint32_t ta = tmem + s * 128 + 64;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_ts(tmem + 256 + s * 128, tmem + s * 128 + 64 + kk * 8, sdesc_sw128(b0 + kk * 2048, 16384, 1024),
-                 idesc_pv, (acc | kk) != 0);
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tmem + 256 + s * 128, ta + kk * 8, sdesc_sw128(b0 + kk * 2048, 16384, 1024), idesc_pv,
+                   (acc | kk) != 0);
         }
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (leader) mma_commit(bar);
+        __syncwarp();
       };
       mbar_wait(&q_full[0], 0);
       mbar_wait(&q_full[1], 0);
-      // tile 0: K_0
       mbar_wait(&kv_full[0], 0);
+      __syncwarp();
       tc_fence_after();
       issue_qk(0, 0);
-      mma_commit(&s_full[0]);
+      commit(&s_full[0]);
       issue_qk(1, 0);
-      mma_commit(&s_full[1]);
-      mma_commit(&kv_empty[0]);
+      commit(&s_full[1]);
+      commit(&kv_empty[0]);
       for (int i = 1; i < n_kv; ++i) {
         const int cv = 2 * i - 1, ck = 2 * i;
         const int sv = cv % kKvStages, sk = ck % kKvStages;
         mbar_wait(&kv_full[sv], (cv / kKvStages) & 1);
         mbar_wait(&kv_full[sk], (ck / kKvStages) & 1);
+        if (leader) progress(1, 1000 * i + 1);
         for (int s = 0; s < 2; ++s) {
           mbar_wait(&p_full[s], (i - 1) & 1);
+          __syncwarp();
           tc_fence_after();
           issue_pv(s, sv, i > 1);
           issue_qk(s, sk);
-          mma_commit(&s_full[s]);
+          commit(&s_full[s]);
         }
-        mma_commit(&kv_empty[sv]);
-        mma_commit(&kv_empty[sk]);
+        commit(&kv_empty[sv]);
+        commit(&kv_empty[sk]);
       }
       {
         const int cv = 2 * n_kv - 1;
@@ -303,11 +328,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&kv_full[sv], (cv / kKvStages) & 1);
         for (int s = 0; s < 2; ++s) {
           mbar_wait(&p_full[s], (n_kv - 1) & 1);
+          __syncwarp();
           tc_fence_after();
           issue_pv(s, sv, n_kv > 1);
-          mma_commit(&o_full[s]);
+          commit(&o_full[s]);
         }
-        mma_commit(&kv_empty[sv]);
+        commit(&kv_empty[sv]);
       }
     }
     __syncwarp();
@@ -325,22 +351,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m = -INFINITY;  // running max, log2 domain (already scaled)
     float l = 0.f;
     const uint32_t* mbits = nullptr;
-    const float* cw = nullptr;
+    int jsrc = -1, jctx = -1;
+    float lwsrc = 6.f, lwctx = 6.f;
     if (MODE == MODE_TAYLOR) {
       int pos = item * 4 + qb;
       if (pos >= p.n_qblk) pos = item * 4;
       mbits = p.member_bits + ((long long)bh * p.n_qblk + pos) * p.W;
-      cw = p.clog2w + (long long)bh * p.tn_pad;
+      if (p.l_src & 63) {  // short last source block = K_new block t_src-1
+        jsrc = p.t_src - 1;
+        lwsrc = log2f(static_cast<float>(p.l_src & 63));
+      }
+      if (p.l_ctx & 63) {  // short last context block, if it was selected
+        jctx = p.ctx_short_j[bh];
+        lwctx = log2f(static_cast<float>(p.l_ctx & 63));
+      }
     }
     for (int i = 0; i < n_kv; ++i) {
       const TileInfo t = kv_tile<MODE>(p, bh, item, i);
       mbar_wait(&s_full[s], i & 1);
+      __syncwarp();  // reconverge before .sync.aligned tcgen05 ops
       tc_fence_after();
-      uint32_t sr[4][32];
+      uint32_t sr[128];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, sr[c]);
+      for (int c = 0; c < 128 / kLdCols; ++c) {
+        if (kLdCols == 16) tmem_ld16(t_s + c * 16, sr + c * 16);
+        else tmem_ld8(t_s + c * 8, sr + c * 8);
+      }
       tmem_ld_wait();
-      float* x = reinterpret_cast<float*>(&sr[0][0]);
+      float* x = reinterpret_cast<float*>(sr);
       const bool plain = !t.centroid && t.valid0 == 64 && t.valid1 == 64 &&
                          (MODE != MODE_TAYLOR || (((t.bits0 & t.bits1) >> qb) & 1));
       float mx[8];
@@ -359,15 +397,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           mx[c & 7] = fmaxf(mx[c & 7], x[c]);
         }
       } else {
+        // centroid column j: log2(valid rows of K_new block j) (64 except the
+        // short last block of either segment), -inf past t_new or when j is on
+        // this row block's exact list (taylor.py:153-157).
         const uint32_t* wb = mbits + t.cidx * 4;
-        const float* wc = cw + t.cidx * 128;
+        const int j0 = t.cidx * 128;
 #pragma unroll
         for (int w4 = 0; w4 < 4; ++w4) {
           const uint32_t bits = __ldg(wb + w4);
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
             const int cc = w4 * 32 + c;
-            const float bias = __ldg(wc + cc);
+            const int j = j0 + cc;
+            float bias = j == jsrc ? lwsrc : (j == jctx ? lwctx : 6.f);
+            bias = j < p.t_new ? bias : -INFINITY;
             x[cc] = ((bits >> c) & 1) ? -INFINITY : fmaf(x[cc], sl2, bias);
             mx[cc & 7] = fmaxf(mx[cc & 7], x[cc]);
           }
@@ -399,44 +442,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       const float mu = (m == -INFINITY) ? 0.f : m;
-      float sm[8];
+      float sm[4] = {0.f, 0.f, 0.f, 0.f};
+      // P in 4 chunks of 32 columns, each stored to TMEM right away so the
+      // live register set stays ~ S row + 16 packed words.
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sm[j] = 0.f;
-      uint32_t pk[2][32];
-      if (plain) {
-        const float nmu = -mu;
+      for (int ch = 0; ch < 4; ++ch) {
+        uint32_t pk[16];
+        if (plain) {
+          const float nmu = -mu;
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float p0 = ex2_approx(fmaf(x[2 * c], sl2, nmu));
-          const float p1 = ex2_approx(fmaf(x[2 * c + 1], sl2, nmu));
-          sm[c & 7] += p0 + p1;
-          pk[c >> 5][c & 31] = pack_bf16x2(p0, p1);
+          for (int c = 0; c < 16; ++c) {
+            const float p0 = ex2_approx(fmaf(x[32 * ch + 2 * c], sl2, nmu));
+            const float p1 = ex2_approx(fmaf(x[32 * ch + 2 * c + 1], sl2, nmu));
+            sm[c & 3] += p0 + p1;
+            pk[c] = pack_bf16x2(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const float p0 = ex2_approx(x[32 * ch + 2 * c] - mu);
+            const float p1 = ex2_approx(x[32 * ch + 2 * c + 1] - mu);
+            sm[c & 3] += p0 + p1;
+            pk[c] = pack_bf16x2(p0, p1);
+          }
         }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float p0 = ex2_approx(x[2 * c] - mu);
-          const float p1 = ex2_approx(x[2 * c + 1] - mu);
-          sm[c & 7] += p0 + p1;
-          pk[c >> 5][c & 31] = pack_bf16x2(p0, p1);
-        }
+        tmem_st16(t_p + 16 * ch, pk);
       }
-      const float sum = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + ((sm[4] + sm[5]) + (sm[6] + sm[7]));
-      tmem_st32(t_p, pk[0]);
-      tmem_st32(t_p + 32, pk[1]);
+      const float sum = (sm[0] + sm[1]) + (sm[2] + sm[3]);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[s]);
       l += sum;
+      if ((threadIdx.x & 127) == 0) progress(2 + s, i + 1);
     }
     // -------------------------------------------------------------- epilogue
     mbar_wait(&o_full[s], 0);
+    __syncwarp();
     tc_fence_after();
     const int u = query_block<MODE>(p, bh, item, qb);
     const int rr = row & 63;
     const bool write = u >= 0 && rr < blk_valid(p, u);
-    if (write && !(l > 0.f) && p.err_flag) atomicOr(p.err_flag, 1);
+    if (write && !(l > 0.f) && p.err_flag) atomicOr(p.err_flag, 2);
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const int hh = bh % p.H, bb = bh / p.H;
     const long long obase =
@@ -444,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
     for (int c = 0; c < D / 32; ++c) {
       uint32_t orr[32];
+      __syncwarp();
       tmem_ld32(t_o + c * 32, orr);
       tmem_ld_wait();
       if (write) {

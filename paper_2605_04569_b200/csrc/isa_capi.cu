@@ -154,7 +154,7 @@ struct Workspace {
   uint32_t* bits;     // [BH][n_flat][W]
   __nv_bfloat16* kc_bf;  // [BH][tn_pad][D]
   __nv_bfloat16* vc_bf;
-  float* clog2w;      // [BH][tn_pad]
+  int* ctx_short;     // [BH]
   int4* tiles;        // [BH][items_f][max_tiles]
   int* n_tiles;       // [BH][items_f]
   size_t bytes;
@@ -185,7 +185,7 @@ Workspace carve(const Dims& d, int dtype, uint8_t* base) {
   w.bits = reinterpret_cast<uint32_t*>(take(4ull * BH * d.n_flat * d.W));
   w.kc_bf = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.tn_pad * d.D));
   w.vc_bf = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.tn_pad * d.D));
-  w.clog2w = reinterpret_cast<float*>(take(4ull * BH * d.tn_pad));
+  w.ctx_short = reinterpret_cast<int*>(take(4ull * BH));
   w.tiles = reinterpret_cast<int4*>(take(16ull * BH * d.items_f * d.max_tiles));
   w.n_tiles = reinterpret_cast<int*>(take(4ull * BH * d.items_f));
   w.bytes = off;
@@ -348,12 +348,12 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
     isa::topk_rank_kernel<<<d.BH, 1024, sm, st>>>(w.ctx, d.t_ctx, d.k_ctx, w.sel, ro ? ro->selection : nullptr);
     ISA_LAUNCHED("topk_rank_kernel");
   }
-  isa::kvblk_from_sel_kernel<<<d.BH, 256, 0, st>>>(w.sel, d.t_src, d.k_ctx, w.kv_blk);
+  isa::kvblk_from_sel_kernel<<<d.BH, 256, 0, st>>>(w.sel, d.t_src, d.k_ctx, w.kv_blk, w.ctx_short);
   ISA_LAUNCHED("kvblk_from_sel_kernel");
   if (d.n_flat) {
     isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};
     isa::centroid_kernel<<<dim3(d.tn_pad, d.BH), d.D, 0, st>>>(kc, vc, w.kv_blk, d.T, d.t_new, d.tn_pad, d.D, seg,
-                                                                w.kc_bf, w.vc_bf, w.clog2w);
+                                                                w.kc_bf, w.vc_bf, w.ctx_short);
     ISA_LAUNCHED("centroid_kernel");
   }
   if (ro && ro->ctx_scores && need_scores && d.t_ctx)
@@ -498,7 +498,7 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
     pf.max_tiles = d.max_tiles;
     pf.member_bits = w.bits;
     pf.W = d.W;
-    pf.clog2w = w.clog2w;
+    pf.ctx_short_j = w.ctx_short;
     pf.tn_pad = d.tn_pad;
     if ((rc = launch_attention_d<isa::MODE_TAYLOR>(d.D, tq, tk, tv, tkc, tvc, pf, d.items_f, d.BH, st))) return rc;
   }

@@ -76,22 +76,35 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
+// Progress words written by each warp role (debug aid printed on a wait
+// timeout): [cta % 1024][role] with roles 0 = TMA, 1 = MMA, 2/3 = softmax 0/1.
+__device__ volatile int g_isa_progress[1024][4];
+
+__device__ __forceinline__ void progress(int role, int v) {
+  g_isa_progress[(blockIdx.y * gridDim.x + blockIdx.x) & 1023][role] = v;
+}
+
 // Blocks until the phase with the given parity has completed. A wait that
-// exceeds ~4 s traps (kernel error instead of a hung GPU) — a protocol bug
-// must never wedge the device.
-__device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
+// exceeds ~3 s traps (kernel error instead of a hung GPU): a protocol bug must
+// never wedge the device. Fully inlined and call-free on purpose: a function
+// called from warp roles with different setmaxnreg budgets makes ptxas fall
+// back to the launch register cap in every role (measured: 1-2 KB of spills).
+// Build with -DISA_DEBUG_WAIT for a diagnostic printf before the trap.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = global_ns();
   uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && global_ns() - t0 > 4000000000ull) {
-      printf("isa: mbarrier wait timeout (block %d,%d thread %d parity %u)\n", blockIdx.x, blockIdx.y,
-             threadIdx.x, parity);
+    if ((++n & 1023u) == 0 && global_ns() - t0 > 3000000000ull) {
+#ifdef ISA_DEBUG_WAIT
+      const int c = (blockIdx.y * gridDim.x + blockIdx.x) & 1023;
+      printf("isa: wait timeout cta(%d,%d) tid %d bar@%u parity %u prog tma=%d mma=%d s0=%d s1=%d\n", blockIdx.x,
+             blockIdx.y, threadIdx.x, smem_u32(bar), parity, g_isa_progress[c][0], g_isa_progress[c][1],
+             g_isa_progress[c][2], g_isa_progress[c][3]);
+#endif
       asm volatile("trap;");
     }
   }
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
 }
 
 // ---------------------------------------------------------------- TMA
@@ -195,6 +208,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 
+// TMEM -> registers, 16 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// 8 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -203,6 +231,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
       "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
 }
 
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }

@@ -420,15 +420,15 @@ __global__ void __launch_bounds__(128) block_mask_kernel(
 }
 
 // ----------------------------------------------------------------------------
-// K_new centroids in bf16 for the Taylor kernel's centroid tiles, and the
-// per-column additive log2(valid_rows) weight (taylor.py:156): rows j < t_new
-// copy kc/vc of original block kv_blk[j]; rows >= t_new are zero with -inf
-// weight. grid (tn_pad, BH), block D.
+// K_new centroids in bf16 for the Taylor kernel's centroid tiles (rows j <
+// t_new copy kc/vc of original block kv_blk[j]; rows >= t_new are zero), and
+// the K_new index of the selected short last context block (its centroid
+// weight is its valid-row count, taylor.py:156). grid (tn_pad, BH), block D.
 // ----------------------------------------------------------------------------
 __global__ void centroid_kernel(const float* __restrict__ kc, const float* __restrict__ vc,
                                 const int* __restrict__ kv_blk, int T, int t_new, int tn_pad, int D, SegInfo seg,
                                 __nv_bfloat16* __restrict__ kc_bf, __nv_bfloat16* __restrict__ vc_bf,
-                                float* __restrict__ clog2w) {
+                                int* __restrict__ ctx_short_j) {
   const int j = blockIdx.x, bh = blockIdx.y;
   const long long o = ((long long)bh * tn_pad + j) * D;
   if (j < t_new) {
@@ -438,13 +438,12 @@ __global__ void centroid_kernel(const float* __restrict__ kc, const float* __res
       kc_bf[o + d] = __float2bfloat16_rn(kc[src + d]);
       vc_bf[o + d] = __float2bfloat16_rn(vc[src + d]);
     }
-    if (threadIdx.x == 0) clog2w[(long long)bh * tn_pad + j] = log2f(static_cast<float>(seg.valid(u)));
+    if (threadIdx.x == 0 && j >= seg.t_src && u == seg.t_src + seg.t_ctx - 1) ctx_short_j[bh] = j;
   } else {
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
       kc_bf[o + d] = __float2bfloat16_rn(0.f);
       vc_bf[o + d] = __float2bfloat16_rn(0.f);
     }
-    if (threadIdx.x == 0) clog2w[(long long)bh * tn_pad + j] = -INFINITY;
   }
 }
 
@@ -528,8 +527,10 @@ __global__ void narrow_kernel(const int64_t* __restrict__ src, int* __restrict__
 }
 
 // Pinned selection -> K_new block table.
-__global__ void kvblk_from_sel_kernel(const int* __restrict__ sel, int t_src, int k_ctx, int* __restrict__ kv_blk) {
+__global__ void kvblk_from_sel_kernel(const int* __restrict__ sel, int t_src, int k_ctx, int* __restrict__ kv_blk,
+                                      int* __restrict__ ctx_short_j) {
   const int bh = blockIdx.x;
+  if (threadIdx.x == 0) ctx_short_j[bh] = -1;
   const int t_new = t_src + k_ctx;
   for (int j = threadIdx.x; j < t_new; j += blockDim.x)
     kv_blk[(long long)bh * t_new + j] = j < t_src ? j : t_src + sel[(long long)bh * k_ctx + j - t_src];
