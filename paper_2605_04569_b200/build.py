@@ -38,6 +38,7 @@ def nvcc_command(out: str = LIB) -> list[str]:
         "-Xcompiler", "-fPIC", "-shared",
         "-Xptxas", "-v",
         "-I", os.path.join(ROOT, "include"),
+        *(["-DISA_DEBUG_WAIT"] if os.environ.get("ISA_DEBUG_WAIT") else []),
         "-o", out,
         *[os.path.join(CSRC, s) for s in SOURCES],
     ]

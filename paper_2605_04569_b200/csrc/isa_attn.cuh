@@ -62,7 +62,13 @@ struct AttnParams {
 constexpr int kThreads = 384;
 constexpr int kKvStages = 4;
 constexpr int kSoftmaxRegs = 208;
-constexpr int kOtherRegs = 96;
+constexpr int kOtherRegs = 88;
+// setmaxnreg moves registers inside the CTA's pool only: the two softmax
+// warpgroups may grow by no more than the third warpgroup shrinks from the
+// launch allocation (65536 / 384 -> 168 per thread). Violating this starves
+// a softmax warp in USETMAXREG.TRY_ALLOC forever (observed on B200).
+constexpr int kLaunchRegs = 168;
+static_assert(2 * (kSoftmaxRegs - kLaunchRegs) <= (kLaunchRegs - kOtherRegs), "register pool overcommitted");
 constexpr int kLdCols = 16;  // tcgen05.ld width (columns) for the S row
 
 template <int D>

@@ -1,5 +1,5 @@
 import re, sys, collections
-pat = re.compile(r"cta\((\d+),(\d+)\) tid (\d+) bar@(\d+) parity (\d+) raw=(\w+) prog tma=(-?\d+) mma=(-?\d+) s0=(-?\d+) s1=(-?\d+)")
+pat = re.compile(r"cta\((\d+),(\d+)\) tid (\d+) bar@(\d+) parity (\d+)(?: raw=(\w+))? prog tma=(-?\d+) mma=(-?\d+) s0=(-?\d+) s1=(-?\d+)")
 groups = collections.defaultdict(list)
 other = []
 for line in sys.stdin:
