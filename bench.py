@@ -1,0 +1,411 @@
+"""Benchmark of the ISA attention layer (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], the config the metric is quoted on):
+one ISA attention layer at 32K source + 32K context tokens, Wan-14B shape
+(B=1, H=40, D=128), bf16, default knobs (alpha_s=0.125, alpha_ns=0.0625,
+alpha_f=0.5, b=64), synthetic i.i.d. N(0,1) Q/K/V (seeded). Inputs are 2 GB,
+larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+One step = one full isa_forward (all five stages, routing included) over the
+heads this rank owns. N > 1: heads are sharded round-robin over ranks and the
+outputs are reassembled with an NCCL all-gather (paper_2605_04569_b200.parallel);
+value = max over ranks of the step time (strong scaling: the layer is fixed).
+
+Prints ONE JSON line on rank 0. `--impl reference` times the reference
+algorithm on the host CPU instead (the oracle port of the pure-Python
+reference, run on a bounded sample and extrapolated).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ISA attn-layer latency (ms) & TFLOPS at 2x32K tokens vs dense attn; GPU scaling"
+WORKLOAD = dict(workload="cfg3: ISA attention layer, Wan-14B shape, 32K source + 32K context",
+                batch=1, heads=40, head_dim=128, l_src=32768, l_ctx=32768, block=64,
+                alpha_s=0.125, alpha_ns=0.0625, alpha_f=0.5,
+                inputs="iid N(0,1) bf16, seed 0; 2 GB of Q/K/V > 126 MB L2 (no flush needed)")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--heads", type=int, default=WORKLOAD["heads"])
+    ap.add_argument("--l-src", type=int, default=WORKLOAD["l_src"])
+    ap.add_argument("--l-ctx", type=int, default=WORKLOAD["l_ctx"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip dense/SDPA/e2e side measurements")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- CPU (reference algorithm)
+def cpu_sample(l_src, l_ctx, heads, D=128, fraction=1 / 16, seed=0):
+    """Time the reference algorithm (oracle port, numpy/BLAS on all host cores)
+    on one head of the workload: routing (stages 1-3) in full, attention on a
+    `fraction` of the query blocks; extrapolate to all heads (the reference runs
+    heads serially: reference.py:159-160, taylor.py:176-177)."""
+    import numpy as np
+
+    from oracle import isa_oracle as O
+
+    rng = np.random.default_rng(seed)
+    S = l_src + l_ctx
+    q, k, v = (O.round_bf16(rng.standard_normal((1, 1, S, D), dtype=np.float32)) for _ in range(3))
+    t0 = time.perf_counter()
+    asm = O.OracleAssembly(q, k, v, l_src, l_ctx)
+    t1 = time.perf_counter()
+    asm.forward(block_fraction=fraction)
+    t2 = time.perf_counter()
+    per_head = (t1 - t0) + (t2 - t1) / fraction
+    return per_head * heads * 1e3, dict(route_s=t1 - t0, attn_sample_s=t2 - t1)
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        n = max((i.get("num_threads", 1) for i in info), default=os.cpu_count())
+        return int(n), [i.get("internal_api") for i in info]
+    except Exception:
+        return os.cpu_count(), []
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    fraction = 1 / 16
+    vals = []
+    for i in range(args.warmup + args.steps):
+        ms, detail = cpu_sample(args.l_src, args.l_ctx, args.heads, fraction=fraction)
+        if i >= args.warmup:
+            vals.append(ms)
+    value = statistics.median(vals)
+    cores, apis = cpu_cores()
+    sample = (f"1 of {args.heads} heads: routing (stages 1-3) in full + attention on 1/16 of the query blocks, "
+              f"extrapolated x{args.heads} heads (oracle port of the pure-Python reference; numpy fp64 over {apis})")
+    line = {
+        "metric": METRIC, "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": dict(WORKLOAD, parallelism="cpu"),
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- GPU
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_04569_b200 as P
+    from paper_2605_04569_b200 import _native as N
+    from paper_2605_04569_b200.parallel import head_shard, isa_forward_sharded
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    H, D = args.heads, WORKLOAD["head_dim"]
+    S = args.l_src + args.l_ctx
+    icl = P.IclLayout(args.l_src, args.l_ctx)
+    cfg = P.IsaConfig()
+    my_heads = head_shard(H, rank, world)
+    Hl = len(my_heads)
+    g = torch.Generator(device=dev).manual_seed(0)
+    # Each rank synthesises only its own heads (round-robin). Identical to
+    # slicing a full seeded (1,H,S,D) tensor because heads are drawn per head.
+    q = torch.empty((1, Hl, S, D), dtype=torch.bfloat16, device=dev)
+    k, v = torch.empty_like(q), torch.empty_like(q)
+    for j, h in enumerate(my_heads):
+        gh = torch.Generator(device=dev).manual_seed(1000 + h)
+        for t in (q, k, v):
+            t[0, j].copy_(torch.randn((S, D), generator=gh, device=dev, dtype=torch.float32).to(torch.bfloat16))
+    del g
+    dims = P.IsaDims.derive((1, H, S, D), icl, cfg)
+    flops = dims.flops()
+    f_isa = flops.total()
+    f_dense = flops.dense_equivalent_mas
+    f_sharp = 4 * 64 * 64 * D * dims.n_sharp * dims.t_new * 1 * Hl
+    f_taylor_alg = (4 * 64 * 64 * D * dims.n_flat * dims.k + 4 * 64 * D * dims.n_flat * (dims.t_new - dims.k)) * Hl
+
+    out_full = torch.empty((1, H, S, D), dtype=torch.bfloat16, device=dev) if world > 1 else None
+    prep = P.prepare(q, k, v, icl, cfg)
+
+    def step():
+        if world > 1:
+            return isa_forward_sharded(prep, out_full, my_heads, world)
+        return prep()
+
+    # warmup
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches = N.load().isa_last_launch_count()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.3)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(args.steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- per-stage / per-kernel times (events recorded by the C ABI on the launching stream)
+    stage = {}
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    ev_struct = N.IsaEvents()
+    for i, e in enumerate(evs):
+        e.record()
+        ev_struct.ev[i] = e.cuda_event
+    reps = 3
+    acc = {k_: 0.0 for k_ in ("coarse", "select", "split", "exact", "taylor")}
+    for _ in range(reps):
+        _call_with_events(prep, ev_struct)
+        torch.cuda.synchronize()
+        acc["coarse"] += evs[0].elapsed_time(evs[1])
+        acc["select"] += evs[1].elapsed_time(evs[2])
+        acc["split"] += evs[2].elapsed_time(evs[3])
+        acc["exact"] += evs[3].elapsed_time(evs[4])
+        acc["taylor"] += evs[4].elapsed_time(evs[5])
+    stage = {k_: v_ / reps for k_, v_ in acc.items()}
+    peaks = _peaks()
+    peak_tc = peaks.get("bf16_tflops_sustained") or 1354.8
+    exact_tflops = f_sharp / (stage["exact"] * 1e-3) / 1e12
+    taylor_tflops = f_taylor_alg / (stage["taylor"] * 1e-3) / 1e12 if stage["taylor"] > 0 else None
+    prof = _profile_summary()
+
+    result = {
+        "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": dict(WORKLOAD, heads=H, l_src=args.l_src, l_ctx=args.l_ctx,
+                       parallelism=f"head-sharded x{world}" if world > 1 else "single GPU",
+                       l2="inputs larger than L2"),
+        "tflops_isa_alg": f_isa / (ms * 1e-3) / 1e12,
+        "tflops_dense_equiv": f_dense / (ms * 1e-3) / 1e12,
+        "flops": {"isa": f_isa, "dense": f_dense, "sharp": f_sharp * world, "taylor_alg": f_taylor_alg * world},
+        "stage_ms": stage,
+        "gpu_launches": launches * args.steps,
+        "roofline": {
+            "kernel": "gba_attention_kernel<128, MODE_EXACT> (K6, sharp branch)",
+            "bound": "tensor", "achieved": exact_tflops, "peak": peak_tc, "unit": "TFLOP/s",
+            "frac": exact_tflops / peak_tc, "traffic": prof.get("exact_dram_bytes"),
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a ~20 ms step)",
+            "algorithmic": "F_sharp = 4*b^2*D*n_sharp*t_new per head (pipeline.py:278) / CUDA-event K6 duration",
+        },
+        "taylor_kernel": {"achieved": taylor_tflops, "frac": (taylor_tflops / peak_tc) if taylor_tflops else None,
+                          "unit": "TFLOP/s", "algorithmic": "reference flop_count (taylor.py:299-316)"},
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_extras:
+        result.update(_extras(args, P, q, k, v, icl, cfg, ms, dev))
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cms, detail = cpu_sample(args.l_src, args.l_ctx, H)
+        cores, apis = cpu_cores()
+        result["cpu_baseline"] = {
+            "value": cms, "unit": "ms", "cores": cores, "kind": "port",
+            "sample": f"1 head (routing full + 1/16 of query blocks for attention) x{H} heads extrapolated; "
+                      f"oracle port of the pure-Python reference (numpy fp64, BLAS {apis}); "
+                      f"route {detail['route_s']:.2f}s, attention sample {detail['attn_sample_s']:.2f}s",
+        }
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def _call_with_events(prep, ev_struct):
+    import ctypes
+
+    import torch
+
+    from paper_2605_04569_b200 import _native as N
+    from paper_2605_04569_b200.pipeline import _ptr
+
+    inp = prep.inp
+    N.check(N.load().isa_forward(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), _ptr(inp.q), _ptr(inp.k),
+                                 _ptr(inp.v), _ptr(prep.out), _ptr(prep.ws), prep.nbytes, None, None, _ptr(prep.err),
+                                 ctypes.byref(ev_struct), torch.cuda.current_stream().cuda_stream))
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "fallback": True}
+
+
+def _profile_summary():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+    except Exception:
+        return {}
+
+
+def _extras(args, P, q, k, v, icl, cfg, ms, dev):
+    """Dense sm_100a baseline (K8), cuDNN SDPA cross-check and the e2e number."""
+    import torch
+    import torch.nn.functional as F
+
+    res = {}
+    st = torch.cuda.current_stream()
+
+    def timeit(fn, reps=2):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    dense_ms = timeit(lambda: P.dense_attention(q, k, v))
+    res["dense_ms"] = dense_ms
+    res["speedup_vs_dense_sm100a"] = dense_ms / ms
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+            sdpa_ms = timeit(lambda: F.scaled_dot_product_attention(q, k, v))
+        res["cudnn_sdpa_ms"] = sdpa_ms
+        res["speedup_vs_cudnn_sdpa"] = sdpa_ms / ms
+    except Exception as exc:  # pragma: no cover
+        res["cudnn_sdpa_ms"] = None
+        res["cudnn_sdpa_error"] = str(exc)[:200]
+    d = P.IsaDims.derive(q.shape, icl, cfg)
+    res["dense_tflops"] = d.flops().dense_equivalent_mas / (dense_ms * 1e-3) / 1e12
+
+    # e2e through the public API with host buffers (pinned), H2D + D2H inside the timed region
+    qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+    outh = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+
+    def e2e():
+        qd, kd, vd = (t.to(dev, non_blocking=True) for t in (qh, kh, vh))
+        out, _ = P.isa_forward(qd, kd, vd, icl, cfg, collect_trace=False)
+        outh.copy_(out, non_blocking=True)
+
+    e2e()
+    torch.cuda.synchronize()
+    steps = max(2, min(args.steps, 5))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(steps):
+        e2e()
+    b.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / steps
+    nb = q.numel() * q.element_size()
+    res["e2e"] = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": 3 * nb, "d2h_bytes_per_step": nb,
+                  "note": "public isa_forward API; pinned host Q/K/V copied in and O copied out every step"}
+    return res
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "--gpus > 1 must be launched with torch.distributed.run"}))
+        return
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -91,14 +91,19 @@ typedef struct IsaRoutingIn {
 
 /* Optional per-stage CUDA events (cudaEvent_t handles cast to void*):
  * ev[0] start, ev[1] after stage 1 "coarse", ev[2] after stage 2 "select",
- * ev[3] after stage 3 "split", ev[4] after stage 4 "kernel" (pipeline.py:157-348;
- * stage 5 "reconstruct" is fused into the stage-4 epilogues). NULL entries skip. */
+ * ev[3] after stage 3 "split", ev[4] after the exact (sharp) attention kernel,
+ * ev[5] after the Taylor (flat) kernel (pipeline.py:157-348; stage 5
+ * "reconstruct" is fused into the stage-4 epilogues). NULL entries skip. */
 typedef struct IsaEvents {
-  void* ev[5];
+  void* ev[6];
 } IsaEvents;
 
 int isa_abi_version(void);
 const char* isa_last_error(void);
+
+/* Number of kernels the calling thread's last isa_forward / isa_routing /
+ * isa_dense_attention call launched (thread-local; for launch accounting). */
+int isa_last_launch_count(void);
 
 /* Workspace needed by isa_forward / isa_routing for this geometry. */
 int isa_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* bytes);

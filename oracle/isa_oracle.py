@@ -281,8 +281,12 @@ class OracleAssembly:
             ctx_scores = self.s_coarse[:, :, : self.t_src, self.t_src:].mean(axis=2)
         return OracleRouting(self.sel, self.sharp, self.flat, self.sharpness, self.mask, ctx_scores, self.s_flat)
 
-    def forward(self) -> np.ndarray:
-        """Stages 4-5 of _forward (pipeline.py:331-358), gamma = 0."""
+    def forward(self, block_fraction: float = 1.0) -> np.ndarray:
+        """Stages 4-5 of _forward (pipeline.py:331-358), gamma = 0.
+
+        block_fraction < 1 computes only the first ceil(f*n) sharp and flat
+        query blocks of each head (bench.py's bounded CPU sample; rows are
+        independent so time scales linearly); the rest of the output is 0."""
         B, H, Sp, D = self.qp.shape
         b = self.b
         out_pad = np.zeros((B, H, Sp, D), dtype=np.float64)
@@ -292,16 +296,20 @@ class OracleAssembly:
             for hi in range(H):
                 kf = self.k_new[bi, hi].astype(np.float64)
                 vf = self.v_new[bi, hi].astype(np.float64)
-                if self.n_sharp:  # pipeline.py:338-343
-                    rows = qb[bi, hi, self.sharp[bi, hi]].reshape(-1, D).astype(np.float64)
+                ns = int(math.ceil(block_fraction * self.n_sharp))
+                nf = int(math.ceil(block_fraction * self.n_flat))
+                if ns:  # pipeline.py:338-343
+                    sel = self.sharp[bi, hi, :ns]
+                    rows = qb[bi, hi, sel].reshape(-1, D).astype(np.float64)
                     o = masked_softmax_attention(rows, kf, vf, self.scale, self.key_mask_new[bi, hi])
-                    ob[bi, hi, self.sharp[bi, hi]] = o.reshape(-1, b, D)
-                if self.n_flat:  # pipeline.py:344-347, taylor.py:163-194
-                    rows = qb[bi, hi, self.flat[bi, hi]].reshape(-1, D).astype(np.float64)
+                    ob[bi, hi, sel] = o.reshape(-1, b, D)
+                if nf:  # pipeline.py:344-347, taylor.py:163-194
+                    sel = self.flat[bi, hi, :nf]
+                    rows = qb[bi, hi, sel].reshape(-1, D).astype(np.float64)
                     o = taylor_head(rows, kf, vf, self.kc_new[bi, hi].astype(np.float64),
-                                    self.vc_new[bi, hi].astype(np.float64), self.mask[bi, hi],
+                                    self.vc_new[bi, hi].astype(np.float64), self.mask[bi, hi, :nf],
                                     self.valid_new[bi, hi], self.scale, b)
-                    ob[bi, hi, self.flat[bi, hi]] = o.reshape(-1, b, D)
+                    ob[bi, hi, sel] = o.reshape(-1, b, D)
         out = out_pad.astype(np.float32)[:, :, self.orig_rows]  # pipeline.py:357 (storage dtype fp32)
         return out
 

@@ -23,6 +23,7 @@ ISA_DTYPE_F32 = 1
 EXPORTED_SYMBOLS = (
     "isa_abi_version",
     "isa_last_error",
+    "isa_last_launch_count",
     "isa_workspace_bytes",
     "isa_forward",
     "isa_routing",
@@ -82,7 +83,7 @@ class IsaRoutingIn(ctypes.Structure):
 
 
 class IsaEvents(ctypes.Structure):
-    _fields_ = [("ev", ctypes.c_void_p * 5)]
+    _fields_ = [("ev", ctypes.c_void_p * 6)]
 
 
 _lib = None
@@ -93,6 +94,7 @@ _I = ctypes.c_int32
 _SIGS = {
     "isa_abi_version": (ctypes.c_int, []),
     "isa_last_error": (ctypes.c_char_p, []),
+    "isa_last_launch_count": (ctypes.c_int, []),
     "isa_workspace_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs),
                                            ctypes.POINTER(ctypes.c_size_t)]),
     "isa_forward": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _P, _P, _P, _P, _P,

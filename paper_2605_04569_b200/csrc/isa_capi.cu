@@ -28,6 +28,7 @@
 namespace {
 
 thread_local std::string g_last_error;
+thread_local int g_launches = 0;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -47,6 +48,7 @@ int fail(int code, const char* fmt, ...) {
 
 #define ISA_LAUNCHED(name)                                                                             \
   do {                                                                                                 \
+    ++g_launches;                                                                                      \
     cudaError_t e_ = cudaGetLastError();                                                               \
     if (e_ != cudaSuccess) return fail(ISA_ERR_CUDA, "launch %s: %s", name, cudaGetErrorString(e_)); \
   } while (0)
@@ -420,6 +422,8 @@ extern "C" {
 
 int isa_abi_version(void) { return ISA_ABI_VERSION; }
 
+int isa_last_launch_count(void) { return g_launches; }
+
 const char* isa_last_error(void) { return g_last_error.c_str(); }
 
 int isa_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* bytes) {
@@ -433,6 +437,7 @@ int isa_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* by
 
 int isa_routing(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
                 void* workspace, size_t workspace_bytes, IsaRoutingOut* routing, int32_t* err_word, void* stream) {
+  g_launches = 0;
   Dims d;
   int rc = derive(shape, knobs, &d);
   if (rc) return rc;
@@ -447,6 +452,7 @@ int isa_routing(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
 int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v, void* out,
                 void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
                 int32_t* err_word, const IsaEvents* events, void* stream) {
+  g_launches = 0;
   Dims d;
   int rc = derive(shape, knobs, &d);
   if (rc) return rc;
@@ -482,6 +488,7 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
     ps.qlist = w.sharp;
     if ((rc = launch_attention_d<isa::MODE_EXACT>(d.D, tq, tk, tv, tq, tq, ps, d.items_s, d.BH, st))) return rc;
   }
+  record(events, 4, st);
   if (d.n_flat) {
     if ((rc = make_map(&tkc, w.kc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
                        (long long)d.BH * d.tn_pad * d.D * 2)))
@@ -502,12 +509,13 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
     pf.tn_pad = d.tn_pad;
     if ((rc = launch_attention_d<isa::MODE_TAYLOR>(d.D, tq, tk, tv, tkc, tvc, pf, d.items_f, d.BH, st))) return rc;
   }
-  record(events, 4, st);
+  record(events, 5, st);
   return ISA_OK;
 }
 
 int isa_dense_attention(const IsaShape* shape, double scale, const void* q, const void* k, const void* v, void* out,
                         void* stream) {
+  g_launches = 0;
   IsaKnobs kn{scale, 0, 0, 1, 1, 0};
   Dims d;
   int rc = derive(shape, &kn, &d);

@@ -22,8 +22,13 @@ struct SegInfo {
   }
 };
 
-// (score desc, index asc): true when (a, ia) ranks before (b, ib).
+// (score desc, index asc): true when (a, ia) ranks before (b, ib). NaN ranks
+// after every number, so the order stays total and every selection emits
+// exactly k indices even on non-finite input (which is then reported as
+// InputError by the pooling kernel's flag).
 __device__ __forceinline__ bool ranks_before(double a, int ia, double b, int ib) {
+  const bool na = a != a, nb = b != b;
+  if (na || nb) return na && nb ? ia < ib : nb;
   return a > b || (a == b && ia < ib);
 }
 
