@@ -145,7 +145,9 @@ struct Workspace {
   int32_t* err;
   float* means;  // [3][BH][T][D]
   __nv_bfloat16* bf;  // [3][BH][S][D] (fp32 inputs only)
-  double* s_src;      // [BH][T][t_src]
+  double* s_new;      // [BH][T][t_new]  fp64 coarse scores vs K_new blocks
+  double* qsum;       // [BH][D]
+  uint8_t* flags;     // [BH][max(T, t_ctx)]
   double* ctx;        // [BH][t_ctx]
   int* sel;           // [BH][k_ctx]
   int* kv_blk;        // [BH][t_new]
@@ -176,7 +178,9 @@ Workspace carve(const Dims& d, int dtype, uint8_t* base) {
   w.err = reinterpret_cast<int32_t*>(take(16));
   w.means = reinterpret_cast<float*>(take(3ull * BH * d.T * d.D * 4));
   w.bf = dtype == ISA_DTYPE_F32 ? reinterpret_cast<__nv_bfloat16*>(take(3ull * BH * d.S * d.D * 2)) : nullptr;
-  w.s_src = reinterpret_cast<double*>(take(8ull * BH * d.T * d.t_src));
+  w.s_new = reinterpret_cast<double*>(take(8ull * BH * d.T * d.t_new));
+  w.qsum = reinterpret_cast<double*>(take(8ull * BH * d.D));
+  w.flags = reinterpret_cast<uint8_t*>(take((size_t)BH * (d.T > d.t_ctx ? d.T : d.t_ctx)));
   w.ctx = reinterpret_cast<double*>(take(8ull * BH * d.t_ctx));
   w.sel = reinterpret_cast<int*>(take(4ull * BH * d.k_ctx));
   w.kv_blk = reinterpret_cast<int*>(take(4ull * BH * d.t_new));
@@ -289,28 +293,54 @@ int run_pool(const IsaShape* sh, const Dims& d, const void* q, const void* k, co
   return ISA_OK;
 }
 
-size_t rank_smem(int n) { return (size_t)n * (8 + 4 + 1) + 16; }
-
-int set_rank_smem(size_t bytes) {
-  static size_t cur_topk = 48 * 1024, cur_split = 48 * 1024, cur_mask = 48 * 1024;
-  (void)cur_mask;
-  if (bytes > cur_topk) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::topk_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    cur_topk = bytes;
-  }
-  if (bytes > cur_split) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    cur_split = bytes;
+// Dynamic shared memory opt-in (once per kernel, grown on demand).
+int ensure_smem(const void* fn, size_t bytes, size_t* cur) {
+  if (bytes > *cur) {
+    ISA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    *cur = bytes;
   }
   return ISA_OK;
 }
 
-int set_mask_smem(size_t bytes) {
+// Stable top-`kth` selection of each row of a (rows, n) fp64 matrix into
+// ascending kept / dropped index lists (rank flags + compaction).
+int select_rows(const double* vals, int rows, int n, int kth, uint8_t* flags, int* kept, int64_t* kept64,
+                int* dropped, int64_t* dropped64, cudaStream_t st) {
+  static size_t cur_rank = 48 * 1024, cur_comp = 48 * 1024;
+  int rc;
+  if ((rc = ensure_smem((const void*)isa::rank_flags_kernel, (size_t)n * 8, &cur_rank))) return rc;
+  if ((rc = ensure_smem((const void*)isa::compact_kernel, (size_t)n * 4, &cur_comp))) return rc;
+  isa::rank_flags_kernel<<<dim3((n + 255) / 256, rows), 256, (size_t)n * 8, st>>>(vals, n, kth, flags);
+  ISA_LAUNCHED("rank_flags_kernel");
+  isa::compact_kernel<<<rows, 1024, (size_t)n * 4, st>>>(flags, n, kth, kept, kept64, dropped, dropped64);
+  ISA_LAUNCHED("compact_kernel");
+  return ISA_OK;
+}
+
+int launch_sharpness(const double* s, long long stride, int rows, int n, int softmax_first, double* out,
+                     cudaStream_t st) {
+  const unsigned g = (unsigned)((rows + 7) / 8);
+  if (n <= 512)
+    isa::sharpness_kernel<16><<<g, 256, 0, st>>>(s, stride, rows, n, softmax_first, out);
+  else if (n <= 1024)
+    isa::sharpness_kernel<32><<<g, 256, 0, st>>>(s, stride, rows, n, softmax_first, out);
+  else if (n <= 2048)
+    isa::sharpness_kernel<64><<<g, 256, 0, st>>>(s, stride, rows, n, softmax_first, out);
+  else
+    return fail(ISA_ERR_CONFIG, "source blocks %d > 2048 not supported", n);
+  ISA_LAUNCHED("sharpness_kernel");
+  return ISA_OK;
+}
+
+int launch_mask(const double* scores, int rows, int n, const int* flat, int n_flat, int T, int k, int W,
+                int* mask_idx, int64_t* mask64, uint32_t* bits, cudaStream_t st) {
   static size_t cur = 48 * 1024;
-  if (bytes > cur) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::block_mask_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    cur = bytes;
-  }
+  const size_t sm = 4 * ((size_t)n * 8 + (size_t)W * 4);
+  int rc;
+  if ((rc = ensure_smem((const void*)isa::block_mask_kernel, sm, &cur))) return rc;
+  isa::block_mask_kernel<<<(rows + 3) / 4, 128, sm, st>>>(scores, rows, n, flat, n_flat, T, k, W, mask_idx, mask64,
+                                                          bits);
+  ISA_LAUNCHED("block_mask_kernel");
   return ISA_OK;
 }
 
@@ -323,21 +353,18 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   float* qc = w.means;
   float* kc = w.means + BH * d.T * d.D;
   float* vc = w.means + 2 * BH * d.T * d.D;
-  // ---- stage 1: coarse
+  // ---- stage 1: coarse (pooled means, context saliency)
   if ((rc = run_pool(sh, d, q, k, v, w.means, w.bf, err, st))) return rc;
   const bool need_scores = !pinned;
-  if (need_scores) {
-    dim3 g((d.t_src + 63) / 64, (d.T + 63) / 64, d.BH);
-    isa::coarse_src_kernel<<<g, 256, 0, st>>>(qc, kc, d.T, d.t_src, d.D, d.scale, w.s_src);
-    ISA_LAUNCHED("coarse_src_kernel");
-    if (d.t_ctx) {
-      isa::ctx_score_kernel<<<d.BH, 256, d.D * sizeof(double), st>>>(qc, kc, d.T, d.t_src, d.t_ctx, d.D, d.scale,
-                                                                      w.ctx);
-      ISA_LAUNCHED("ctx_score_kernel");
-    }
+  if (need_scores && d.t_ctx) {
+    isa::qsum_kernel<<<d.BH, d.D, 0, st>>>(qc, d.T, d.t_src, d.D, w.qsum);
+    ISA_LAUNCHED("qsum_kernel");
+    isa::ctx_score_kernel<<<dim3((d.t_ctx + 7) / 8, d.BH), 256, 0, st>>>(w.qsum, kc, d.T, d.t_src, d.t_ctx, d.D,
+                                                                         d.scale, w.ctx);
+    ISA_LAUNCHED("ctx_score_kernel");
   }
   record(ev, 1, st);
-  // ---- stage 2: select
+  // ---- stage 2: select (context top-k, K_new block table, fp64 scores vs K_new, centroids)
   if (pinned) {
     if (d.k_ctx) {
       if (!pinned->selection) return fail(ISA_ERR_CONTRACT, "pinned routing lacks selection");
@@ -345,13 +372,17 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
       ISA_LAUNCHED("narrow_kernel");
     }
   } else if (d.k_ctx) {
-    size_t sm = rank_smem(d.t_ctx);
-    if ((rc = set_rank_smem(sm))) return rc;
-    isa::topk_rank_kernel<<<d.BH, 1024, sm, st>>>(w.ctx, d.t_ctx, d.k_ctx, w.sel, ro ? ro->selection : nullptr);
-    ISA_LAUNCHED("topk_rank_kernel");
+    if ((rc = select_rows(w.ctx, d.BH, d.t_ctx, d.k_ctx, w.flags, w.sel, ro ? ro->selection : nullptr, nullptr,
+                          nullptr, st)))
+      return rc;
   }
   isa::kvblk_from_sel_kernel<<<d.BH, 256, 0, st>>>(w.sel, d.t_src, d.k_ctx, w.kv_blk, w.ctx_short);
   ISA_LAUNCHED("kvblk_from_sel_kernel");
+  if (need_scores) {
+    dim3 g((d.t_new + 63) / 64, (d.T + 63) / 64, d.BH);
+    isa::coarse_kernel<<<g, 256, 0, st>>>(qc, kc, w.kv_blk, d.T, d.t_new, d.D, d.scale, w.s_new);
+    ISA_LAUNCHED("coarse_kernel");
+  }
   if (d.n_flat) {
     isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};
     isa::centroid_kernel<<<dim3(d.tn_pad, d.BH), d.D, 0, st>>>(kc, vc, w.kv_blk, d.T, d.t_new, d.tn_pad, d.D, seg,
@@ -373,30 +404,25 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
     if (d.n_flat) {
       if (!pinned->mask) return fail(ISA_ERR_CONTRACT, "pinned routing lacks mask");
       isa::narrow_kernel<<<grid1d(BH * d.n_flat, 256), 256, 0, st>>>(pinned->flat, w.flat, BH * d.n_flat);
+      ISA_LAUNCHED("narrow_kernel");
       isa::narrow_kernel<<<grid1d(BH * d.n_flat * d.k, 256), 256, 0, st>>>(pinned->mask, w.mask,
                                                                          BH * d.n_flat * d.k);
+      ISA_LAUNCHED("narrow_kernel");
       isa::bits_from_mask_kernel<<<BH * d.n_flat, 128, 0, st>>>(w.mask, d.k, d.W, w.bits);
       ISA_LAUNCHED("bits_from_mask_kernel");
     }
   } else {
-    isa::sharpness_kernel<<<(unsigned)((BH * d.T + 7) / 8), 256, 0, st>>>(w.s_src, (int)(BH * d.T), d.t_src,
-                                                                          kn->softmax_first, w.sharpness);
-    ISA_LAUNCHED("sharpness_kernel");
-    size_t sm = rank_smem(d.T);
-    if ((rc = set_rank_smem(sm))) return rc;
-    isa::split_kernel<<<d.BH, 1024, sm, st>>>(w.sharpness, d.T, d.n_flat, w.sharp, w.flat, ro ? ro->sharp : nullptr,
-                                              ro ? ro->flat : nullptr);
-    ISA_LAUNCHED("split_kernel");
+    if ((rc = launch_sharpness(w.s_new, d.t_new, (int)(BH * d.T), d.t_src, kn->softmax_first, w.sharpness, st)))
+      return rc;
+    if ((rc = select_rows(w.sharpness, d.BH, d.T, d.n_sharp, w.flags, w.sharp, ro ? ro->sharp : nullptr, w.flat,
+                          ro ? ro->flat : nullptr, st)))
+      return rc;
     if (ro && ro->sharpness)
       ISA_CUDA(cudaMemcpyAsync(ro->sharpness, w.sharpness, 8ull * BH * d.T, cudaMemcpyDeviceToDevice, st));
     if (d.n_flat) {
-      size_t sm2 = 4 * ((size_t)d.t_new * 8 + (size_t)d.W * 4);
-      if ((rc = set_mask_smem(sm2))) return rc;
-      const int rows = (int)(BH * d.n_flat);
-      isa::block_mask_kernel<<<(rows + 3) / 4, 128, sm2, st>>>(
-          nullptr, rows, w.s_src, qc, kc, w.flat, w.kv_blk, d.T, d.t_src, d.n_flat, d.D, d.scale, d.t_new, d.k,
-          d.W, w.mask, ro ? ro->mask : nullptr, w.bits);
-      ISA_LAUNCHED("block_mask_kernel");
+      if ((rc = launch_mask(w.s_new, (int)(BH * d.n_flat), d.t_new, w.flat, d.n_flat, d.T, d.k, d.W, w.mask,
+                            ro ? ro->mask : nullptr, w.bits, st)))
+        return rc;
     }
   }
   if (pinned && ro) {
@@ -555,48 +581,40 @@ int isa_pool_means(const IsaShape* shape, const void* q, const void* k, const vo
 
 int isa_topk_rows_f64(const double* scores, int32_t rows, int32_t n, int32_t k, int64_t* out_idx, int32_t method,
                       void* stream) {
+  g_launches = 0;
   if (rows < 0 || n < 1 || k < 0 || k > n) return fail(ISA_ERR_CONFIG, "bad topk geometry");
   if (rows == 0 || k == 0) return ISA_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int rc;
   if (method == 0) {
-    size_t sm = rank_smem(n);
-    if ((rc = set_rank_smem(sm))) return rc;
-    isa::topk_rank_kernel<<<rows, 1024, sm, st>>>(scores, n, k, nullptr, out_idx);
-    ISA_LAUNCHED("topk_rank_kernel");
-  } else {
-    const int W = (n + 31) / 32;
-    size_t sm2 = 4 * ((size_t)n * 8 + (size_t)W * 4);
-    if ((rc = set_mask_smem(sm2))) return rc;
-    isa::block_mask_kernel<<<(rows + 3) / 4, 128, sm2, st>>>(scores, rows, nullptr, nullptr, nullptr, nullptr,
-                                                              nullptr, 0, 0, 1, 0, 1.0, n, k, W, nullptr,
-                                                              out_idx, nullptr);
-    ISA_LAUNCHED("block_mask_kernel");
+    uint8_t* flags = nullptr;
+    ISA_CUDA(cudaMallocAsync(&flags, (size_t)rows * n, st));
+    int rc = select_rows(scores, rows, n, k, flags, nullptr, out_idx, nullptr, nullptr, st);
+    cudaFreeAsync(flags, st);
+    return rc;
   }
-  return ISA_OK;
+  const int W = (n + 31) / 32;
+  return launch_mask(scores, rows, n, nullptr, 1, 0, k, W, nullptr, out_idx, nullptr, st);
 }
 
 int isa_sharpness_rows_f64(const double* s, int32_t rows, int32_t n, int32_t softmax_first, double* out,
                            void* stream) {
+  g_launches = 0;
   if (rows < 0 || n < 1) return fail(ISA_ERR_CONFIG, "bad sharpness geometry");
   if (rows == 0) return ISA_OK;
-  isa::sharpness_kernel<<<(rows + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(s, rows, n, softmax_first,
-                                                                                      out);
-  ISA_LAUNCHED("sharpness_kernel");
-  return ISA_OK;
+  return launch_sharpness(s, n, rows, n, softmax_first, out, static_cast<cudaStream_t>(stream));
 }
 
 int isa_split_rows_f64(const double* m, int32_t rows, int32_t n, int32_t n_flat, int64_t* sharp, int64_t* flat,
                        void* stream) {
+  g_launches = 0;
   if (rows < 0 || n < 1 || n_flat < 0 || n_flat > n) return fail(ISA_ERR_CONFIG, "bad split geometry");
   if (rows == 0) return ISA_OK;
-  int rc;
-  size_t sm = rank_smem(n);
-  if ((rc = set_rank_smem(sm))) return rc;
-  isa::split_kernel<<<rows, 1024, sm, static_cast<cudaStream_t>(stream)>>>(
-      m, n, n_flat, nullptr, nullptr, sharp, flat);
-  ISA_LAUNCHED("split_kernel");
-  return ISA_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* flags = nullptr;
+  ISA_CUDA(cudaMallocAsync(&flags, (size_t)rows * n, st));
+  int rc = select_rows(m, rows, n, n - n_flat, flags, nullptr, sharp, nullptr, flat, st);
+  cudaFreeAsync(flags, st);
+  return rc;
 }
 
 }  // extern "C"

@@ -33,38 +33,46 @@ __device__ __forceinline__ bool ranks_before(double a, int ia, double b, int ib)
 }
 
 // ----------------------------------------------------------------------------
-// K1: block means of Q, K, V (fp64 sums over valid rows -> fp32), finiteness
-// flag, and (fp32 inputs) the bf16 copy consumed by the TMA attention kernels.
-// grid (T, BH, 3), block 256. One CTA = one 64-row block of one tensor.
+// K1: block means of Q, K, V (fp64 sums over valid rows -> fp32; bit-identical
+// to tensor.py:115-119 whenever the 64-term fp64 sum is exact, always for bf16
+// inputs), finiteness flag, and (fp32 inputs) the bf16 copy consumed by the TMA
+// attention kernels. One warp per 64-row block: lanes own 8 consecutive
+// columns (16-byte loads), D/8 lanes per row, 32/(D/8) rows per load wave,
+// 8 waves unrolled for memory-level parallelism. grid (ceil(T/4), BH, 3).
 // ----------------------------------------------------------------------------
 template <typename Tin, int D>
-__global__ void __launch_bounds__(256) pool_means_kernel(const Tin* __restrict__ q, const Tin* __restrict__ k,
+__global__ void __launch_bounds__(128) pool_means_kernel(const Tin* __restrict__ q, const Tin* __restrict__ k,
                                                          const Tin* __restrict__ v, long long sb, long long sh,
                                                          long long ss, int H, SegInfo seg, int T,
                                                          float* __restrict__ means,  // [3][BH][T][D]
                                                          __nv_bfloat16* __restrict__ bf_copy,  // [3][BH][S][D] or null
                                                          int S, int* __restrict__ err) {
-  constexpr int VEC = 8;                    // elements per thread-load
-  constexpr int LPR = D / VEC;              // threads per row
-  constexpr int RPAR = 256 / LPR;           // rows in flight
-  __shared__ double part[RPAR][D + 1];
-  const int u = blockIdx.x, bh = blockIdx.y, which = blockIdx.z;
+  constexpr int VEC = 8;
+  constexpr int LPR = D / VEC;     // lanes per row
+  constexpr int RPW = 32 / LPR;    // rows per warp wave
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.x * 4 + warp, bh = blockIdx.y, which = blockIdx.z;
+  if (u >= T) return;
   const Tin* x = which == 0 ? q : (which == 1 ? k : v);
   const int b = bh / H, h = bh % H;
   const int tok0 = seg.tok0(u), valid = seg.valid(u);
-  const int col = (threadIdx.x % LPR) * VEC;
-  const int r0 = threadIdx.x / LPR;
+  const int col = (lane % LPR) * VEC;
+  const int r0 = lane / LPR;
   double acc[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) acc[e] = 0.0;
   bool finite = true;
-  const Tin* base = x + b * sb + h * sh;
-  for (int r = r0; r < valid; r += RPAR) {
-    const Tin* rowp = base + (long long)(tok0 + r) * ss + col;
+  const Tin* base = x + b * sb + h * sh + (long long)tok0 * ss + col;
+  constexpr int WAVES = 64 / RPW;
+#pragma unroll 8
+  for (int w = 0; w < WAVES; ++w) {
+    const int r = r0 + w * RPW;
+    if (r >= valid) break;
+    const Tin* rowp = base + (long long)r * ss;
     float f[VEC];
     if constexpr (sizeof(Tin) == 2) {
-      const uint4 w = *reinterpret_cast<const uint4*>(rowp);
-      const __nv_bfloat162* hw = reinterpret_cast<const __nv_bfloat162*>(&w);
+      const uint4 wv = __ldg(reinterpret_cast<const uint4*>(rowp));
+      const __nv_bfloat162* hw = reinterpret_cast<const __nv_bfloat162*>(&wv);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 t = __bfloat1622float2(hw[e]);
@@ -72,21 +80,21 @@ __global__ void __launch_bounds__(256) pool_means_kernel(const Tin* __restrict__
         f[2 * e + 1] = t.y;
       }
     } else {
-      const float4 a = *reinterpret_cast<const float4*>(rowp);
-      const float4 c = *reinterpret_cast<const float4*>(rowp + 4);
+      const float4 a = __ldg(reinterpret_cast<const float4*>(rowp));
+      const float4 c = __ldg(reinterpret_cast<const float4*>(rowp + 4));
       f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
       f[4] = c.x; f[5] = c.y; f[6] = c.z; f[7] = c.w;
       if (bf_copy) {
-        uint4 w;
+        uint4 wv;
         __nv_bfloat162 t0 = __floats2bfloat162_rn(f[0], f[1]);
         __nv_bfloat162 t1 = __floats2bfloat162_rn(f[2], f[3]);
         __nv_bfloat162 t2 = __floats2bfloat162_rn(f[4], f[5]);
         __nv_bfloat162 t3 = __floats2bfloat162_rn(f[6], f[7]);
-        w.x = *reinterpret_cast<uint32_t*>(&t0);
-        w.y = *reinterpret_cast<uint32_t*>(&t1);
-        w.z = *reinterpret_cast<uint32_t*>(&t2);
-        w.w = *reinterpret_cast<uint32_t*>(&t3);
-        *reinterpret_cast<uint4*>(bf_copy + (((long long)which * (gridDim.y) + bh) * S + tok0 + r) * D + col) = w;
+        wv.x = *reinterpret_cast<uint32_t*>(&t0);
+        wv.y = *reinterpret_cast<uint32_t*>(&t1);
+        wv.z = *reinterpret_cast<uint32_t*>(&t2);
+        wv.w = *reinterpret_cast<uint32_t*>(&t3);
+        *reinterpret_cast<uint4*>(bf_copy + (((long long)which * gridDim.y + bh) * S + tok0 + r) * D + col) = wv;
       }
     }
 #pragma unroll
@@ -95,41 +103,56 @@ __global__ void __launch_bounds__(256) pool_means_kernel(const Tin* __restrict__
       acc[e] += static_cast<double>(f[e]);
     }
   }
+  // combine the RPW row-groups of the warp (lanes with equal column): fixed tree order
 #pragma unroll
-  for (int e = 0; e < VEC; ++e) part[r0][col + e] = acc[e];
-  if (!finite && err) atomicOr(err, 1);
-  __syncthreads();
-  float* out = means + (((long long)which * gridDim.y + bh) * T + u) * D;
-  for (int c = threadIdx.x; c < D; c += 256) {
-    double s = 0.0;
-#pragma unroll 4
-    for (int r = 0; r < RPAR; ++r) s += part[r][c];  // fixed order: deterministic
-    out[c] = static_cast<float>(s / static_cast<double>(valid));
+  for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+  if (__any_sync(0xffffffffu, !finite) && lane == 0 && err) atomicOr(err, 1);
+  if (lane < LPR) {
+    float* out = means + (((long long)which * gridDim.y + bh) * T + u) * D + col;
+    float4 o0, o1;
+    const double inv = static_cast<double>(valid);
+    o0.x = static_cast<float>(acc[0] / inv); o0.y = static_cast<float>(acc[1] / inv);
+    o0.z = static_cast<float>(acc[2] / inv); o0.w = static_cast<float>(acc[3] / inv);
+    o1.x = static_cast<float>(acc[4] / inv); o1.y = static_cast<float>(acc[5] / inv);
+    o1.z = static_cast<float>(acc[6] / inv); o1.w = static_cast<float>(acc[7] / inv);
+    reinterpret_cast<float4*>(out)[0] = o0;
+    reinterpret_cast<float4*>(out)[1] = o1;
   }
 }
 
 // ----------------------------------------------------------------------------
-// K2a: S_src[bh][u][j] = scale * <qc_u, kc_j>, u < T, j < t_src, float64.
-// 64x64 tiles, 256 threads, 4x4 outputs per thread. grid (ceil(t_src/64),
-// ceil(T/64), BH).
+// K2: S_new[bh][u][j] = scale * <qc_u, kc_{kv_blk[j]}> for every query block u
+// < T and every K_new block j < t_new, float64 (pipeline.py:180-182 for the
+// source columns; pipeline.py:221-223 s_flat for the selected context
+// columns, which equal the kc rows of the selected blocks, pipeline.py:210).
+// 64x64 tiles, 256 threads, 4x4 outputs per thread, sequential fp64 FMA over
+// d. kv_blk == null means identity columns. grid (ceil(n/64), ceil(T/64), BH).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) coarse_src_kernel(const float* __restrict__ qc, const float* __restrict__ kc,
-                                                         int T, int t_src, int D, double scale,
-                                                         double* __restrict__ s_src) {
+__global__ void __launch_bounds__(256) coarse_kernel(const float* __restrict__ qc, const float* __restrict__ kc,
+                                                     const int* __restrict__ kv_blk, int T, int n, int D,
+                                                     double scale, double* __restrict__ s_out) {
   __shared__ double As[16][64 + 1];
   __shared__ double Bs[16][64 + 1];
+  __shared__ int colrow[64];
   const int bh = blockIdx.z;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
   const float* qb = qc + (long long)bh * T * D;
   const float* kb = kc + (long long)bh * T * D;
+  if (threadIdx.x < 64) {
+    const int j = j0 + threadIdx.x;
+    colrow[threadIdx.x] = j < n ? (kv_blk ? kv_blk[(long long)bh * n + j] : j) : -1;
+  }
+  __syncthreads();
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   double acc[4][4] = {};
   for (int d0 = 0; d0 < D; d0 += 16) {
     for (int e = threadIdx.x; e < 64 * 16; e += 256) {
       const int r = e / 16, dd = e % 16;
-      const int gi = i0 + r, gj = j0 + r;
+      const int gi = i0 + r, gj = colrow[r];
       As[dd][r] = gi < T ? static_cast<double>(qb[(long long)gi * D + d0 + dd]) : 0.0;
-      Bs[dd][r] = gj < t_src ? static_cast<double>(kb[(long long)gj * D + d0 + dd]) : 0.0;
+      Bs[dd][r] = gj >= 0 ? static_cast<double>(kb[(long long)gj * D + d0 + dd]) : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -154,39 +177,49 @@ __global__ void __launch_bounds__(256) coarse_src_kernel(const float* __restrict
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int gj = j0 + tx + 16 * c;
-      if (gj < t_src) s_src[((long long)bh * T + gi) * t_src + gj] = scale * acc[r][c];
+      if (gj < n) s_out[((long long)bh * T + gi) * n + gj] = scale * acc[r][c];
     }
   }
 }
 
 // ----------------------------------------------------------------------------
 // K2b: context saliency = mean over source query blocks of the scaled coarse
-// score (coarse.py:155), computed through linearity:
+// score (coarse.py:155), through linearity:
 //   ctx[c] = scale * <sum_{i<t_src} qc_i, kc_{t_src+c}> / t_src   (fp64).
-// grid BH, block 256.
+// qsum_kernel: grid (BH), block D: column sums in fp64 (coalesced over d).
+// ctx_score_kernel: grid (ceil(t_ctx/8), BH), 8 warps, one context column per
+// warp (lanes over d).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) ctx_score_kernel(const float* __restrict__ qc, const float* __restrict__ kc,
-                                                        int T, int t_src, int t_ctx, int D, double scale,
-                                                        double* __restrict__ ctx) {
-  extern __shared__ double qsum[];  // [D]
+__global__ void qsum_kernel(const float* __restrict__ qc, int T, int t_src, int D, double* __restrict__ qsum) {
   const int bh = blockIdx.x;
   const float* qb = qc + (long long)bh * T * D;
-  const float* kb = kc + (long long)bh * T * D;
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    double s = 0.0;
-    for (int i = 0; i < t_src; ++i) s += static_cast<double>(qb[(long long)i * D + d]);
-    qsum[d] = s;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = 0;
+    for (; i + 4 <= t_src; i += 4) {
+      s0 += static_cast<double>(qb[(long long)(i + 0) * D + d]);
+      s1 += static_cast<double>(qb[(long long)(i + 1) * D + d]);
+      s2 += static_cast<double>(qb[(long long)(i + 2) * D + d]);
+      s3 += static_cast<double>(qb[(long long)(i + 3) * D + d]);
+    }
+    for (; i < t_src; ++i) s0 += static_cast<double>(qb[(long long)i * D + d]);
+    qsum[(long long)bh * D + d] = (s0 + s1) + (s2 + s3);
   }
-  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) ctx_score_kernel(const double* __restrict__ qsum, const float* __restrict__ kc,
+                                                        int T, int t_src, int t_ctx, int D, double scale,
+                                                        double* __restrict__ ctx) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c = warp; c < t_ctx; c += blockDim.x / 32) {
-    const float* kr = kb + (long long)(t_src + c) * D;
-    double s = 0.0;
-    for (int d = lane; d < D; d += 32) s = fma(qsum[d], static_cast<double>(kr[d]), s);
+  const int c = blockIdx.x * 8 + warp, bh = blockIdx.y;
+  if (c >= t_ctx) return;
+  const float* kr = kc + ((long long)bh * T + t_src + c) * D;
+  const double* qs = qsum + (long long)bh * D;
+  double s = 0.0;
+  for (int d = lane; d < D; d += 32) s = fma(qs[d], static_cast<double>(kr[d]), s);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) ctx[(long long)bh * t_ctx + c] = scale * s / static_cast<double>(t_src);
-  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) ctx[(long long)bh * t_ctx + c] = scale * s / static_cast<double>(t_src);
 }
 
 // ----------------------------------------------------------------------------
@@ -223,36 +256,57 @@ __device__ int block_exclusive_scan(const uint8_t* flags, int* pos, int n, int* 
 }
 
 // ----------------------------------------------------------------------------
-// K3: per row, keep the k best of n fp64 scores (desc, ties -> lower index),
-// emitted ascending (coarse.py:130-136). One CTA per row; rank by counting.
-// Used for context selection (coarse.py:139-157) and as the explicit-score
-// test primitive. Optionally also writes the K_new block table.
-// dyn smem: n doubles + n bytes + n ints.
+// Stable rank selection (coarse.py:130-136, 196-200), parallel over elements:
+// element i of a row is kept iff rank_i < kth where rank_i = #{j : (x_j, j)
+// ranks before (x_i, i)} under (value desc, index asc). Values are mapped to
+// order-preserving uint64 keys (-0.0 folded onto +0.0, NaN lowest) so each
+// comparison is integer. grid (ceil(n/256), rows), block 256,
+// dyn smem n * 8 bytes.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) topk_rank_kernel(const double* __restrict__ scores, int n, int k,
-                                                         int* __restrict__ out_idx,    // [rows][k] (int32) or null
-                                                         int64_t* __restrict__ out_idx64) {  // [rows][k] or null
-  extern __shared__ __align__(16) uint8_t sm[];
-  double* sv = reinterpret_cast<double*>(sm);
-  int* pos = reinterpret_cast<int*>(sm + sizeof(double) * n);
-  uint8_t* flag = reinterpret_cast<uint8_t*>(sm + sizeof(double) * n + sizeof(int) * n);
+__device__ __forceinline__ unsigned long long order_key(double x) {
+  if (x != x) return 0ull;             // NaN ranks last
+  if (x == 0.0) x = 0.0;               // -0.0 == +0.0 (numpy comparison semantics)
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void __launch_bounds__(256) rank_flags_kernel(const double* __restrict__ vals, int n, int kth,
+                                                         uint8_t* __restrict__ flags) {
+  extern __shared__ unsigned long long keys[];
+  const int row = blockIdx.y;
+  const double* v = vals + (long long)row * n;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) keys[j] = order_key(v[j]);
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long ki = keys[i];
+  int rank = 0;
+  int j = 0;
+  for (; j < i; ++j) rank += keys[j] >= ki;  // earlier index wins ties
+  for (++j; j < n; ++j) rank += keys[j] > ki;
+  flags[(long long)row * n + i] = rank < kth;
+}
+
+// Ascending compaction of the kept (flag = 1) and dropped (flag = 0) indices of
+// each row. grid rows, block 1024.
+__global__ void __launch_bounds__(1024) compact_kernel(const uint8_t* __restrict__ flags, int n, int n_kept,
+                                                       int* __restrict__ kept, int64_t* __restrict__ kept64,
+                                                       int* __restrict__ dropped, int64_t* __restrict__ dropped64) {
+  extern __shared__ int pos[];  // n ints
   __shared__ int scratch[40];
   const int row = blockIdx.x;
-  const double* sr = scores + (long long)row * n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sv[i] = sr[i];
-  __syncthreads();
+  const uint8_t* f = flags + (long long)row * n;
+  block_exclusive_scan(f, pos, n, scratch);
+  const int n_drop = n - n_kept;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double a = sv[i];
-    int rank = 0;
-    for (int j = 0; j < n; ++j) rank += ranks_before(sv[j], j, a, i) ? 1 : 0;
-    flag[i] = rank < k;
-  }
-  __syncthreads();
-  block_exclusive_scan(flag, pos, n, scratch);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    if (flag[i]) {
-      if (out_idx) out_idx[(long long)row * k + pos[i]] = i;
-      if (out_idx64) out_idx64[(long long)row * k + pos[i]] = i;
+    if (f[i]) {
+      const int p = pos[i];
+      if (kept) kept[(long long)row * n_kept + p] = i;
+      if (kept64) kept64[(long long)row * n_kept + p] = i;
+    } else {
+      const int p = i - pos[i];
+      if (dropped) dropped[(long long)row * n_drop + p] = i;
+      if (dropped64) dropped64[(long long)row * n_drop + p] = i;
     }
   }
 }
@@ -261,36 +315,49 @@ __global__ void __launch_bounds__(1024) topk_rank_kernel(const double* __restric
 // K4a: sharpness of every query block: population variance over the source
 // columns of the row-softmax (softmax_first) or of the raw scaled scores
 // (coarse.py:193-195; softmax_rows util.py:32-40; numpy var = mean((x-mean)^2)).
-// One warp per row. grid ceil(rows/8), block 256.
+// One warp per row; the row lives in registers (MAXV values per lane), so the
+// fp64 exp runs once per element. grid ceil(rows/8), block 256.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) sharpness_kernel(const double* __restrict__ s, int rows, int n,
-                                                        int softmax_first, double* __restrict__ out) {
+template <int MAXV>
+__global__ void __launch_bounds__(256) sharpness_kernel(const double* __restrict__ s, long long row_stride, int rows,
+                                                        int n, int softmax_first, double* __restrict__ out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
   if (row >= rows) return;
-  const double* x = s + (long long)row * n;
+  const double* x = s + (long long)row * row_stride;
+  double val[MAXV];
   double mx = -INFINITY;
-  for (int j = lane; j < n; j += 32) mx = fmax(mx, x[j]);
+#pragma unroll
+  for (int m = 0; m < MAXV; ++m) {
+    const int j = lane + 32 * m;
+    val[m] = j < n ? x[j] : -INFINITY;
+    mx = fmax(mx, val[m]);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  double z = 1.0;
   if (softmax_first) {
     double se = 0.0;
-    for (int j = lane; j < n; j += 32) se += exp(x[j] - mx);
+#pragma unroll
+    for (int m = 0; m < MAXV; ++m) {
+      val[m] = (lane + 32 * m < n) ? exp(val[m] - mx) : 0.0;
+      se += val[m];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-    z = se;
+#pragma unroll
+    for (int m = 0; m < MAXV; ++m) val[m] = val[m] / se;
   }
-  auto val = [&](double xv) { return softmax_first ? exp(xv - mx) / z : xv; };
   double sum = 0.0;
-  for (int j = lane; j < n; j += 32) sum += val(x[j]);
+#pragma unroll
+  for (int m = 0; m < MAXV; ++m) sum += (lane + 32 * m < n) ? val[m] : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   const double mean = sum / n;
   double sq = 0.0;
-  for (int j = lane; j < n; j += 32) {
-    const double d = val(x[j]) - mean;
-    sq += d * d;
+#pragma unroll
+  for (int m = 0; m < MAXV; ++m) {
+    const double dv = val[m] - mean;
+    sq += (lane + 32 * m < n) ? dv * dv : 0.0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
@@ -298,99 +365,50 @@ __global__ void __launch_bounds__(256) sharpness_kernel(const double* __restrict
 }
 
 // ----------------------------------------------------------------------------
-// K4b: split (coarse.py:196-200): order = argsort(-M, stable); the first
-// T - n_flat stay sharp. Both lists ascending. One CTA per row.
-// dyn smem: n doubles + n ints + n bytes.
-// ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) split_kernel(const double* __restrict__ m, int n, int n_flat,
-                                                     int* __restrict__ sharp, int* __restrict__ flat,
-                                                     int64_t* __restrict__ sharp64, int64_t* __restrict__ flat64) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  double* sv = reinterpret_cast<double*>(sm);
-  int* pos = reinterpret_cast<int*>(sm + sizeof(double) * n);
-  uint8_t* flag = reinterpret_cast<uint8_t*>(sm + sizeof(double) * n + sizeof(int) * n);
-  __shared__ int scratch[40];
-  const int row = blockIdx.x;
-  const int n_sharp = n - n_flat;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sv[i] = m[(long long)row * n + i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double a = sv[i];
-    int rank = 0;
-    for (int j = 0; j < n; ++j) rank += ranks_before(sv[j], j, a, i) ? 1 : 0;
-    flag[i] = rank < n_sharp;
-  }
-  __syncthreads();
-  block_exclusive_scan(flag, pos, n, scratch);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    if (flag[i]) {
-      const int p = pos[i];
-      if (sharp) sharp[(long long)row * n_sharp + p] = i;
-      if (sharp64) sharp64[(long long)row * n_sharp + p] = i;
-    } else {
-      const int p = i - pos[i];
-      if (flat) flat[(long long)row * n_flat + p] = i;
-      if (flat64) flat64[(long long)row * n_flat + p] = i;
-    }
-  }
-}
-
-// ----------------------------------------------------------------------------
 // K5: block mask for the flat query blocks (pipeline.py:219-225,
-// coarse.py:160-170): fp64 scores of the flat block's mean query against the
-// means of every K_new block (source columns read from S_src, selected
-// context columns recomputed), top-k by k rounds of warp arg-max (desc, ties ->
-// lower index), emitted ascending plus a membership bitmask (W words).
-// One warp per flat row; 4 warps per CTA. When `explicit_scores` is given the
-// scores are read from it instead ([rows][n]; test primitive).
-// dyn smem: 4 * (n doubles + W words).
+// coarse.py:160-170): the fp64 scores of the flat block against every K_new
+// block are row u of S_new; keep the top k (desc, ties -> lower index) by k
+// rounds of warp arg-max over order-preserving keys in shared memory, emit
+// them ascending plus a membership bitmask (W words) for the Taylor kernel.
+// Row r reads scores + (row_map ? row_map[r] : r) * n. One warp per row,
+// 4 warps per CTA; dyn smem 4 * (n * 8 + W * 4).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) block_mask_kernel(
-    const double* __restrict__ explicit_scores, int rows, const double* __restrict__ s_src,
-    const float* __restrict__ qc, const float* __restrict__ kc, const int* __restrict__ flat,
-    const int* __restrict__ kv_blk, int T, int t_src, int n_flat, int D, double scale, int n, int k, int W,
-    int* __restrict__ mask_idx, int64_t* __restrict__ mask64, uint32_t* __restrict__ member_bits) {
+__global__ void __launch_bounds__(128) block_mask_kernel(const double* __restrict__ scores, int rows, int n,
+                                                         const int* __restrict__ flat, int n_flat, int T, int k,
+                                                         int W, int* __restrict__ mask_idx,
+                                                         int64_t* __restrict__ mask64,
+                                                         uint32_t* __restrict__ member_bits) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 4 + warp;
-  double* sv = reinterpret_cast<double*>(sm) + (long long)warp * n;
+  unsigned long long* sv = reinterpret_cast<unsigned long long*>(sm) + (long long)warp * n;
   uint32_t* bits = reinterpret_cast<uint32_t*>(sm + sizeof(double) * 4 * n) + warp * W;
   if (row >= rows) return;
-  if (explicit_scores) {
-    for (int j = lane; j < n; j += 32) sv[j] = explicit_scores[(long long)row * n + j];
-  } else {
+  long long src_row = row;
+  if (flat) {
     const int bh = row / n_flat, f = row % n_flat;
-    const int u = flat[(long long)bh * n_flat + f];
-    const double* srow = s_src + ((long long)bh * T + u) * t_src;
-    const float* qrow = qc + ((long long)bh * T + u) * D;
-    const int* tab = kv_blk + (long long)bh * n;
-    for (int j = lane; j < t_src; j += 32) sv[j] = srow[j];
-    for (int j = t_src; j < n; ++j) {  // selected context columns: warp-cooperative fp64 dot
-      const float* krow = kc + ((long long)bh * T + tab[j]) * D;
-      double s = 0.0;
-      for (int d = lane; d < D; d += 32) s = fma(static_cast<double>(qrow[d]), static_cast<double>(krow[d]), s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) sv[j] = scale * s;
-    }
+    src_row = (long long)bh * T + flat[(long long)bh * n_flat + f];
   }
+  const double* srow = scores + src_row * n;
+  for (int j = lane; j < n; j += 32) sv[j] = order_key(srow[j]);
   for (int w = lane; w < W; w += 32) bits[w] = 0u;
   __syncwarp();
   for (int r = 0; r < k; ++r) {
-    double best = -INFINITY;
+    unsigned long long best = 0ull;
     int bi = 0x7fffffff;
     for (int j = lane; j < n; j += 32) {
       const bool taken = (bits[j >> 5] >> (j & 31)) & 1u;
-      if (!taken && (bi == 0x7fffffff || ranks_before(sv[j], j, best, bi))) {
-        best = sv[j];
+      const unsigned long long kj = sv[j];
+      if (!taken && (bi == 0x7fffffff || kj > best)) {  // ascending j per lane: ties keep the lower index
+        best = kj;
         bi = j;
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (oi != 0x7fffffff && (bi == 0x7fffffff || ranks_before(ob, oi, best, bi))) {
+      if (oi != 0x7fffffff && (bi == 0x7fffffff || ob > best || (ob == best && oi < bi))) {
         best = ob;
         bi = oi;
       }
