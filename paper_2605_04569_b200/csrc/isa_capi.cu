@@ -265,17 +265,17 @@ void record(const IsaEvents* ev, int i, cudaStream_t st) {
 int run_pool(const IsaShape* sh, const Dims& d, const void* q, const void* k, const void* v, float* means,
              __nv_bfloat16* bf, int32_t* err, cudaStream_t st) {
   isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};
-  dim3 grid(d.T, d.BH, 3);
+  dim3 grid((d.T + 3) / 4, d.BH, 3);
   if (sh->dtype == ISA_DTYPE_BF16) {
     auto* qq = static_cast<const __nv_bfloat16*>(q);
     auto* kk = static_cast<const __nv_bfloat16*>(k);
     auto* vv = static_cast<const __nv_bfloat16*>(v);
     if (d.D == 128)
-      isa::pool_means_kernel<__nv_bfloat16, 128><<<grid, 256, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h,
+      isa::pool_means_kernel<__nv_bfloat16, 128><<<grid, 128, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h,
                                                                        sh->stride_s, d.H, seg, d.T, means, nullptr,
                                                                        d.S, err);
     else
-      isa::pool_means_kernel<__nv_bfloat16, 64><<<grid, 256, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h,
+      isa::pool_means_kernel<__nv_bfloat16, 64><<<grid, 128, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h,
                                                                       sh->stride_s, d.H, seg, d.T, means, nullptr,
                                                                       d.S, err);
   } else {
@@ -283,10 +283,10 @@ int run_pool(const IsaShape* sh, const Dims& d, const void* q, const void* k, co
     auto* kk = static_cast<const float*>(k);
     auto* vv = static_cast<const float*>(v);
     if (d.D == 128)
-      isa::pool_means_kernel<float, 128><<<grid, 256, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h, sh->stride_s,
+      isa::pool_means_kernel<float, 128><<<grid, 128, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h, sh->stride_s,
                                                                d.H, seg, d.T, means, bf, d.S, err);
     else
-      isa::pool_means_kernel<float, 64><<<grid, 256, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h, sh->stride_s,
+      isa::pool_means_kernel<float, 64><<<grid, 128, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h, sh->stride_s,
                                                               d.H, seg, d.T, means, bf, d.S, err);
   }
   ISA_LAUNCHED("pool_means_kernel");
@@ -334,6 +334,21 @@ int launch_sharpness(const double* s, long long stride, int rows, int n, int sof
 
 int launch_mask(const double* scores, int rows, int n, const int* flat, int n_flat, int T, int k, int W,
                 int* mask_idx, int64_t* mask64, uint32_t* bits, cudaStream_t st) {
+  const unsigned g = (unsigned)((rows + 3) / 4);
+#define ISA_MASK_THR(M)                                                                                           \
+  if (n <= 32 * M) {                                                                                             \
+    isa::block_mask_thr_kernel<M><<<g, 128, 0, st>>>(scores, rows, n, flat, n_flat, T, k, W, mask_idx, mask64, bits); \
+    ISA_LAUNCHED("block_mask_thr_kernel");                                                                        \
+    return ISA_OK;                                                                                                \
+  }
+  ISA_MASK_THR(4)
+  ISA_MASK_THR(8)
+  ISA_MASK_THR(12)
+  ISA_MASK_THR(16)
+  ISA_MASK_THR(20)
+  ISA_MASK_THR(24)
+  ISA_MASK_THR(32)
+#undef ISA_MASK_THR
   static size_t cur = 48 * 1024;
   const size_t sm = 4 * ((size_t)n * 8 + (size_t)W * 4);
   int rc;
@@ -357,7 +372,7 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   if ((rc = run_pool(sh, d, q, k, v, w.means, w.bf, err, st))) return rc;
   const bool need_scores = !pinned;
   if (need_scores && d.t_ctx) {
-    isa::qsum_kernel<<<d.BH, d.D, 0, st>>>(qc, d.T, d.t_src, d.D, w.qsum);
+    isa::qsum_kernel<<<dim3(d.D / 32, d.BH), 256, 0, st>>>(qc, d.T, d.t_src, d.D, w.qsum);
     ISA_LAUNCHED("qsum_kernel");
     isa::ctx_score_kernel<<<dim3((d.t_ctx + 7) / 8, d.BH), 256, 0, st>>>(w.qsum, kc, d.T, d.t_src, d.t_ctx, d.D,
                                                                          d.scale, w.ctx);
@@ -379,7 +394,7 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   isa::kvblk_from_sel_kernel<<<d.BH, 256, 0, st>>>(w.sel, d.t_src, d.k_ctx, w.kv_blk, w.ctx_short);
   ISA_LAUNCHED("kvblk_from_sel_kernel");
   if (need_scores) {
-    dim3 g((d.t_new + 63) / 64, (d.T + 63) / 64, d.BH);
+    dim3 g((d.t_new + 127) / 128, (d.T + 127) / 128, d.BH);
     isa::coarse_kernel<<<g, 256, 0, st>>>(qc, kc, w.kv_blk, d.T, d.t_new, d.D, d.scale, w.s_new);
     ISA_LAUNCHED("coarse_kernel");
   }
@@ -593,6 +608,16 @@ int isa_topk_rows_f64(const double* scores, int32_t rows, int32_t n, int32_t k, 
     return rc;
   }
   const int W = (n + 31) / 32;
+  if (method == 2) {  // generic arg-max-rounds kernel (n > 1024 path)
+    static size_t cur = 48 * 1024;
+    const size_t sm = 4 * ((size_t)n * 8 + (size_t)W * 4);
+    int rc;
+    if ((rc = ensure_smem((const void*)isa::block_mask_kernel, sm, &cur))) return rc;
+    isa::block_mask_kernel<<<(rows + 3) / 4, 128, sm, st>>>(scores, rows, n, nullptr, 1, 0, k, W, nullptr, out_idx,
+                                                            nullptr);
+    ISA_LAUNCHED("block_mask_kernel");
+    return ISA_OK;
+  }
   return launch_mask(scores, rows, n, nullptr, 1, 0, k, W, nullptr, out_idx, nullptr, st);
 }
 

@@ -133,51 +133,60 @@ __global__ void __launch_bounds__(128) pool_means_kernel(const Tin* __restrict__
 __global__ void __launch_bounds__(256) coarse_kernel(const float* __restrict__ qc, const float* __restrict__ kc,
                                                      const int* __restrict__ kv_blk, int T, int n, int D,
                                                      double scale, double* __restrict__ s_out) {
-  __shared__ double As[16][64 + 1];
-  __shared__ double Bs[16][64 + 1];
-  __shared__ int colrow[64];
+  // 128x128 output tile per CTA, 16x16 threads with 8x8 outputs each (rows
+  // ty+16r, cols tx+16c: conflict-free shared reads), k-chunks of 8.
+  __shared__ double As[8][128];
+  __shared__ double Bs[8][128];
+  __shared__ int colrow[128];
   const int bh = blockIdx.z;
-  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 128;
   const float* qb = qc + (long long)bh * T * D;
   const float* kb = kc + (long long)bh * T * D;
-  if (threadIdx.x < 64) {
+  if (threadIdx.x < 128) {
     const int j = j0 + threadIdx.x;
     colrow[threadIdx.x] = j < n ? (kv_blk ? kv_blk[(long long)bh * n + j] : j) : -1;
   }
   __syncthreads();
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  double acc[4][4] = {};
-  for (int d0 = 0; d0 < D; d0 += 16) {
-    for (int e = threadIdx.x; e < 64 * 16; e += 256) {
-      const int r = e / 16, dd = e % 16;
-      const int gi = i0 + r, gj = colrow[r];
-      As[dd][r] = gi < T ? static_cast<double>(qb[(long long)gi * D + d0 + dd]) : 0.0;
-      Bs[dd][r] = gj >= 0 ? static_cast<double>(kb[(long long)gj * D + d0 + dd]) : 0.0;
-    }
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+  // loader: thread -> (row = tid / 2, 4 consecutive d) for both operands
+  const int lr = threadIdx.x >> 1, ld = (threadIdx.x & 1) * 4;
+  const int gi = i0 + lr;
+  const int gj = colrow[lr];
+  for (int d0 = 0; d0 < D; d0 += 8) {
+    float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f), b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (gi < T) a4 = *reinterpret_cast<const float4*>(qb + (long long)gi * D + d0 + ld);
+    if (gj >= 0) b4 = *reinterpret_cast<const float4*>(kb + (long long)gj * D + d0 + ld);
+    As[ld + 0][lr] = a4.x; As[ld + 1][lr] = a4.y; As[ld + 2][lr] = a4.z; As[ld + 3][lr] = a4.w;
+    Bs[ld + 0][lr] = b4.x; Bs[ld + 1][lr] = b4.y; Bs[ld + 2][lr] = b4.z; Bs[ld + 3][lr] = b4.w;
     __syncthreads();
 #pragma unroll
-    for (int dd = 0; dd < 16; ++dd) {
-      double a[4], bv[4];
+    for (int dd = 0; dd < 8; ++dd) {
+      double a[8], bv[8];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < 8; ++t) {
         a[t] = As[dd][ty + 16 * t];
         bv[t] = Bs[dd][tx + 16 * t];
       }
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], bv[c], acc[r][c]);
+        for (int c = 0; c < 8; ++c) acc[r][c] = fma(a[r], bv[c], acc[r][c]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int gi = i0 + ty + 16 * r;
-    if (gi >= T) continue;
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + ty + 16 * r;
+    if (i >= T) continue;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int gj = j0 + tx + 16 * c;
-      if (gj < n) s_out[((long long)bh * T + gi) * n + gj] = scale * acc[r][c];
+    for (int c = 0; c < 8; ++c) {
+      const int j = j0 + tx + 16 * c;
+      if (j < n) s_out[((long long)bh * T + i) * n + j] = scale * acc[r][c];
     }
   }
 }
@@ -190,20 +199,28 @@ __global__ void __launch_bounds__(256) coarse_kernel(const float* __restrict__ q
 // ctx_score_kernel: grid (ceil(t_ctx/8), BH), 8 warps, one context column per
 // warp (lanes over d).
 // ----------------------------------------------------------------------------
-__global__ void qsum_kernel(const float* __restrict__ qc, int T, int t_src, int D, double* __restrict__ qsum) {
-  const int bh = blockIdx.x;
-  const float* qb = qc + (long long)bh * T * D;
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int i = 0;
-    for (; i + 4 <= t_src; i += 4) {
-      s0 += static_cast<double>(qb[(long long)(i + 0) * D + d]);
-      s1 += static_cast<double>(qb[(long long)(i + 1) * D + d]);
-      s2 += static_cast<double>(qb[(long long)(i + 2) * D + d]);
-      s3 += static_cast<double>(qb[(long long)(i + 3) * D + d]);
-    }
-    for (; i < t_src; ++i) s0 += static_cast<double>(qb[(long long)i * D + d]);
-    qsum[(long long)bh * D + d] = (s0 + s1) + (s2 + s3);
+__global__ void __launch_bounds__(256) qsum_kernel(const float* __restrict__ qc, int T, int t_src, int D,
+                                                   double* __restrict__ qsum) {
+  // grid (D/32, BH): 8 warps stride over the source rows for 32 columns, then a
+  // fixed-order combine across warps (deterministic).
+  __shared__ double part[8][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = blockIdx.x * 32 + lane, bh = blockIdx.y;
+  const float* qb = qc + (long long)bh * T * D + d;
+  double s0 = 0.0, s1 = 0.0;
+  int i = warp;
+  for (; i + 8 < t_src; i += 16) {
+    s0 += static_cast<double>(qb[(long long)i * D]);
+    s1 += static_cast<double>(qb[(long long)(i + 8) * D]);
+  }
+  if (i < t_src) s0 += static_cast<double>(qb[(long long)i * D]);
+  part[warp][lane] = s0 + s1;
+  __syncthreads();
+  if (warp == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    qsum[(long long)bh * D + d] = t;
   }
 }
 
@@ -319,7 +336,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(const uint8_t* __restrict
 // fp64 exp runs once per element. grid ceil(rows/8), block 256.
 // ----------------------------------------------------------------------------
 template <int MAXV>
-__global__ void __launch_bounds__(256) sharpness_kernel(const double* __restrict__ s, long long row_stride, int rows,
+__global__ void __launch_bounds__(256, MAXV <= 16 ? 3 : 1) sharpness_kernel(const double* __restrict__ s, long long row_stride, int rows,
                                                         int n, int softmax_first, double* __restrict__ out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
@@ -344,8 +361,9 @@ __global__ void __launch_bounds__(256) sharpness_kernel(const double* __restrict
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const double rz = 1.0 / se;
 #pragma unroll
-    for (int m = 0; m < MAXV; ++m) val[m] = val[m] / se;
+    for (int m = 0; m < MAXV; ++m) val[m] = val[m] * rz;
   }
   double sum = 0.0;
 #pragma unroll
@@ -440,6 +458,99 @@ __global__ void __launch_bounds__(128) block_mask_kernel(const double* __restric
     if (w < W && member_bits) member_bits[(long long)row * W + w] = word;
     base += __shfl_sync(0xffffffffu, incl, 31);
   }
+}
+
+// K5 (fast path, n <= 32*MAXM): same selection as block_mask_kernel, by a
+// bitwise threshold search instead of k arg-max rounds. With ordered keys
+// (hi:lo 32-bit halves) the k-th largest key is found MSB-first on hi, then
+// on lo among the hi ties; elements above it are kept and exact key ties are
+// taken in ascending index order (the stable tie rule). Element j of the row
+// is (lane j%32, register j/32), so membership word m is one ballot.
+// ----------------------------------------------------------------------------
+template <int MAXM>
+__global__ void __launch_bounds__(128) block_mask_thr_kernel(const double* __restrict__ scores, int rows, int n,
+                                                             const int* __restrict__ flat, int n_flat, int T, int k,
+                                                             int W, int* __restrict__ mask_idx,
+                                                             int64_t* __restrict__ mask64,
+                                                             uint32_t* __restrict__ member_bits) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 4 + warp;
+  if (row >= rows) return;
+  long long src_row = row;
+  if (flat) {
+    const int bh = row / n_flat, f = row % n_flat;
+    src_row = (long long)bh * T + flat[(long long)bh * n_flat + f];
+  }
+  const double* srow = scores + src_row * n;
+  uint32_t hi[MAXM], lo[MAXM];
+#pragma unroll
+  for (int m = 0; m < MAXM; ++m) {
+    const int j = lane + 32 * m;
+    const unsigned long long key = j < n ? order_key(srow[j]) : 0ull;
+    hi[m] = static_cast<uint32_t>(key >> 32);
+    lo[m] = static_cast<uint32_t>(key);
+  }
+  auto valid = [&](int m) { return lane + 32 * m < n; };
+  // hi threshold: largest th with #(hi >= th) >= k
+  uint32_t th = 0;
+#pragma unroll 1
+  for (int b = 31; b >= 0; --b) {
+    const uint32_t cand = th | (1u << b);
+    int c = 0;
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) c += (valid(m) && hi[m] >= cand) ? 1 : 0;
+    if (__reduce_add_sync(0xffffffffu, c) >= k) th = cand;
+  }
+  int c_gt = 0, c_eq = 0;
+#pragma unroll
+  for (int m = 0; m < MAXM; ++m) {
+    c_gt += (valid(m) && hi[m] > th) ? 1 : 0;
+    c_eq += (valid(m) && hi[m] == th) ? 1 : 0;
+  }
+  c_gt = __reduce_add_sync(0xffffffffu, c_gt);
+  c_eq = __reduce_add_sync(0xffffffffu, c_eq);
+  const int need = k - c_gt;  // >= 1 and <= c_eq
+  uint32_t tl = 0;
+  int need2 = 0;  // ties at exactly (th, tl) to take in index order
+  if (c_eq == need) {
+    tl = 0;
+    need2 = 0x7fffffff;  // every hi tie is kept (lo >= 0 always)
+  } else {
+#pragma unroll 1
+    for (int b = 31; b >= 0; --b) {
+      const uint32_t cand = tl | (1u << b);
+      int c = 0;
+#pragma unroll
+      for (int m = 0; m < MAXM; ++m) c += (valid(m) && hi[m] == th && lo[m] >= cand) ? 1 : 0;
+      if (__reduce_add_sync(0xffffffffu, c) >= need) tl = cand;
+    }
+    int c_gt2 = 0;
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) c_gt2 += (valid(m) && hi[m] == th && lo[m] > tl) ? 1 : 0;
+    need2 = need - __reduce_add_sync(0xffffffffu, c_gt2);
+  }
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  int taken = 0, base = 0;
+#pragma unroll
+  for (int m = 0; m < MAXM; ++m) {
+    const bool v = valid(m);
+    bool sel = v && (hi[m] > th || (hi[m] == th && lo[m] > tl));
+    const bool tie = v && hi[m] == th && lo[m] == tl;
+    const uint32_t tb = __ballot_sync(0xffffffffu, tie);
+    sel = sel || (tie && taken + __popc(tb & lt_mask) < need2);
+    taken += __popc(tb);
+    const uint32_t word = __ballot_sync(0xffffffffu, sel);
+    if (sel) {
+      const int p = base + __popc(word & lt_mask);
+      const int j = lane + 32 * m;
+      if (mask_idx) mask_idx[(long long)row * k + p] = j;
+      if (mask64) mask64[(long long)row * k + p] = j;
+    }
+    base += __popc(word);
+    if (lane == 0 && member_bits && m < W) member_bits[(long long)row * W + m] = word;
+  }
+  if (member_bits)
+    for (int m = MAXM + lane; m < W; m += 32) member_bits[(long long)row * W + m] = 0u;
 }
 
 // ----------------------------------------------------------------------------

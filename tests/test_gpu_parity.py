@@ -77,7 +77,7 @@ def _topk(scores, k, method):
     return out.cpu().numpy()
 
 
-@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("method", [0, 1, 2])
 def test_topk_known_answers(method):
     # argmax / top-2 / ties to the lowest index (test_coarse.py:71-84)
     assert _topk([0.1, 0.9, 0.3], 1, method).tolist() == [[1]]
