@@ -60,7 +60,7 @@ struct AttnParams {
 };
 
 constexpr int kThreads = 384;
-constexpr int kKvStages = 4;
+constexpr int kKvStages = 5;  // K/V ring slots (D=128: 64 KB Q + 5 x 32 KB = 224 KB)
 constexpr int kSoftmaxRegs = 208;
 constexpr int kOtherRegs = 88;
 // setmaxnreg moves registers inside the CTA's pool only: the two softmax
@@ -104,8 +104,12 @@ __device__ __forceinline__ int num_kv_tiles(const AttnParams& p, int bh, int ite
   return (p.t_new + 1) >> 1;
 }
 
+// K/V tile i of the stream that Q tile `s` consumes. DENSE/EXACT: one stream
+// shared by both Q tiles (K_new blocks 2i, 2i+1). TAYLOR: each Q tile (pair of
+// flat query blocks) has its own exact-union stream, padded to a common
+// length with empty tiles, followed by the shared centroid tiles.
 template <int MODE>
-__device__ __forceinline__ TileInfo kv_tile(const AttnParams& p, int bh, int item, int i) {
+__device__ __forceinline__ TileInfo kv_tile(const AttnParams& p, int bh, int item, int i, int s) {
   TileInfo t;
   t.centroid = 0;
   t.cidx = 0;
@@ -121,7 +125,7 @@ __device__ __forceinline__ TileInfo kv_tile(const AttnParams& p, int bh, int ite
       t.valid0 = t.valid1 = 64;
       return t;
     }
-    const int4 e = p.tiles[((long long)bh * p.n_items + item) * p.max_tiles + i];
+    const int4 e = p.tiles[(((long long)bh * p.n_items + item) * 2 + s) * p.max_tiles + i];
     kn0 = e.x;
     kn1 = e.y;
     t.bits0 = e.z;
@@ -133,11 +137,11 @@ __device__ __forceinline__ TileInfo kv_tile(const AttnParams& p, int bh, int ite
   int u0 = kn0, u1 = kn1;
   if (MODE != MODE_DENSE) {
     const int* tab = p.kv_blk + (long long)bh * p.t_new;
-    u0 = tab[kn0];
+    u0 = kn0 >= 0 ? tab[kn0] : 0;  // empty padding tile: load block 0, fully masked
     u1 = kn1 >= 0 ? tab[kn1] : -1;
   }
   t.tok0 = blk_tok0(p, u0);
-  t.valid0 = blk_valid(p, u0);
+  t.valid0 = kn0 >= 0 ? blk_valid(p, u0) : 0;
   if (u1 >= 0) {
     t.tok1 = blk_tok0(p, u1);
     t.valid1 = blk_valid(p, u1);
@@ -147,6 +151,38 @@ __device__ __forceinline__ TileInfo kv_tile(const AttnParams& p, int bh, int ite
     t.bits1 = 0;
   }
   return t;
+}
+
+// Ring entry e in consumption order -> (tile, stage, is_v).
+// Shared stream: K_0 | V_0 K_1 | V_1 K_2 | ... | V_{n-1}.
+// Per-stage (TAYLOR): K0_0 K1_0 | V0_0 K0_1 V1_0 K1_1 | ... | V0_{n-1} V1_{n-1}.
+struct Entry {
+  int tile, stage, is_v;
+};
+template <int MODE>
+__device__ __forceinline__ Entry ring_entry(int e, int n) {
+  Entry r;
+  if (MODE == MODE_TAYLOR) {
+    if (e < 2) {
+      r.tile = 0; r.stage = e; r.is_v = 0;
+    } else if (e >= 4 * n - 2) {
+      r.tile = n - 1; r.stage = e - (4 * n - 2); r.is_v = 1;
+    } else {
+      const int q = e - 2, step = q / 4 + 1, w = q % 4;
+      r.stage = w >> 1;
+      r.is_v = (w & 1) == 0;
+      r.tile = r.is_v ? step - 1 : step;
+    }
+  } else {
+    r.stage = 0;
+    if (e == 0) {
+      r.tile = 0; r.is_v = 0;
+    } else {
+      r.is_v = (e & 1);
+      r.tile = r.is_v ? (e - 1) / 2 : e / 2;
+    }
+  }
+  return r;
 }
 
 template <int MODE>
@@ -234,35 +270,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      for (int i = 0; i < n_kv; ++i) {
-        const TileInfo t = kv_tile<MODE>(p, bh, item, i);
-        for (int kv = 0; kv < 2; ++kv) {
-          const int c = 2 * i + kv;
-          const int slot = c % kKvStages;
-          const int use = c / kKvStages;
-          if (use > 0) mbar_wait(&kv_empty[slot], (use - 1) & 1);
-          __syncwarp();
-          if (leader) {
-            mbar_arrive_expect_tx(&kv_full[slot], L::kTileBytes);
-            uint8_t* dst = sKV + slot * L::kTileBytes;
-            const CUtensorMap* tm;
-            int c2, c3;
-            if (t.centroid) {
-              tm = kv == 0 ? &tm_kc : &tm_vc;
-              c2 = bh;
-              c3 = 0;
-            } else {
-              tm = kv == 0 ? &tm_k : &tm_v;
-              c2 = hh;
-              c3 = bb;
-            }
-            for (int half = 0; half < 2; ++half) {
-              const int tok = half ? t.tok1 : t.tok0;
-              for (int pl = 0; pl < L::kPlanes; ++pl)
-                tma_load_4d(dst + pl * 16384 + half * 8192, tm, &kv_full[slot], pl * 64, tok, c2, c3, pol_kv);
-            }
-            progress(0, c + 1);
+      const int n_entries = (MODE == MODE_TAYLOR ? 4 : 2) * n_kv;
+      for (int c = 0; c < n_entries; ++c) {
+        const Entry en = ring_entry<MODE>(c, n_kv);
+        const TileInfo t = kv_tile<MODE>(p, bh, item, en.tile, en.stage);
+        const int slot = c % kKvStages;
+        const int use = c / kKvStages;
+        if (use > 0) mbar_wait(&kv_empty[slot], (use - 1) & 1);
+        __syncwarp();
+        if (leader) {
+          mbar_arrive_expect_tx(&kv_full[slot], L::kTileBytes);
+          uint8_t* dst = sKV + slot * L::kTileBytes;
+          const CUtensorMap* tm;
+          int c2, c3;
+          if (t.centroid) {
+            tm = en.is_v ? &tm_vc : &tm_kc;
+            c2 = bh;
+            c3 = 0;
+          } else {
+            tm = en.is_v ? &tm_v : &tm_k;
+            c2 = hh;
+            c3 = bb;
           }
+          for (int half = 0; half < 2; ++half) {
+            const int tok = half ? t.tok1 : t.tok0;
+            for (int pl = 0; pl < L::kPlanes; ++pl)
+              tma_load_4d(dst + pl * 16384 + half * 8192, tm, &kv_full[slot], pl * 64, tok, c2, c3, pol_kv);
+          }
+          progress(0, c + 1);
         }
       }
     } else if (warp == 8) {
@@ -301,45 +336,83 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (leader) mma_commit(bar);
         __syncwarp();
       };
+      auto wait_entry = [&](int e) { mbar_wait(&kv_full[e % kKvStages], (e / kKvStages) & 1); };
+      auto release = [&](int e) { commit(&kv_empty[e % kKvStages]); };
       mbar_wait(&q_full[0], 0);
       mbar_wait(&q_full[1], 0);
-      mbar_wait(&kv_full[0], 0);
-      __syncwarp();
-      tc_fence_after();
-      issue_qk(0, 0);
-      commit(&s_full[0]);
-      issue_qk(1, 0);
-      commit(&s_full[1]);
-      commit(&kv_empty[0]);
-      for (int i = 1; i < n_kv; ++i) {
-        const int cv = 2 * i - 1, ck = 2 * i;
-        const int sv = cv % kKvStages, sk = ck % kKvStages;
-        mbar_wait(&kv_full[sv], (cv / kKvStages) & 1);
-        mbar_wait(&kv_full[sk], (ck / kKvStages) & 1);
-        if (leader) progress(1, 1000 * i + 1);
+      if (MODE == MODE_TAYLOR) {
         for (int s = 0; s < 2; ++s) {
-          mbar_wait(&p_full[s], (i - 1) & 1);
+          wait_entry(s);
           __syncwarp();
           tc_fence_after();
-          issue_pv(s, sv, i > 1);
-          issue_qk(s, sk);
+          issue_qk(s, s % kKvStages);
           commit(&s_full[s]);
+          release(s);
         }
-        commit(&kv_empty[sv]);
-        commit(&kv_empty[sk]);
-      }
-      {
-        const int cv = 2 * n_kv - 1;
-        const int sv = cv % kKvStages;
-        mbar_wait(&kv_full[sv], (cv / kKvStages) & 1);
+        for (int i = 1; i < n_kv; ++i) {
+          const int base = 2 + 4 * (i - 1);
+          for (int s = 0; s < 2; ++s) {
+            const int ev = base + 2 * s, ek = ev + 1;
+            mbar_wait(&p_full[s], (i - 1) & 1);
+            wait_entry(ev);
+            __syncwarp();
+            tc_fence_after();
+            issue_pv(s, ev % kKvStages, i > 1);
+            release(ev);
+            wait_entry(ek);
+            __syncwarp();
+            tc_fence_after();
+            issue_qk(s, ek % kKvStages);
+            commit(&s_full[s]);
+            release(ek);
+          }
+          if (leader) progress(1, 1000 * i + 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+          const int ev = 4 * n_kv - 2 + s;
+          mbar_wait(&p_full[s], (n_kv - 1) & 1);
+          wait_entry(ev);
+          __syncwarp();
+          tc_fence_after();
+          issue_pv(s, ev % kKvStages, n_kv > 1);
+          commit(&o_full[s]);
+          release(ev);
+        }
+      } else {
+        wait_entry(0);
+        __syncwarp();
+        tc_fence_after();
+        issue_qk(0, 0);
+        commit(&s_full[0]);
+        issue_qk(1, 0);
+        commit(&s_full[1]);
+        release(0);
+        for (int i = 1; i < n_kv; ++i) {
+          const int ev = 2 * i - 1, ek = 2 * i;
+          wait_entry(ev);
+          wait_entry(ek);
+          if (leader) progress(1, 1000 * i + 1);
+          for (int s = 0; s < 2; ++s) {
+            mbar_wait(&p_full[s], (i - 1) & 1);
+            __syncwarp();
+            tc_fence_after();
+            issue_pv(s, ev % kKvStages, i > 1);
+            issue_qk(s, ek % kKvStages);
+            commit(&s_full[s]);
+          }
+          release(ev);
+          release(ek);
+        }
+        const int ev = 2 * n_kv - 1;
+        wait_entry(ev);
         for (int s = 0; s < 2; ++s) {
           mbar_wait(&p_full[s], (n_kv - 1) & 1);
           __syncwarp();
           tc_fence_after();
-          issue_pv(s, sv, n_kv > 1);
+          issue_pv(s, ev % kKvStages, n_kv > 1);
           commit(&o_full[s]);
         }
-        commit(&kv_empty[sv]);
+        release(ev);
       }
     }
     __syncwarp();
@@ -373,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     for (int i = 0; i < n_kv; ++i) {
-      const TileInfo t = kv_tile<MODE>(p, bh, item, i);
+      const TileInfo t = kv_tile<MODE>(p, bh, item, i, s);
       mbar_wait(&s_full[s], i & 1);
       __syncwarp();  // reconverge before .sync.aligned tcgen05 ops
       tc_fence_after();

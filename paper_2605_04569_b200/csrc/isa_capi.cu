@@ -134,7 +134,7 @@ int derive(const IsaShape* sh, const IsaKnobs* kn, Dims* d) {
   d->W = d->tn_pad / 32;
   d->items_s = (d->n_sharp + 3) / 4;
   d->items_f = (d->n_flat + 3) / 4;
-  int u = 4 * d->k < d->t_new ? 4 * d->k : d->t_new;
+  int u = 2 * d->k < d->t_new ? 2 * d->k : d->t_new;  // union of a pair of exact lists
   d->max_tiles = (u + 1) / 2;
   if (d->max_tiles < 1) d->max_tiles = 1;
   d->scale = kn->scale;
@@ -192,7 +192,7 @@ Workspace carve(const Dims& d, int dtype, uint8_t* base) {
   w.kc_bf = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.tn_pad * d.D));
   w.vc_bf = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.tn_pad * d.D));
   w.ctx_short = reinterpret_cast<int*>(take(4ull * BH));
-  w.tiles = reinterpret_cast<int4*>(take(16ull * BH * d.items_f * d.max_tiles));
+  w.tiles = reinterpret_cast<int4*>(take(16ull * BH * d.items_f * 2 * d.max_tiles));
   w.n_tiles = reinterpret_cast<int*>(take(4ull * BH * d.items_f));
   w.bytes = off;
   return w;
@@ -449,7 +449,7 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
       ISA_CUDA(cudaMemcpyAsync(ro->mask, pinned->mask, 8ull * BH * d.n_flat * d.k, cudaMemcpyDeviceToDevice, st));
   }
   if (d.n_flat) {
-    isa::taylor_plan_kernel<<<dim3(d.items_f, d.BH), 32, 0, st>>>(w.bits, d.n_flat, d.W, d.items_f, d.max_tiles,
+    isa::taylor_plan_kernel<<<dim3(d.items_f, d.BH), 64, 0, st>>>(w.bits, d.n_flat, d.W, d.items_f, d.max_tiles,
                                                                    w.tiles, w.n_tiles);
     ISA_LAUNCHED("taylor_plan_kernel");
   }

@@ -582,34 +582,35 @@ __global__ void centroid_kernel(const float* __restrict__ kc, const float* __res
 }
 
 // ----------------------------------------------------------------------------
-// Taylor work plan: for each CTA item (4 flat query blocks) merge the 4 exact
-// lists (bitmask OR) into an ascending union stream paired into 128-key tiles;
-// each half carries a 4-bit visibility mask (which of the 4 query blocks has
-// that K_new block on its exact list). One warp per item.
+// Taylor work plan. A CTA item holds 4 flat query blocks: Q tile s (stage)
+// = blocks (4*item + 2s, 4*item + 2s + 1). For each stage, merge the two
+// exact lists (bitmask OR) into an ascending union stream paired into
+// 128-key tiles; each half carries the visibility bits of the CTA's query
+// blocks (bit qb = 2s + row-half). The shorter stream is padded with empty
+// tiles (kn = -1) so both stages share one step count. grid (n_items, BH),
+// block 64 (one warp per stage).
 // ----------------------------------------------------------------------------
-__global__ void taylor_plan_kernel(const uint32_t* __restrict__ member_bits, int n_flat, int W, int n_items,
-                                   int max_tiles, int4* __restrict__ tiles, int* __restrict__ n_tiles) {
-  const int item = blockIdx.x, bh = blockIdx.y, lane = threadIdx.x;
-  const uint32_t* mb[4];
-  int nq = 0;
-  for (int q = 0; q < 4; ++q) {
-    const int f = item * 4 + q;
-    mb[q] = f < n_flat ? member_bits + ((long long)bh * n_flat + f) * W : nullptr;
-    nq += f < n_flat;
+__global__ void __launch_bounds__(64) taylor_plan_kernel(const uint32_t* __restrict__ member_bits, int n_flat,
+                                                         int W, int n_items, int max_tiles, int4* __restrict__ tiles,
+                                                         int* __restrict__ n_tiles) {
+  __shared__ int counts[2];
+  const int item = blockIdx.x, bh = blockIdx.y;
+  const int s = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t* mb[2];
+  for (int h = 0; h < 2; ++h) {
+    const int f = item * 4 + 2 * s + h;
+    mb[h] = f < n_flat ? member_bits + ((long long)bh * n_flat + f) * W : nullptr;
   }
-  int4* out = tiles + ((long long)bh * n_items + item) * max_tiles;
+  int4* out = tiles + (((long long)bh * n_items + item) * 2 + s) * max_tiles;
   int base = 0;
   for (int w0 = 0; w0 < W; w0 += 32) {
     const int w = w0 + lane;
-    uint32_t wq[4] = {0u, 0u, 0u, 0u};
-    uint32_t uni = 0u;
+    uint32_t wq[2] = {0u, 0u};
     if (w < W) {
-      for (int q = 0; q < 4; ++q)
-        if (mb[q]) {
-          wq[q] = mb[q][w];
-          uni |= wq[q];
-        }
+      for (int h = 0; h < 2; ++h)
+        if (mb[h]) wq[h] = mb[h][w];
     }
+    const uint32_t uni = wq[0] | wq[1];
     const int cnt = __popc(uni);
     int incl = cnt;
 #pragma unroll
@@ -623,8 +624,7 @@ __global__ void taylor_plan_kernel(const uint32_t* __restrict__ member_bits, int
       const int bpos = __ffs(wb) - 1;
       wb &= wb - 1;
       const int j = w * 32 + bpos;
-      int vis = 0;
-      for (int q = 0; q < 4; ++q) vis |= ((wq[q] >> bpos) & 1u) << q;
+      const int vis = (int)(((wq[0] >> bpos) & 1u) | (((wq[1] >> bpos) & 1u) << 1)) << (2 * s);
       int* e = reinterpret_cast<int*>(out + (p >> 1));
       if (p & 1) {
         e[1] = j;
@@ -637,16 +637,18 @@ __global__ void taylor_plan_kernel(const uint32_t* __restrict__ member_bits, int
     }
     base += __shfl_sync(0xffffffffu, incl, 31);
   }
-  __syncwarp();
-  if (lane == 0) {
-    n_tiles[bh * n_items + item] = (base + 1) >> 1;
-    if (base & 1) {  // odd union: the last tile's second half is absent (fully masked)
-      int* e = reinterpret_cast<int*>(out + (base >> 1));
-      e[1] = -1;
-      e[3] = 0;
-    }
+  if (lane == 0) counts[s] = base;
+  __syncthreads();
+  const int nt = max((counts[0] + 1) >> 1, (counts[1] + 1) >> 1);
+  // close this stage's stream: odd tail half, then empty padding tiles
+  const int mine = counts[s];
+  if (lane == 0 && (mine & 1)) {
+    int* e = reinterpret_cast<int*>(out + (mine >> 1));
+    e[1] = -1;
+    e[3] = 0;
   }
-  (void)nq;
+  for (int t = ((mine + 1) >> 1) + lane; t < nt; t += 32) out[t] = make_int4(-1, -1, 0, 0);
+  if (threadIdx.x == 0) n_tiles[bh * n_items + item] = nt;
 }
 
 // int32 -> int64 export of routing lists (caller-facing int64 API, pipeline types).
