@@ -35,19 +35,26 @@ def gather_heads(out_local: torch.Tensor, out_full: torch.Tensor, world: int, gr
                  chunks: Optional[List[int]] = None) -> None:
     """All-gather head shards into out_full (B, H, S, D) (round-robin layout).
 
-    B == 1 on CUDA: one all_gather_into_tensor per local head chunk c straight
-    into the contiguous slab out_full[0, c*P:(c+1)*P]. Otherwise a generic
-    all_gather + strided scatter (used by the CPU/gloo tests)."""
+    B == 1 on CUDA with H % P == 0: one all_gather_into_tensor per local head
+    chunk c straight into the contiguous slab out_full[0, c*P:(c+1)*P].
+    Otherwise a generic all_gather of shards padded to ceil(H/P) heads and a
+    strided scatter (uneven head counts; the CPU/gloo tests)."""
     B, Hl, S, D = out_local.shape
-    if B == 1 and out_full.is_cuda and out_full.is_contiguous():
+    H = out_full.shape[1]
+    if B == 1 and out_full.is_cuda and out_full.is_contiguous() and H % world == 0:
         for c in (chunks if chunks is not None else range(Hl)):
             dist.all_gather_into_tensor(out_full[0, c * world:(c + 1) * world], out_local[0, c].contiguous(),
                                         group=group)
         return
-    parts = [torch.empty_like(out_local) for _ in range(world)]
-    dist.all_gather(parts, out_local.contiguous(), group=group)
+    h_max = -(-H // world)
+    send = out_local
+    if Hl < h_max:
+        send = torch.cat([out_local, out_local.new_zeros(B, h_max - Hl, S, D)], dim=1)
+    parts = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send.contiguous(), group=group)
     for r in range(world):
-        out_full[:, r::world] = parts[r]
+        n_r = len(range(r, H, world))
+        out_full[:, r::world] = parts[r][:, :n_r]
 
 
 def isa_forward_sharded(prepared, out_full: torch.Tensor, my_heads: List[int], world: int, group=None,
