@@ -69,7 +69,8 @@ constexpr int kOtherRegs = 88;
 // a softmax warp in USETMAXREG.TRY_ALLOC forever (observed on B200).
 constexpr int kLaunchRegs = 168;
 static_assert(2 * (kSoftmaxRegs - kLaunchRegs) <= (kLaunchRegs - kOtherRegs), "register pool overcommitted");
-constexpr int kLdCols = 16;  // tcgen05.ld width (columns) for the S row
+constexpr int kLdCols = 16;   // tcgen05.ld width (columns) for the S row
+constexpr int kEmuEvery = 4;  // 1 in 4 exp2 pairs of the plain softmax path on the FMA pipe
 
 template <int D>
 struct AttnSmem {
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
       if (plain) {  // raw scores; scaled inside the exp2 FMA below
 #pragma unroll
-        for (int c = 0; c < 128; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
+        for (int c = 0; c < 128; c += 2) mx[(c >> 1) & 7] = fmax3(mx[(c >> 1) & 7], x[c], x[c + 1]);
       } else if (!t.centroid) {
         const int v0 = ((t.bits0 >> qb) & 1) ? t.valid0 : 0;
         const int v1 = ((t.bits1 >> qb) & 1) ? t.valid1 : 0;
@@ -522,19 +523,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float mu = (m == -INFINITY) ? 0.f : m;
       float sm[4] = {0.f, 0.f, 0.f, 0.f};
+      float2 sm2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       // P in 4 chunks of 32 columns, each stored to TMEM right away so the
       // live register set stays ~ S row + 16 packed words.
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t pk[16];
         if (plain) {
-          const float nmu = -mu;
+          // FFMA2 scale-subtract; 1 in kEmuEvery pairs takes the FMA-pipe
+          // polynomial exp2, the rest the MUFU (the SFU is the softmax's
+          // binding unit: 16 exp/clk/SM vs 1024 MMA-clk per 128x128 tile).
+          const float2 sl2x2 = make_float2(sl2, sl2), nmu2 = make_float2(-mu, -mu);
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
-            const float p0 = ex2_approx(fmaf(x[32 * ch + 2 * c], sl2, nmu));
-            const float p1 = ex2_approx(fmaf(x[32 * ch + 2 * c + 1], sl2, nmu));
-            sm[c & 3] += p0 + p1;
-            pk[c] = pack_bf16x2(p0, p1);
+            const float2 t = ffma2(make_float2(x[32 * ch + 2 * c], x[32 * ch + 2 * c + 1]), sl2x2, nmu2);
+            float2 pp;
+            if (kEmuEvery > 0 && (c % kEmuEvery) == kEmuEvery - 1) {
+              pp = ex2_emu2(t);
+            } else {
+              pp.x = ex2_approx(t.x);
+              pp.y = ex2_approx(t.y);
+            }
+            sm2[c & 3] = fadd2(sm2[c & 3], pp);
+            pk[c] = pack_bf16x2(pp.x, pp.y);
           }
         } else {
 #pragma unroll
@@ -547,7 +558,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_st16(t_p + 16 * ch, pk);
       }
-      const float sum = (sm[0] + sm[1]) + (sm[2] + sm[3]);
+      const float2 s2 = fadd2(fadd2(sm2[0], sm2[1]), fadd2(sm2[2], sm2[3]));
+      const float sum = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + (s2.x + s2.y);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();

@@ -257,6 +257,68 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two lanes of work per instruction).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2_rm(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rm.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// 2^x for two lanes on the FMA/ALU pipes instead of the MUFU (SFU) unit:
+// floor via the 1.5*2^23 round-down trick, 2^frac by a degree-3 polynomial
+// (least-squares fit with p(0) = 1, max relative error 8.6e-5 on [0,1)),
+// then the integer exponent is added into the IEEE exponent field. Inputs are
+// clamped at -127 (2^-127 ~ 6e-39 stands in for exp2(-inf) = 0).
+__device__ __forceinline__ float2 ex2_emu2(float2 x) {
+  const float kRound = 12582912.0f;  // 1.5 * 2^23
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 r = fadd2_rm(x, make_float2(kRound, kRound));
+  const float2 f = fsub2(x, fsub2(r, make_float2(kRound, kRound)));
+  float2 p = ffma2(make_float2(0.0770670473575592f, 0.0770670473575592f), f,
+                   make_float2(0.22764497995376587f, 0.22764497995376587f));
+  p = ffma2(p, f, make_float2(0.6951168179512024f, 0.6951168179512024f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  float2 o;
+  o.x = __int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23));
+  o.y = __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23));
+  return o;
+}
+
 template <uint32_t kRegs>
 __device__ __forceinline__ void setmaxnreg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
