@@ -446,8 +446,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         lwctx = log2f(static_cast<float>(p.l_ctx & 63));
       }
     }
+    // Column validity of the current K/V tile, computed without the block
+    // table: only K_new block t_src-1 and the selected short context block can
+    // hold fewer than 64 rows. TAYLOR tile descriptors are prefetched one
+    // tile ahead so their load latency hides behind the current tile.
+    const int jshort = (MODE != MODE_DENSE && (p.l_ctx & 63)) ? p.ctx_short_j[bh] : -1;
+    auto kn_valid = [&](int kn) -> int {
+      if (kn < 0 || kn >= p.t_new) return 0;
+      if (MODE == MODE_DENSE) return blk_valid(p, kn);
+      if ((p.l_src & 63) && kn == p.t_src - 1) return p.l_src & 63;
+      if (kn == jshort) return p.l_ctx & 63;
+      return 64;
+    };
+    const int n_exact = (MODE == MODE_TAYLOR) ? p.n_tiles[bh * p.n_items + item] : 0;
+    const int4* tlist = (MODE == MODE_TAYLOR)
+                            ? p.tiles + (((long long)bh * p.n_items + item) * 2 + s) * p.max_tiles
+                            : nullptr;
+    int4 e_next = (MODE == MODE_TAYLOR && n_exact > 0) ? tlist[0] : make_int4(0, 0, 0, 0);
     for (int i = 0; i < n_kv; ++i) {
-      const TileInfo t = kv_tile<MODE>(p, bh, item, i, s);
+      TileInfo t;
+      t.centroid = 0;
+      t.cidx = 0;
+      if (MODE == MODE_TAYLOR) {
+        if (i < n_exact) {
+          const int4 e = e_next;
+          if (i + 1 < n_exact) e_next = tlist[i + 1];
+          t.valid0 = kn_valid(e.x);
+          t.valid1 = kn_valid(e.y);
+          t.bits0 = e.z;
+          t.bits1 = e.w;
+        } else {
+          t.centroid = 1;
+          t.cidx = i - n_exact;
+          t.valid0 = t.valid1 = 64;
+          t.bits0 = t.bits1 = 0xF;
+        }
+      } else {
+        t.valid0 = kn_valid(2 * i);
+        t.valid1 = kn_valid(2 * i + 1);
+        t.bits0 = t.bits1 = 0xF;
+      }
       mbar_wait(&s_full[s], i & 1);
       __syncwarp();  // reconverge before .sync.aligned tcgen05 ops
       tc_fence_after();

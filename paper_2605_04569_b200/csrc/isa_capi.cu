@@ -391,7 +391,8 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
                           nullptr, st)))
       return rc;
   }
-  isa::kvblk_from_sel_kernel<<<d.BH, 256, 0, st>>>(w.sel, d.t_src, d.k_ctx, w.kv_blk, w.ctx_short);
+  isa::kvblk_from_sel_kernel<<<d.BH, 256, 0, st>>>(w.sel, d.t_src, d.k_ctx, d.t_ctx, d.l_ctx, w.kv_blk,
+                                                   w.ctx_short);
   ISA_LAUNCHED("kvblk_from_sel_kernel");
   if (need_scores) {
     dim3 g((d.t_new + 127) / 128, (d.T + 127) / 128, d.BH);
@@ -527,6 +528,7 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
     isa::AttnParams ps = p;
     ps.n_qblk = d.n_sharp;
     ps.qlist = w.sharp;
+    ps.ctx_short_j = w.ctx_short;
     if ((rc = launch_attention_d<isa::MODE_EXACT>(d.D, tq, tk, tv, tq, tq, ps, d.items_s, d.BH, st))) return rc;
   }
   record(events, 4, st);

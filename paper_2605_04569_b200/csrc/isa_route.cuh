@@ -572,7 +572,6 @@ __global__ void centroid_kernel(const float* __restrict__ kc, const float* __res
       kc_bf[o + d] = __float2bfloat16_rn(kc[src + d]);
       vc_bf[o + d] = __float2bfloat16_rn(vc[src + d]);
     }
-    if (threadIdx.x == 0 && j >= seg.t_src && u == seg.t_src + seg.t_ctx - 1) ctx_short_j[bh] = j;
   } else {
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
       kc_bf[o + d] = __float2bfloat16_rn(0.f);
@@ -663,10 +662,19 @@ __global__ void narrow_kernel(const int64_t* __restrict__ src, int* __restrict__
 }
 
 // Pinned selection -> K_new block table.
-__global__ void kvblk_from_sel_kernel(const int* __restrict__ sel, int t_src, int k_ctx, int* __restrict__ kv_blk,
-                                      int* __restrict__ ctx_short_j) {
+// Also records the K_new index of the short last context block when it was
+// selected (-1 otherwise): the only K_new block besides t_src-1 whose valid
+// row count can be < 64 (ragged segments, pipeline.py:199-209).
+__global__ void kvblk_from_sel_kernel(const int* __restrict__ sel, int t_src, int k_ctx, int t_ctx, int l_ctx,
+                                      int* __restrict__ kv_blk, int* __restrict__ ctx_short_j) {
   const int bh = blockIdx.x;
-  if (threadIdx.x == 0) ctx_short_j[bh] = -1;
+  if (threadIdx.x == 0) {
+    int js = -1;
+    if (l_ctx & 63)
+      for (int c = 0; c < k_ctx; ++c)
+        if (sel[(long long)bh * k_ctx + c] == t_ctx - 1) js = t_src + c;
+    ctx_short_j[bh] = js;
+  }
   const int t_new = t_src + k_ctx;
   for (int j = threadIdx.x; j < t_new; j += blockDim.x)
     kv_blk[(long long)bh * t_new + j] = j < t_src ? j : t_src + sel[(long long)bh * k_ctx + j - t_src];
