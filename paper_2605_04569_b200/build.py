@@ -39,6 +39,7 @@ def nvcc_command(out: str = LIB) -> list[str]:
         "-Xptxas", "-v",
         "-I", os.path.join(ROOT, "include"),
         *(["-DISA_DEBUG_WAIT"] if os.environ.get("ISA_DEBUG_WAIT") else []),
+        *([f"-D{f}" for f in os.environ.get("ISA_EXTRA_DEFINES", "").split(",") if f]),
         "-o", out,
         *[os.path.join(CSRC, s) for s in SOURCES],
     ]

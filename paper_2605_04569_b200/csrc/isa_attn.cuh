@@ -70,7 +70,10 @@ constexpr int kOtherRegs = 88;
 constexpr int kLaunchRegs = 168;
 static_assert(2 * (kSoftmaxRegs - kLaunchRegs) <= (kLaunchRegs - kOtherRegs), "register pool overcommitted");
 constexpr int kLdCols = 16;   // tcgen05.ld width (columns) for the S row
-constexpr int kEmuEvery = 4;  // 1 in 4 exp2 pairs of the plain softmax path on the FMA pipe
+#ifndef ISA_EMU_EVERY
+#define ISA_EMU_EVERY 4
+#endif
+constexpr int kEmuEvery = ISA_EMU_EVERY;  // 1 in kEmuEvery exp2 pairs of the plain softmax path on the FMA pipe
 
 template <int D>
 struct AttnSmem {
@@ -489,53 +492,115 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&s_full[s], i & 1);
       __syncwarp();  // reconverge before .sync.aligned tcgen05 ops
       tc_fence_after();
+#ifdef ISA_EXP_NOSOFTMAX
+      // Experiment: MMA/TMA ceiling with the softmax reduced to a P store.
+      {
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) pk[c] = 0x3c003c00u;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) tmem_st16(t_p + 16 * ch, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[s]);
+        l += 1.f;
+        continue;
+      }
+#endif
       uint32_t sr[128];
+#ifdef ISA_EXP_NOLOAD
+      // Experiment: skip the TMEM read of S (synthetic scores).
+#pragma unroll
+      for (int c = 0; c < 128; ++c) sr[c] = __float_as_uint(0.001f * (float)((c * 7 + lane + i) & 63));
+#else
 #pragma unroll
       for (int c = 0; c < 128 / kLdCols; ++c) {
         if (kLdCols == 16) tmem_ld16(t_s + c * 16, sr + c * 16);
         else tmem_ld8(t_s + c * 8, sr + c * 8);
       }
       tmem_ld_wait();
+#endif
+#ifdef ISA_EXP_LOADONLY
+      {
+        float mm = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 128; c += 2) mm = fmax3(mm, __uint_as_float(sr[c]), __uint_as_float(sr[c + 1]));
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) pk[c] = __float_as_uint(mm) & 0x3c003c00u;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) tmem_st16(t_p + 16 * ch, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[s]);
+        l += 1.f;
+        continue;
+      }
+#endif
       float* x = reinterpret_cast<float*>(sr);
-      const bool plain = !t.centroid && t.valid0 == 64 && t.valid1 == 64 &&
-                         (MODE != MODE_TAYLOR || (((t.bits0 & t.bits1) >> qb) & 1));
-      float mx[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
-      if (plain) {  // raw scores; scaled inside the exp2 FMA below
-#pragma unroll
-        for (int c = 0; c < 128; c += 2) mx[(c >> 1) & 7] = fmax3(mx[(c >> 1) & 7], x[c], x[c + 1]);
-      } else if (!t.centroid) {
+      // Column masks of this tile for this row's query block, one word per 32
+      // columns (1 = excluded), plus an additive log2 weight: 0 for key
+      // blocks, log2(64) for centroid columns (taylor.py:156). Masks are
+      // warp-uniform (a warp's 32 rows belong to one query block), so wholly
+      // masked halves skip their exponentials.
+      uint32_t mw[4];
+      float bias = 0.f;
+      bool special = false;  // centroid tile holding a short block's centroid (per-column weight)
+      if (!t.centroid) {
         const int v0 = ((t.bits0 >> qb) & 1) ? t.valid0 : 0;
         const int v1 = ((t.bits1 >> qb) & 1) ? t.valid1 : 0;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          const int lim = c < 64 ? v0 : v1;
-          x[c] = ((c & 63) < lim) ? x[c] * sl2 : -INFINITY;
-          mx[c & 7] = fmaxf(mx[c & 7], x[c]);
+        for (int w = 0; w < 4; ++w) {
+          const int lim = (w < 2 ? v0 : v1) - 32 * (w & 1);
+          mw[w] = lim >= 32 ? 0u : (lim <= 0 ? 0xffffffffu : ~((1u << lim) - 1u));
         }
       } else {
-        // centroid column j: log2(valid rows of K_new block j) (64 except the
-        // short last block of either segment), -inf past t_new or when j is on
-        // this row block's exact list (taylor.py:153-157).
         const uint32_t* wb = mbits + t.cidx * 4;
         const int j0 = t.cidx * 128;
 #pragma unroll
-        for (int w4 = 0; w4 < 4; ++w4) {
-          const uint32_t bits = __ldg(wb + w4);
+        for (int w = 0; w < 4; ++w) {
+          const int live = p.t_new - (j0 + 32 * w);  // columns < t_new in this word
+          const uint32_t oob = live >= 32 ? 0u : (live <= 0 ? 0xffffffffu : ~((1u << live) - 1u));
+          mw[w] = __ldg(wb + w) | oob;
+        }
+        bias = 6.f;
+        special = (jsrc >= j0 && jsrc < j0 + 128) || (jctx >= j0 && jctx < j0 + 128);
+      }
+      const bool skip0 = (mw[0] & mw[1]) == 0xffffffffu;
+      const bool skip1 = (mw[2] & mw[3]) == 0xffffffffu;
+      const bool dense = (mw[0] | mw[1] | mw[2] | mw[3]) == 0u;
+      float mx[8];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int cc = w4 * 32 + c;
-            const int j = j0 + cc;
-            float bias = j == jsrc ? lwsrc : (j == jctx ? lwctx : 6.f);
-            bias = j < p.t_new ? bias : -INFINITY;
-            x[cc] = ((bits >> c) & 1) ? -INFINITY : fmaf(x[cc], sl2, bias);
-            mx[cc & 7] = fmaxf(mx[cc & 7], x[cc]);
+      for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+      if (special) {  // rare: per-column weights, scaled in place
+        const int j0 = t.cidx * 128;
+#pragma unroll
+        for (int cc = 0; cc < 128; ++cc) {
+          const int j = j0 + cc;
+          const float bj = j == jsrc ? lwsrc : (j == jctx ? lwctx : 6.f);
+          x[cc] = ((mw[cc >> 5] >> (cc & 31)) & 1) ? -INFINITY : fmaf(x[cc], sl2, bj);
+          mx[cc & 7] = fmaxf(mx[cc & 7], x[cc]);
+        }
+      } else if (dense) {  // raw scores, scaled inside the exp2 FMA below
+#pragma unroll
+        for (int c = 0; c < 128; c += 2) mx[(c >> 1) & 7] = fmax3(mx[(c >> 1) & 7], x[c], x[c + 1]);
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 0 ? skip0 : skip1) continue;
+#pragma unroll
+          for (int c = 64 * h; c < 64 * h + 64; c += 2) {
+            const uint32_t w = mw[c >> 5];
+            const float a0 = ((w >> (c & 31)) & 1) ? -INFINITY : x[c];
+            const float a1 = ((w >> ((c + 1) & 31)) & 1) ? -INFINITY : x[c + 1];
+            mx[(c >> 1) & 7] = fmax3(mx[(c >> 1) & 7], a0, a1);
           }
         }
       }
       float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-      if (plain) mt *= sl2;
+      if (!special) mt = fmaf(mt, sl2, bias);  // max(x*sl2 + b) over the kept columns
       // running max with lazy rescale (threshold 8 in log2 units)
       float m_new = fmaxf(m, mt);
       float o_scale = 1.f;
@@ -567,31 +632,39 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         uint32_t pk[16];
-        if (plain) {
-          // FFMA2 scale-subtract; 1 in kEmuEvery pairs takes the FMA-pipe
-          // polynomial exp2, the rest the MUFU (the SFU is the softmax's
-          // binding unit: 16 exp/clk/SM vs 1024 MMA-clk per 128x128 tile).
-          const float2 sl2x2 = make_float2(sl2, sl2), nmu2 = make_float2(-mu, -mu);
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const float2 t = ffma2(make_float2(x[32 * ch + 2 * c], x[32 * ch + 2 * c + 1]), sl2x2, nmu2);
-            float2 pp;
-            if (kEmuEvery > 0 && (c % kEmuEvery) == kEmuEvery - 1) {
-              pp = ex2_emu2(t);
-            } else {
-              pp.x = ex2_approx(t.x);
-              pp.y = ex2_approx(t.y);
-            }
-            sm2[c & 3] = fadd2(sm2[c & 3], pp);
-            pk[c] = pack_bf16x2(pp.x, pp.y);
-          }
-        } else {
+        const uint32_t w = mw[ch];
+        if (special) {
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
             const float p0 = ex2_approx(x[32 * ch + 2 * c] - mu);
             const float p1 = ex2_approx(x[32 * ch + 2 * c + 1] - mu);
             sm[c & 3] += p0 + p1;
             pk[c] = pack_bf16x2(p0, p1);
+          }
+        } else if (ch < 2 ? skip0 : skip1) {  // wholly masked half: P = 0, no exponentials
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk[c] = 0u;
+        } else {
+          // FFMA2 scale-subtract; in fully kept words 1 in kEmuEvery pairs
+          // takes the FMA-pipe polynomial exp2, the rest the MUFU (SFU);
+          // excluded columns are zeroed after the exponential.
+          const float2 sl2x2 = make_float2(sl2, sl2), nb2 = make_float2(bias - mu, bias - mu);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const float2 tt = ffma2(make_float2(x[32 * ch + 2 * c], x[32 * ch + 2 * c + 1]), sl2x2, nb2);
+            float2 pp;
+            if (kEmuEvery > 0 && (c % kEmuEvery) == kEmuEvery - 1 && w == 0u) {
+              pp = ex2_emu2(tt);
+            } else {
+              pp.x = ex2_approx(tt.x);
+              pp.y = ex2_approx(tt.y);
+            }
+            if (w != 0u) {
+              pp.x = ((w >> (2 * c)) & 1) ? 0.f : pp.x;
+              pp.y = ((w >> (2 * c + 1)) & 1) ? 0.f : pp.y;
+            }
+            sm2[c & 3] = fadd2(sm2[c & 3], pp);
+            pk[c] = pack_bf16x2(pp.x, pp.y);
           }
         }
         tmem_st16(t_p + 16 * ch, pk);
