@@ -629,11 +629,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       float2 sm2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       // P in 4 chunks of 32 columns, each stored to TMEM right away so the
       // live register set stays ~ S row + 16 packed words.
+      const float2 sl2x2 = make_float2(sl2, sl2), nb2 = make_float2(bias - mu, bias - mu);
+      if (dense && !special) {
+        // hot path (every K6/K8 tile): FFMA2 scale-subtract; 1 in kEmuEvery
+        // pairs takes the FMA-pipe polynomial exp2, the rest the MUFU (SFU).
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        uint32_t pk[16];
-        const uint32_t w = mw[ch];
-        if (special) {
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const float2 tt = ffma2(make_float2(x[32 * ch + 2 * c], x[32 * ch + 2 * c + 1]), sl2x2, nb2);
+            float2 pp;
+            if (kEmuEvery > 0 && (c % kEmuEvery) == kEmuEvery - 1) {
+              pp = ex2_emu2(tt);
+            } else {
+              pp.x = ex2_approx(tt.x);
+              pp.y = ex2_approx(tt.y);
+            }
+            sm2[c & 3] = fadd2(sm2[c & 3], pp);
+            pk[c] = pack_bf16x2(pp.x, pp.y);
+          }
+          tmem_st16(t_p + 16 * ch, pk);
+        }
+      } else if (special) {
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
             const float p0 = ex2_approx(x[32 * ch + 2 * c] - mu);
@@ -641,33 +662,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             sm[c & 3] += p0 + p1;
             pk[c] = pack_bf16x2(p0, p1);
           }
-        } else if (ch < 2 ? skip0 : skip1) {  // wholly masked half: P = 0, no exponentials
-#pragma unroll
-          for (int c = 0; c < 16; ++c) pk[c] = 0u;
-        } else {
-          // FFMA2 scale-subtract; in fully kept words 1 in kEmuEvery pairs
-          // takes the FMA-pipe polynomial exp2, the rest the MUFU (SFU);
-          // excluded columns are zeroed after the exponential.
-          const float2 sl2x2 = make_float2(sl2, sl2), nb2 = make_float2(bias - mu, bias - mu);
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const float2 tt = ffma2(make_float2(x[32 * ch + 2 * c], x[32 * ch + 2 * c + 1]), sl2x2, nb2);
-            float2 pp;
-            if (kEmuEvery > 0 && (c % kEmuEvery) == kEmuEvery - 1 && w == 0u) {
-              pp = ex2_emu2(tt);
-            } else {
-              pp.x = ex2_approx(tt.x);
-              pp.y = ex2_approx(tt.y);
-            }
-            if (w != 0u) {
-              pp.x = ((w >> (2 * c)) & 1) ? 0.f : pp.x;
-              pp.y = ((w >> (2 * c + 1)) & 1) ? 0.f : pp.y;
-            }
-            sm2[c & 3] = fadd2(sm2[c & 3], pp);
-            pk[c] = pack_bf16x2(pp.x, pp.y);
-          }
+          tmem_st16(t_p + 16 * ch, pk);
         }
-        tmem_st16(t_p + 16 * ch, pk);
+      } else {
+        // masked tiles (Taylor unions, centroids, ragged/missing halves):
+        // wholly excluded halves write P = 0 with no exponentials; partial
+        // words zero their excluded columns after the MUFU exp2.
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t pk[16];
+          const uint32_t w = mw[ch];
+          if (ch < 2 ? skip0 : skip1) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) pk[c] = 0u;
+          } else {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const float2 tt = ffma2(make_float2(x[32 * ch + 2 * c], x[32 * ch + 2 * c + 1]), sl2x2, nb2);
+              float2 pp;
+              pp.x = ((w >> (2 * c)) & 1) ? 0.f : ex2_approx(tt.x);
+              pp.y = ((w >> (2 * c + 1)) & 1) ? 0.f : ex2_approx(tt.y);
+              sm2[c & 3] = fadd2(sm2[c & 3], pp);
+              pk[c] = pack_bf16x2(pp.x, pp.y);
+            }
+          }
+          tmem_st16(t_p + 16 * ch, pk);
+        }
       }
       const float2 s2 = fadd2(fadd2(sm2[0], sm2[1]), fadd2(sm2[2], sm2[3]));
       const float sum = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + (s2.x + s2.y);
