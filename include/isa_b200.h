@@ -67,8 +67,12 @@ typedef struct IsaKnobs {
   int32_t n_flat;
   int32_t k_mask;
   int32_t softmax_first; /* coarse.py:194 */
-  int32_t flags;         /* reserved, 0 */
+  int32_t flags;         /* ISA_FLAG_* bits, 0 = defaults */
 } IsaKnobs;
+
+/* IsaKnobs.flags: launch the exact (sharp) and Taylor (flat) attention
+ * branches as two kernels instead of one fused grid (per-branch profiling). */
+#define ISA_FLAG_SEPARATE_BRANCHES 1
 
 /* Optional routing export (device pointers; any may be NULL). */
 typedef struct IsaRoutingOut {

@@ -198,10 +198,9 @@ __device__ __forceinline__ int query_block(const AttnParams& p, int bh, int item
 }
 
 template <int D, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
-    gba_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
-                         const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
+__device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensorMap& tm_k, const CUtensorMap& tm_v,
+                                         const CUtensorMap& tm_kc, const CUtensorMap& tm_vc, const AttnParams& p,
+                                         const int item, const int bh) {
   using L = AttnSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -218,8 +217,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int item = blockIdx.x;
-  const int bh = blockIdx.y;
   const int n_kv = num_kv_tiles<MODE>(p, bh, item);
 
   if (threadIdx.x == 0) {
@@ -744,6 +741,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+}
+
+// One branch per launch (K6 exact, K7 Taylor or K8 dense).
+template <int D, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    gba_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
+                         const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
+  gba_body<D, MODE>(tm_q, tm_k, tm_v, tm_kc, tm_vc, p, blockIdx.x, blockIdx.y);
+}
+
+// Both ISA branches in one launch: CTAs [0, n_exact) run the sharp items (288
+// K/V steps each at cfg3), the rest the Taylor items (~41 steps). The short
+// Taylor CTAs fill the tail wave of the long exact ones instead of a second
+// kernel ramping up after a ~60%-occupied last wave.
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    gba_isa_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
+                   const __grid_constant__ CUtensorMap tm_vc, const AttnParams pe, const AttnParams pt,
+                   const int n_exact) {
+  if ((int)blockIdx.x < n_exact)
+    gba_body<D, MODE_EXACT>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pe, blockIdx.x, blockIdx.y);
+  else
+    gba_body<D, MODE_TAYLOR>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pt, blockIdx.x - n_exact, blockIdx.y);
 }
 
 }  // namespace isa

@@ -220,6 +220,29 @@ int launch_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtenso
   return ISA_OK;
 }
 
+template <int D>
+int launch_isa_fused_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
+                       const CUtensorMap& tvc, const isa::AttnParams& pe, const isa::AttnParams& pt, int items_e,
+                       int items_t, int BH, cudaStream_t st) {
+  using L = isa::AttnSmem<D>;
+  static bool configured = false;
+  if (!configured) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::gba_isa_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
+    configured = true;
+  }
+  dim3 grid(items_e + items_t, BH);
+  isa::gba_isa_kernel<D><<<grid, isa::kThreads, L::kAlloc, st>>>(tq, tk, tv, tkc, tvc, pe, pt, items_e);
+  ISA_LAUNCHED("gba_isa_kernel");
+  return ISA_OK;
+}
+
+int launch_isa_fused(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                     const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& pe,
+                     const isa::AttnParams& pt, int items_e, int items_t, int BH, cudaStream_t st) {
+  if (D == 128) return launch_isa_fused_t<128>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
+  return launch_isa_fused_t<64>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
+}
+
 template <int MODE>
 int launch_attention_d(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& p, int items, int BH,
@@ -524,14 +547,11 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
   p.o_sb = (long long)d.H * d.S * d.D;
   p.o_ss = d.D;
   p.err_flag = err_word;
-  if (d.n_sharp) {
-    isa::AttnParams ps = p;
-    ps.n_qblk = d.n_sharp;
-    ps.qlist = w.sharp;
-    ps.ctx_short_j = w.ctx_short;
-    if ((rc = launch_attention_d<isa::MODE_EXACT>(d.D, tq, tk, tv, tq, tq, ps, d.items_s, d.BH, st))) return rc;
-  }
-  record(events, 4, st);
+  isa::AttnParams ps = p;
+  ps.n_qblk = d.n_sharp;
+  ps.qlist = w.sharp;
+  ps.ctx_short_j = w.ctx_short;
+  isa::AttnParams pf = p;
   if (d.n_flat) {
     if ((rc = make_map(&tkc, w.kc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
                        (long long)d.BH * d.tn_pad * d.D * 2)))
@@ -539,7 +559,6 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
     if ((rc = make_map(&tvc, w.vc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
                        (long long)d.BH * d.tn_pad * d.D * 2)))
       return rc;
-    isa::AttnParams pf = p;
     pf.n_qblk = d.n_flat;
     pf.qlist = w.flat;
     pf.tiles = w.tiles;
@@ -550,7 +569,19 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
     pf.W = d.W;
     pf.ctx_short_j = w.ctx_short;
     pf.tn_pad = d.tn_pad;
-    if ((rc = launch_attention_d<isa::MODE_TAYLOR>(d.D, tq, tk, tv, tkc, tvc, pf, d.items_f, d.BH, st))) return rc;
+  }
+  const bool fuse = d.n_sharp && d.n_flat && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES);
+  if (fuse) {
+    // K6 + K7 in one grid: exact items first, Taylor items fill the tail.
+    if ((rc = launch_isa_fused(d.D, tq, tk, tv, tkc, tvc, ps, pf, d.items_s, d.items_f, d.BH, st))) return rc;
+    record(events, 4, st);
+  } else {
+    if (d.n_sharp)
+      if ((rc = launch_attention_d<isa::MODE_EXACT>(d.D, tq, tk, tv, tq, tq, ps, d.items_s, d.BH, st))) return rc;
+    record(events, 4, st);
+    if (d.n_flat)
+      if ((rc = launch_attention_d<isa::MODE_TAYLOR>(d.D, tq, tk, tv, tkc, tvc, pf, d.items_f, d.BH, st)))
+        return rc;
   }
   record(events, 5, st);
   return ISA_OK;

@@ -226,8 +226,7 @@ def _run(inp: _Inputs, collect_trace: bool, pinned=None, out: Optional[torch.Ten
         means = ws[256: 256 + 3 * d.B * d.H * T * D * 4].view(torch.float32).view(3, d.B, d.H, T, D)
         qc, kc = means[0].clone(), means[1].clone()
         times = _LazyStageTimes({"coarse": (evs[0], evs[1]), "select": (evs[1], evs[2]),
-                                 "split": (evs[2], evs[3]), "kernel": (evs[3], evs[5]),
-                                 "kernel_exact": (evs[3], evs[4]), "kernel_taylor": (evs[4], evs[5])})
+                                 "split": (evs[2], evs[3]), "kernel": (evs[3], evs[5])})
         dict.__setitem__(times, "reconstruct", 0.0)
         routing = _make_routing(d, bufs)
         trace = IsaTrace(coarse_summary=_LazySummary(qc, kc, d.scale), selection=routing.selection,
