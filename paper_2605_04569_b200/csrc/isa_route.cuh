@@ -157,13 +157,20 @@ __global__ void __launch_bounds__(256) coarse_kernel(const float* __restrict__ q
   const int lr = threadIdx.x >> 1, ld = (threadIdx.x & 1) * 4;
   const int gi = i0 + lr;
   const int gj = colrow[lr];
+  const float* arow = gi < T ? qb + (long long)gi * D + ld : nullptr;
+  const float* brow = gj >= 0 ? kb + (long long)gj * D + ld : nullptr;
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  // register prefetch of the next k-chunk hides the global-load latency
+  float4 a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow)) : zero4;
+  float4 b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow)) : zero4;
   for (int d0 = 0; d0 < D; d0 += 8) {
-    float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f), b4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gi < T) a4 = *reinterpret_cast<const float4*>(qb + (long long)gi * D + d0 + ld);
-    if (gj >= 0) b4 = *reinterpret_cast<const float4*>(kb + (long long)gj * D + d0 + ld);
     As[ld + 0][lr] = a4.x; As[ld + 1][lr] = a4.y; As[ld + 2][lr] = a4.z; As[ld + 3][lr] = a4.w;
     Bs[ld + 0][lr] = b4.x; Bs[ld + 1][lr] = b4.y; Bs[ld + 2][lr] = b4.z; Bs[ld + 3][lr] = b4.w;
     __syncthreads();
+    if (d0 + 8 < D) {
+      a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow + d0 + 8)) : zero4;
+      b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow + d0 + 8)) : zero4;
+    }
 #pragma unroll
     for (int dd = 0; dd < 8; ++dd) {
       double a[8], bv[8];

@@ -292,9 +292,14 @@ def dense_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: Op
     return out
 
 
-def prepare(q, k, v, icl, cfg):
-    """Validated inputs + a reusable workspace for repeated calls (bench/CUDA graphs)."""
+def prepare(q, k, v, icl, cfg, separate_branches: bool = False):
+    """Validated inputs + a reusable workspace for repeated calls (bench/CUDA graphs).
+
+    separate_branches launches the exact and Taylor attention branches as two
+    kernels (per-branch profiling) instead of the default fused grid."""
     inp = _Inputs(q, k, v, icl, cfg)
+    if separate_branches:
+        inp.knobs.flags |= 1
     ws, nbytes = inp.workspace()
     return _Prepared(inp, ws, nbytes)
 
