@@ -17,12 +17,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 
 #include "../../include/isa_b200.h"
 #include "isa_attn.cuh"
+#include "isa_attn_p2.cuh"
 #include "isa_route.cuh"
 
 namespace {
@@ -88,6 +90,17 @@ int make_map(CUtensorMap* m, const void* ptr, int D, long long d1, long long d2,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ISA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return ISA_OK;
+}
+
+// Exact/dense attention pipeline: 2 = double-buffered 64-key tiles
+// (isa_attn_p2.cuh, default), 1 = single-buffered 128-key tiles. ISA_PIPE=1|2
+// in the environment overrides (A/B measurements).
+int pipe_mode() {
+  static int mode = [] {
+    const char* e = getenv("ISA_PIPE");
+    return (e && e[0] == '1') ? 1 : 2;
+  }();
+  return mode;
 }
 
 // ---------------------------------------------------------------- geometry
@@ -220,6 +233,39 @@ int launch_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtenso
   return ISA_OK;
 }
 
+template <int D, int MODE>
+int launch_attention_p2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                        const isa::AttnParams& p, int items, int BH, cudaStream_t st) {
+  using L = isa::P2Smem<D>;
+  static bool configured = false;
+  if (!configured) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::gba_attention_p2_kernel<D, MODE>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
+    configured = true;
+  }
+  if (items < 1) return ISA_OK;
+  isa::gba_attention_p2_kernel<D, MODE><<<dim3(items, BH), isa::kThreads, L::kAlloc, st>>>(tq, tk, tv, p);
+  ISA_LAUNCHED("gba_attention_p2_kernel");
+  return ISA_OK;
+}
+
+template <int D>
+int launch_isa_fused_p2_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                          const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& pe,
+                          const isa::AttnParams& pt, int items_e, int items_t, int BH, cudaStream_t st) {
+  constexpr int kA = isa::P2Smem<D>::kAlloc > isa::AttnSmem<D>::kAlloc ? isa::P2Smem<D>::kAlloc
+                                                                        : isa::AttnSmem<D>::kAlloc;
+  static bool configured = false;
+  if (!configured) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::gba_isa_p2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kA));
+    configured = true;
+  }
+  isa::gba_isa_p2_kernel<D><<<dim3(items_e + items_t, BH), isa::kThreads, kA, st>>>(tq, tk, tv, tkc, tvc, pe, pt,
+                                                                                    items_e);
+  ISA_LAUNCHED("gba_isa_p2_kernel");
+  return ISA_OK;
+}
+
 template <int D>
 int launch_isa_fused_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
                        const CUtensorMap& tvc, const isa::AttnParams& pe, const isa::AttnParams& pt, int items_e,
@@ -239,6 +285,10 @@ int launch_isa_fused_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUten
 int launch_isa_fused(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& pe,
                      const isa::AttnParams& pt, int items_e, int items_t, int BH, cudaStream_t st) {
+  if (pipe_mode() == 2) {
+    if (D == 128) return launch_isa_fused_p2_t<128>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
+    return launch_isa_fused_p2_t<64>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
+  }
   if (D == 128) return launch_isa_fused_t<128>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
   return launch_isa_fused_t<64>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
 }
@@ -247,6 +297,12 @@ template <int MODE>
 int launch_attention_d(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& p, int items, int BH,
                        cudaStream_t st) {
+  if constexpr (MODE != isa::MODE_TAYLOR) {
+    if (pipe_mode() == 2) {
+      if (D == 128) return launch_attention_p2<128, MODE>(tq, tk, tv, p, items, BH, st);
+      return launch_attention_p2<64, MODE>(tq, tk, tv, p, items, BH, st);
+    }
+  }
   if (D == 128) return launch_attention<128, MODE>(tq, tk, tv, tkc, tvc, p, items, BH, st);
   return launch_attention<64, MODE>(tq, tk, tv, tkc, tvc, p, items, BH, st);
 }
