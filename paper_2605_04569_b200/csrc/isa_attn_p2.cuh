@@ -43,9 +43,12 @@ __device__ __forceinline__ void gba_body_p2(const CUtensorMap& tm_q, const CUten
   uint64_t* kv_full = bars + 2;                 // [kP2Slots]
   uint64_t* kv_empty = bars + 2 + kP2Slots;     // [kP2Slots]
   uint64_t* s_full = bars + 2 + 2 * kP2Slots;   // [2 stages][2 buffers]
-  uint64_t* p_full = bars + 6 + 2 * kP2Slots;   // [2]
-  uint64_t* o_ready = bars + 8 + 2 * kP2Slots;  // [2] one phase per PV
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 2 * kP2Slots);
+  // p_full per (stage, buffer): the softmax can run two tiles ahead of the MMA
+  // warp, so one barrier per stage would alias phases i and i+2.
+  uint64_t* p_full = bars + 6 + 2 * kP2Slots;   // [2 stages][2 buffers]
+  uint64_t* o_ready = bars + 10 + 2 * kP2Slots; // [2] one phase per PV (rescale waits)
+  uint64_t* o_full = bars + 12 + 2 * kP2Slots;  // [2] after the last PV (epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14 + 2 * kP2Slots);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -58,10 +61,13 @@ __device__ __forceinline__ void gba_body_p2(const CUtensorMap& tm_q, const CUten
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int s = 0; s < 4; ++s) mbar_init(&s_full[s], 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], 4);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&o_ready[s], 1);
+      mbar_init(&o_full[s], 1);
     }
     fence_barrier_init();
   }
@@ -181,11 +187,12 @@ __device__ __forceinline__ void gba_body_p2(const CUtensorMap& tm_q, const CUten
         wait_entry(cv);
         if (ck >= 0) wait_entry(ck);
         for (int s = 0; s < 2; ++s) {
-          mbar_wait(&p_full[s], i & 1);
+          mbar_wait(&p_full[2 * s + buf], (i >> 1) & 1);
           __syncwarp();
           tc_fence_after();
           issue_pv(s, buf, cv % kP2Slots, i > 0);
           commit(&o_ready[s]);
+          if (i == n_kv - 1) commit(&o_full[s]);
           if (ck >= 0) {
             issue_qk(s, buf, ck % kP2Slots);  // S_s[buf] is free once PV(i) is in the pipe
             commit(&s_full[2 * s + buf]);
@@ -296,11 +303,13 @@ __device__ __forceinline__ void gba_body_p2(const CUtensorMap& tm_q, const CUten
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[s]);
+      if (lane == 0) mbar_arrive(&p_full[2 * s + buf]);
       l += s2.x + s2.y;
     }
     // -------------------------------------------------------------- epilogue
-    mbar_wait(&o_ready[s], (n_kv - 1) & 1);
+    // S(n-1) only implies PV(n-3), and o_ready's parity cannot tell phase n-2
+    // from n: the last PV has its own barrier.
+    mbar_wait(&o_full[s], 0);
     __syncwarp();
     tc_fence_after();
     const int u = query_block<MODE>(p, bh, item, qb);
