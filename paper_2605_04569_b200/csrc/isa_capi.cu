@@ -92,13 +92,16 @@ int make_map(CUtensorMap* m, const void* ptr, int D, long long d1, long long d2,
   return ISA_OK;
 }
 
-// Exact/dense attention pipeline: 2 = double-buffered 64-key tiles
-// (isa_attn_p2.cuh, default), 1 = single-buffered 128-key tiles. ISA_PIPE=1|2
-// in the environment overrides (A/B measurements).
+// Exact/dense attention pipeline: 1 = single-buffered 128-key tiles
+// (isa_attn.cuh, default), 2 = double-buffered 64-key tiles (isa_attn_p2.cuh).
+// Measured on B200 (same box, cfg3): pipe 1 K6 1159 TFLOP/s, pipe 2 934 —
+// the N=64 QK re-reads Q from shared memory twice as often and the extra
+// operand traffic costs more than the hidden MMA round trip saves. Kept
+// selectable (ISA_PIPE=2) for A/B measurements.
 int pipe_mode() {
   static int mode = [] {
     const char* e = getenv("ISA_PIPE");
-    return (e && e[0] == '1') ? 1 : 2;
+    return (e && e[0] == '2') ? 2 : 1;
   }();
   return mode;
 }
