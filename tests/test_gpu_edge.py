@@ -1,0 +1,166 @@
+"""GPU edge cases and full-scale geometry (north-star sizes) against the CPU
+oracle: strided inputs, batches, knob extremes, ragged segments (strict=False),
+cfg3 and cfg5 geometries on a head subset (heads are independent), large
+scores, determinism. Routing must match bit-exactly; outputs within max-abs
+2e-2 / cosine 0.999 of the fp32 reference."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import isa_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _P():
+    import paper_2605_04569_b200 as P
+
+    return P
+
+
+def _bf16(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda().to(torch.bfloat16)
+
+
+def _inputs(B, H, S, D, seed, scale=1.0, kind="iid-gaussian"):
+    if kind == "iid-gaussian":
+        rng = np.random.default_rng(seed)
+        q, k, v = (rng.standard_normal((B, H, S, D)).astype(np.float32) * s for s in (scale, scale, 1.0))
+    else:
+        q, k, v = O.workload(kind, B, H, S, D, seed)
+    return tuple(O.round_bf16(x) for x in (q, k, v))
+
+
+def _sampled_rows(asm, frac, l_src, l_ctx):
+    """Token rows (per (b, h)) the oracle computed with forward(block_fraction=frac)."""
+    b = 64
+    B, H = asm.sharp.shape[:2]
+    rows = np.zeros((B, H, l_src + l_ctx), dtype=bool)
+    ns = int(math.ceil(frac * asm.n_sharp))
+    nf = int(math.ceil(frac * asm.n_flat))
+    for bi in range(B):
+        for hi in range(H):
+            blocks = list(asm.sharp[bi, hi, :ns]) + list(asm.flat[bi, hi, :nf])
+            for u in blocks:
+                if u < asm.t_src:
+                    lo, hi_ = u * b, min(u * b + b, l_src)
+                else:
+                    lo = l_src + (u - asm.t_src) * b
+                    hi_ = min(lo + b, l_src + l_ctx)
+                rows[bi, hi, lo:hi_] = True
+    return rows
+
+
+def _check(out, ref, rows=None, max_abs=2e-2, min_cos=0.999):
+    a = out.float().cpu().numpy().astype(np.float64)
+    r = np.asarray(ref, dtype=np.float64)
+    if rows is not None:
+        a, r = a[rows], r[rows]
+    a, r = a.ravel(), r.ravel()
+    err = float(np.max(np.abs(a - r)))
+    cos = float(a @ r / (np.linalg.norm(a) * np.linalg.norm(r) + 1e-300))
+    assert err <= max_abs and cos >= min_cos, f"max_abs={err:.3e} cos={cos:.6f}"
+
+
+def _run_and_compare(q, k, v, l_src, l_ctx, cfg_kw, frac=1.0):
+    P = _P()
+    strict = cfg_kw.get("strict", True)
+    okw = {kk: vv for kk, vv in cfg_kw.items() if kk in ("alpha_s", "alpha_ns", "alpha_f", "softmax_first")}
+    asm = O.OracleAssembly(q, k, v, l_src, l_ctx, **okw)
+    out_ref = asm.forward(block_fraction=frac)
+    out, tr = P.isa_forward(_bf16(q), _bf16(k), _bf16(v), P.IclLayout(l_src, l_ctx),
+                            P.IsaConfig(strict=strict, **okw))
+    np.testing.assert_array_equal(tr.selection.numpy(), asm.sel)
+    np.testing.assert_array_equal(tr.split.sharp.cpu().numpy(), asm.sharp)
+    np.testing.assert_array_equal(tr.split.flat.cpu().numpy(), asm.flat)
+    if asm.mask is not None:
+        np.testing.assert_array_equal(tr.mask.numpy(), asm.mask)
+    rows = None if frac >= 1.0 else _sampled_rows(asm, frac, l_src, l_ctx)
+    _check(out, out_ref, rows)
+    return out
+
+
+# ------------------------------------------------------------------ addressing / batching
+def test_strided_bshd_inputs_match_contiguous():
+    """Q/K/V given as (B,S,H,D) storage permuted to (B,H,S,D): TMA descriptors
+    carry the strides, results are bit-identical to the contiguous call."""
+    P = _P()
+    torch.manual_seed(0)
+    B, S, H, D = 2, 2048, 3, 128
+    x = [torch.randn(B, S, H, D, device="cuda").to(torch.bfloat16) for _ in range(3)]
+    q, k, v = (t.permute(0, 2, 1, 3) for t in x)
+    assert not q.is_contiguous()
+    icl, cfg = P.IclLayout(1024, 1024), P.IsaConfig()
+    a, _ = P.isa_forward(q, k, v, icl, cfg, collect_trace=False)
+    b, _ = P.isa_forward(q.contiguous(), k.contiguous(), v.contiguous(), icl, cfg, collect_trace=False)
+    assert torch.equal(a, b)
+
+
+def test_batch_and_heads_vs_oracle():
+    q, k, v = _inputs(2, 3, 2048, 64, seed=1)
+    _run_and_compare(q, k, v, 1024, 1024, {})
+
+
+def test_deterministic():
+    P = _P()
+    q, k, v = (_bf16(x) for x in _inputs(1, 4, 4096, 128, seed=2))
+    icl, cfg = P.IclLayout(2048, 2048), P.IsaConfig()
+    a, _ = P.isa_forward(q, k, v, icl, cfg, collect_trace=False)
+    b, _ = P.isa_forward(q, k, v, icl, cfg, collect_trace=False)
+    assert torch.equal(a, b)
+
+
+# ------------------------------------------------------------------ knob extremes (reference test_pipeline.py)
+@pytest.mark.parametrize("kw", [
+    dict(alpha_s=0.0),                      # source-only keys (coarse.py:153-154 k_ctx = 0)
+    dict(alpha_f=1.0),                      # every query block on the Taylor branch
+    dict(alpha_f=0.0),                      # every query block exact
+    dict(alpha_f=1.0, alpha_ns=1.0),        # Taylor with every block exact
+    dict(alpha_s=1.0, alpha_ns=0.01),       # k = max(1, floor) floor clamp
+    dict(alpha_s=0.3, alpha_f=0.7, alpha_ns=0.2),
+    dict(softmax_first=False),
+])
+def test_knob_extremes_vs_oracle(kw):
+    q, k, v = _inputs(1, 2, 4096, 128, seed=3, kind="clustered")
+    _run_and_compare(q, k, v, 2048, 2048, kw)
+
+
+# ------------------------------------------------------------------ ragged segments (strict=False)
+@pytest.mark.parametrize("l_src,l_ctx", [(100, 30), (1000, 1), (64 * 7 + 1, 64 * 9 - 5), (2000, 0), (65, 64)])
+def test_ragged_vs_oracle(l_src, l_ctx):
+    q, k, v = _inputs(1, 2, l_src + l_ctx, 64, seed=l_src + l_ctx)
+    _run_and_compare(q, k, v, l_src, l_ctx, dict(strict=False, alpha_s=0.5, alpha_ns=0.25))
+
+
+def test_strict_mode_rejects_ragged():
+    P = _P()
+    q = torch.zeros(1, 1, 130, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(P.ConfigError):
+        P.isa_forward(q, q, q, P.IclLayout(100, 30), P.IsaConfig())
+
+
+# ------------------------------------------------------------------ numerics
+def test_large_scores_stay_finite_and_accurate():
+    """Peaked attention (reference test_taylor.py:150-167 / test_reference.py:126-135)."""
+    q, k, v = _inputs(1, 2, 2048, 64, seed=4, scale=6.0)
+    out = _run_and_compare(q, k, v, 1024, 1024, {})
+    assert torch.isfinite(out.float()).all()
+
+
+# ------------------------------------------------------------------ north-star geometries on a head subset
+@pytest.mark.slow
+def test_cfg3_geometry_one_head_vs_oracle():
+    """32K + 32K, D = 128 (BASELINE configs[2]); routing over the full head,
+    output on a 1/16 sample of the query blocks."""
+    q, k, v = _inputs(1, 1, 65536, 128, seed=5)
+    _run_and_compare(q, k, v, 32768, 32768, {}, frac=1 / 16)
+
+
+@pytest.mark.slow
+def test_cfg5_ragged_geometry_one_head_vs_oracle():
+    """50,000 + 50,000 tokens (BASELINE configs[4] as ragged segments)."""
+    q, k, v = _inputs(1, 1, 100000, 128, seed=6, kind="clustered")
+    _run_and_compare(q, k, v, 50000, 50000, dict(strict=False), frac=1 / 32)
