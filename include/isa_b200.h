@@ -12,9 +12,11 @@
  * exactly as INTEGRATION.md shows a maintainer would.
  *
  * Conventions: plain C types only; every pointer to tensor data is a CUDA
- * device pointer; every call is asynchronous and ordered on `stream`; the
+ * device pointer (except the host-streamed isa_forward_host, whose q/k/v/out
+ * are host pointers); every call is asynchronous and ordered on `stream`; the
  * caller owns all buffers (inputs, outputs, workspace, routing arrays); no
- * hidden allocations and no host synchronisation. Thread-safe for distinct
+ * hidden allocations (isa_forward_host keeps a per-thread ring of 5 CUDA
+ * events) and no host synchronisation. Thread-safe for distinct
  * streams/workspaces. Every entry point returns an IsaStatus; on failure
  * isa_last_error() (thread-local) describes it. Status codes map 1:1 onto the
  * reference exception classes (errors.py:4-37).
@@ -121,6 +123,22 @@ int isa_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* by
 int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
                 void* out, void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned,
                 IsaRoutingOut* routing, int32_t* err_word, const IsaEvents* events, void* stream);
+
+/* Host-streamed pipeline: q/k/v/out are HOST pointers (contiguous (B,H,S,D);
+ * page-locked for copy/compute overlap). The flattened (b,h) range is processed
+ * in chunks of `heads_per_chunk` heads (<= 0: ceil(B*H/8)); the H2D copy of
+ * chunk c+1 (streams[1]) and the D2H copy of chunk c-1 (streams[2]) overlap the
+ * device pipeline of chunk c (streams[0]). streams[0] completes after the last
+ * D2H. `stage` (device, caller-owned) and `workspace` are sized by
+ * isa_forward_host_bytes. `pinned`/`routing` are device arrays for all B*H
+ * heads, as in isa_forward. Same operator as isa_forward (pipeline.py:307-328):
+ * heads are independent (reference.py:159-160, taylor.py:176-177). */
+int isa_forward_host_bytes(const IsaShape* shape, const IsaKnobs* knobs, int32_t heads_per_chunk,
+                           size_t* stage_bytes, size_t* workspace_bytes);
+int isa_forward_host(const IsaShape* shape, const IsaKnobs* knobs, const void* q_host, const void* k_host,
+                     const void* v_host, void* out_host, int32_t heads_per_chunk, void* stage, size_t stage_bytes,
+                     void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
+                     int32_t* err_word, void* const* streams);
 
 /* Stages 1-3 only (isa_routing, pipeline.py:302-304). */
 int isa_routing(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,

@@ -32,6 +32,8 @@ EXPORTED_SYMBOLS = (
     "isa_topk_rows_f64",
     "isa_sharpness_rows_f64",
     "isa_split_rows_f64",
+    "isa_forward_host_bytes",
+    "isa_forward_host",
 )
 
 
@@ -107,6 +109,11 @@ _SIGS = {
     "isa_topk_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _I, _P]),
     "isa_sharpness_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P]),
     "isa_split_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P, _P]),
+    "isa_forward_host_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _I,
+                                              ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
+    "isa_forward_host": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _P, _P, _P, _P, _I, _P,
+                                        ctypes.c_size_t, _P, ctypes.c_size_t, ctypes.POINTER(IsaRoutingIn),
+                                        ctypes.POINTER(IsaRoutingOut), _P, ctypes.POINTER(_P)]),
 }
 
 

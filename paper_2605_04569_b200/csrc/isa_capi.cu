@@ -540,6 +540,69 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   return ISA_OK;
 }
 
+// ---------------------------------------------------------------- host-streamed execution
+// isa_forward_host: Q/K/V/out live in host memory. The flattened (b, h) range
+// is cut into chunks of `hc` heads; each chunk is an independent (1, hc, S, D)
+// problem (every stage is per head: reference.py:159-160, taylor.py:176-177).
+// Three streams overlap the PCIe traffic with the pipeline: H2D of chunk c+1
+// (streams[1]) and D2H of chunk c-1 (streams[2]) run under the pipeline of
+// chunk c (streams[0]). Device staging holds kSlots chunks of 3 inputs + 1
+// output, recycled through events.
+constexpr int kHostSlots = 2;
+
+struct HostPlan {
+  Dims d;            // whole problem
+  int hc, n_chunks;  // heads per chunk, chunks
+  size_t elem, chunk_bytes, stage_bytes, ws_bytes;
+};
+
+IsaShape chunk_shape(const IsaShape* sh, int heads) {
+  IsaShape c = *sh;
+  c.batch = 1;
+  c.heads = heads;
+  c.stride_s = sh->head_dim;
+  c.stride_h = (long long)sh->seq_len * sh->head_dim;
+  c.stride_b = c.stride_h * heads;
+  return c;
+}
+
+int host_plan(const IsaShape* sh, const IsaKnobs* kn, int heads_per_chunk, HostPlan* hp) {
+  int rc = derive(sh, kn, &hp->d);
+  if (rc) return rc;
+  const Dims& d = hp->d;
+  const long long sd = (long long)d.S * d.D;
+  if (sh->stride_s != d.D || sh->stride_h != sd || sh->stride_b != sd * d.H)
+    return fail(ISA_ERR_LAYOUT, "host-streamed q/k/v must be contiguous (B,H,S,D)");
+  int hc = heads_per_chunk > 0 ? heads_per_chunk : (d.BH + 7) / 8;
+  if (hc > d.BH) hc = d.BH;
+  if (hc < 1) hc = 1;
+  hp->hc = hc;
+  hp->n_chunks = (d.BH + hc - 1) / hc;
+  hp->elem = sh->dtype == ISA_DTYPE_BF16 ? 2 : 4;
+  hp->chunk_bytes = align256((size_t)hc * sd * hp->elem);
+  hp->stage_bytes = (size_t)kHostSlots * 4 * hp->chunk_bytes;
+  IsaShape cs = chunk_shape(sh, hc);
+  Dims cd;
+  if ((rc = derive(&cs, kn, &cd))) return rc;
+  hp->ws_bytes = carve(cd, sh->dtype, nullptr).bytes;
+  return ISA_OK;
+}
+
+// Per-thread, per-device event ring (created on first use; timing disabled).
+constexpr int kMaxDevices = 16;
+cudaEvent_t* host_events() {
+  thread_local cudaEvent_t ev[kMaxDevices][3 * kHostSlots + 1] = {};
+  thread_local bool made[kMaxDevices] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+  if (!made[dev]) {
+    for (auto& e : ev[dev])
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    made[dev] = true;
+  }
+  return ev[dev];
+}
+
 }  // namespace
 
 extern "C" {
@@ -732,6 +795,98 @@ int isa_split_rows_f64(const double* m, int32_t rows, int32_t n, int32_t n_flat,
   int rc = select_rows(m, rows, n, n - n_flat, flags, nullptr, sharp, nullptr, flat, st);
   cudaFreeAsync(flags, st);
   return rc;
+}
+
+int isa_forward_host_bytes(const IsaShape* shape, const IsaKnobs* knobs, int32_t heads_per_chunk,
+                           size_t* stage_bytes, size_t* workspace_bytes) {
+  HostPlan hp;
+  int rc = host_plan(shape, knobs, heads_per_chunk, &hp);
+  if (rc) return rc;
+  if (!stage_bytes || !workspace_bytes) return fail(ISA_ERR_CONFIG, "null byte counts");
+  *stage_bytes = hp.stage_bytes;
+  *workspace_bytes = hp.ws_bytes;
+  return ISA_OK;
+}
+
+int isa_forward_host(const IsaShape* shape, const IsaKnobs* knobs, const void* q_host, const void* k_host,
+                     const void* v_host, void* out_host, int32_t heads_per_chunk, void* stage, size_t stage_bytes,
+                     void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
+                     int32_t* err_word, void* const* streams) {
+  HostPlan hp;
+  int rc = host_plan(shape, knobs, heads_per_chunk, &hp);
+  if (rc) return rc;
+  if (!q_host || !k_host || !v_host || !out_host) return fail(ISA_ERR_LAYOUT, "null host q/k/v/out");
+  if (!stage || stage_bytes < hp.stage_bytes)
+    return fail(ISA_ERR_CONFIG, "staging buffer too small (%zu < %zu)", stage_bytes, hp.stage_bytes);
+  if (!workspace || workspace_bytes < hp.ws_bytes)
+    return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, hp.ws_bytes);
+  if (!streams) return fail(ISA_ERR_CONFIG, "null streams");
+  cudaStream_t s_comp = static_cast<cudaStream_t>(streams[0]);
+  cudaStream_t s_in = static_cast<cudaStream_t>(streams[1]);
+  cudaStream_t s_out = static_cast<cudaStream_t>(streams[2]);
+  cudaEvent_t* ev = host_events();
+  if (!ev) return fail(ISA_ERR_CUDA, "cudaEventCreate failed");
+  cudaEvent_t* in_done = ev;                 // [slot] inputs resident
+  cudaEvent_t* comp_done = ev + kHostSlots;  // [slot] pipeline finished (inputs free, output ready)
+  cudaEvent_t* out_done = ev + 2 * kHostSlots;  // [slot] output copied back (output slot free)
+  cudaEvent_t start = ev[3 * kHostSlots];
+  // the copy streams must not run ahead of work already queued on the caller's stream
+  ISA_CUDA(cudaEventRecord(start, s_comp));
+  ISA_CUDA(cudaStreamWaitEvent(s_in, start, 0));
+  ISA_CUDA(cudaStreamWaitEvent(s_out, start, 0));
+  const Dims& d = hp.d;
+  const size_t head_bytes = (size_t)d.S * d.D * hp.elem;
+  const uint8_t* src[3] = {static_cast<const uint8_t*>(q_host), static_cast<const uint8_t*>(k_host),
+                           static_cast<const uint8_t*>(v_host)};
+  int launches = 0;
+  for (int c = 0; c < hp.n_chunks; ++c) {
+    const int slot = c % kHostSlots;
+    const int bh0 = c * hp.hc;
+    const int nh = d.BH - bh0 < hp.hc ? d.BH - bh0 : hp.hc;
+    uint8_t* base = static_cast<uint8_t*>(stage) + (size_t)slot * 4 * hp.chunk_bytes;
+    uint8_t* dq = base;
+    uint8_t* dout = base + 3 * hp.chunk_bytes;
+    // H2D: the slot's inputs are free once the pipeline two chunks back is done
+    if (c >= kHostSlots) ISA_CUDA(cudaStreamWaitEvent(s_in, comp_done[slot], 0));
+    for (int t = 0; t < 3; ++t)
+      ISA_CUDA(cudaMemcpyAsync(dq + t * hp.chunk_bytes, src[t] + bh0 * head_bytes, nh * head_bytes,
+                               cudaMemcpyHostToDevice, s_in));
+    ISA_CUDA(cudaEventRecord(in_done[slot], s_in));
+    // pipeline on the chunk; its output slot is free once its last D2H finished
+    ISA_CUDA(cudaStreamWaitEvent(s_comp, in_done[slot], 0));
+    if (c >= kHostSlots) ISA_CUDA(cudaStreamWaitEvent(s_comp, out_done[slot], 0));
+    IsaShape cs = chunk_shape(shape, nh);
+    IsaRoutingOut ro{};
+    if (routing) {
+      ro.selection = routing->selection ? routing->selection + (long long)bh0 * d.k_ctx : nullptr;
+      ro.sharp = routing->sharp ? routing->sharp + (long long)bh0 * d.n_sharp : nullptr;
+      ro.flat = routing->flat ? routing->flat + (long long)bh0 * d.n_flat : nullptr;
+      ro.mask = routing->mask ? routing->mask + (long long)bh0 * d.n_flat * d.k : nullptr;
+      ro.sharpness = routing->sharpness ? routing->sharpness + (long long)bh0 * d.T : nullptr;
+      ro.ctx_scores = routing->ctx_scores ? routing->ctx_scores + (long long)bh0 * d.t_ctx : nullptr;
+    }
+    IsaRoutingIn pi{};
+    if (pinned) {
+      pi.selection = pinned->selection ? pinned->selection + (long long)bh0 * d.k_ctx : nullptr;
+      pi.sharp = pinned->sharp ? pinned->sharp + (long long)bh0 * d.n_sharp : nullptr;
+      pi.flat = pinned->flat ? pinned->flat + (long long)bh0 * d.n_flat : nullptr;
+      pi.mask = pinned->mask ? pinned->mask + (long long)bh0 * d.n_flat * d.k : nullptr;
+    }
+    rc = isa_forward(&cs, knobs, dq, dq + hp.chunk_bytes, dq + 2 * hp.chunk_bytes, dout, workspace,
+                     workspace_bytes, pinned ? &pi : nullptr, routing ? &ro : nullptr, err_word, nullptr, s_comp);
+    if (rc) return rc;
+    launches += g_launches;
+    ISA_CUDA(cudaEventRecord(comp_done[slot], s_comp));
+    // D2H of the chunk's output
+    ISA_CUDA(cudaStreamWaitEvent(s_out, comp_done[slot], 0));
+    ISA_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(out_host) + bh0 * head_bytes, dout, nh * head_bytes,
+                             cudaMemcpyDeviceToHost, s_out));
+    ISA_CUDA(cudaEventRecord(out_done[slot], s_out));
+  }
+  // join: the caller's stream completes only after the last D2H
+  ISA_CUDA(cudaStreamWaitEvent(s_comp, out_done[(hp.n_chunks - 1) % kHostSlots], 0));
+  g_launches = launches;
+  return ISA_OK;
 }
 
 }  // extern "C"

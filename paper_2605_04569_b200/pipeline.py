@@ -10,8 +10,12 @@ plus `dense_attention` (the full_attention oracle / dense baseline,
 reference.py:79-123) on the same sm_100a kernel.
 
 Inputs may be torch CUDA tensors (bf16 or fp32; any B/H/S strides with a
-contiguous D axis) or numpy arrays (copied to the current CUDA device; the
-result is returned as a numpy float32 array, like the reference). All compute
+contiguous D axis), or HOST data: numpy arrays (cast to float32 like the
+reference, result returned as a numpy float32 array) or CPU torch tensors
+(bf16/fp32; result returned as a CPU tensor of the input dtype). Host data is
+streamed through the GPU head-chunk by head-chunk by the native
+`isa_forward_host` (H2D of chunk c+1 and D2H of chunk c-1 overlap the device
+pipeline of chunk c; pass page-locked tensors for the overlap). All compute
 runs in libisa_b200.so; there is no CPU path.
 """
 
@@ -55,7 +59,17 @@ class _Inputs:
         self.cfg = cfg_from_any(cfg).validate_b200()
         self.icl = icl_from_any(icl)
         self.numpy_io = isinstance(q, np.ndarray)
-        q, k, v = (self._to_device(x, n) for x, n in ((q, "Q"), (k, "K"), (v, "V")))
+        self.host = all(isinstance(x, np.ndarray) or (isinstance(x, torch.Tensor) and not x.is_cuda)
+                        for x in (q, k, v))
+        if self.host:
+            if not torch.cuda.is_available():
+                raise LayoutError("host Q/K/V are streamed through a CUDA device and none is available "
+                                  "(there is no CPU path)")
+            q, k, v = (self._to_host(x, n) for x, n in ((q, "Q"), (k, "K"), (v, "V")))
+            if q.dtype != k.dtype or q.dtype != v.dtype:
+                q, k, v = q.float(), k.float(), v.float()
+        else:
+            q, k, v = (self._to_device(x, n) for x, n in ((q, "Q"), (k, "K"), (v, "V")))
         if not (q.shape == k.shape == v.shape):
             raise LayoutError(f"Q/K/V must share one shape, got {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
         if q.stride() != k.stride() or q.stride() != v.stride() or q.dtype != k.dtype or q.dtype != v.dtype:
@@ -79,6 +93,21 @@ class _Inputs:
         self.knobs = N.IsaKnobs(d.scale, d.k_ctx, d.n_flat, max(d.k, 1), int(bool(self.cfg.softmax_first)), 0)
 
     @staticmethod
+    def _to_host(x, name):
+        """Host operand for the streamed path: contiguous (B,H,S,D), bf16 or fp32."""
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+        if x.dim() != 4:
+            raise LayoutError(f"{name}: expected 4 axes (B,H,S,D), got shape {tuple(x.shape)}")
+        if min(x.shape) < 1:
+            raise LayoutError(f"{name}: all dims must be >= 1, got shape {tuple(x.shape)}")
+        if x.dtype not in (torch.bfloat16, torch.float32):
+            if not x.is_floating_point():
+                raise InputError(f"{name}: floating-point input required")
+            x = x.float()
+        return x.contiguous()
+
+    @staticmethod
     def _to_device(x, name):
         if isinstance(x, np.ndarray):
             if x.ndim != 4:
@@ -91,7 +120,7 @@ class _Inputs:
         if min(x.shape) < 1:
             raise LayoutError(f"{name}: all dims must be >= 1, got shape {tuple(x.shape)}")
         if not x.is_cuda:
-            raise LayoutError(f"{name}: tensor must live on a CUDA device (no CPU path)")
+            raise LayoutError(f"{name}: Q, K and V must all be CUDA tensors or all host data (no CPU path)")
         if x.dtype not in (torch.bfloat16, torch.float32):
             if not x.is_floating_point():
                 raise InputError(f"{name}: floating-point input required")
@@ -102,6 +131,10 @@ class _Inputs:
         if any((s * elem) % 16 for s in x.stride()[:3]) or x.data_ptr() % 16:
             x = x.contiguous()
         return x
+
+    @property
+    def device(self):
+        return torch.device("cuda", torch.cuda.current_device()) if self.host else self.q.device
 
     def workspace(self):
         nbytes = ctypes.c_size_t(0)
@@ -190,7 +223,78 @@ def _pinned_struct(routing, d: IsaDims, device):
     return N.IsaRoutingIn(*(_ptr(t) if t is not None and t.numel() else None for t in keep)), keep
 
 
-def _run(inp: _Inputs, collect_trace: bool, pinned=None, out: Optional[torch.Tensor] = None, validate=True):
+_SIDE_STREAMS: dict = {}
+
+
+def _side_streams(dev):
+    """Two long-lived copy streams per device for the host-streamed path."""
+    key = dev.index
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return _SIDE_STREAMS[key]
+
+
+def _run_host(inp: _Inputs, collect_trace: bool, pinned=None, out=None, validate=True, heads_per_chunk=0):
+    """Host data in, host data out: native head-chunk streaming (isa_forward_host)."""
+    lib = N.load()
+    d = inp.dims
+    dev = inp.device
+    st_b, ws_b = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    N.check(lib.isa_forward_host_bytes(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), int(heads_per_chunk),
+                                       ctypes.byref(st_b), ctypes.byref(ws_b)))
+    stage = torch.empty(int(st_b.value), dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(ws_b.value), dtype=torch.uint8, device=dev)
+    pin = inp.q.is_pinned()
+    if out is None:
+        out = torch.empty((d.B, d.H, d.S, d.D), dtype=inp.q.dtype, pin_memory=pin)
+    elif not (isinstance(out, torch.Tensor) and not out.is_cuda and out.is_contiguous()
+              and tuple(out.shape) == (d.B, d.H, d.S, d.D) and out.dtype == inp.q.dtype):
+        raise LayoutError("out must be a contiguous host (B,H,S,D) tensor of the input dtype")
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    bufs = _routing_buffers(d, dev) if collect_trace else None
+    rout = _routing_struct(bufs) if bufs is not None else None
+    pin_struct, keep = (None, None)
+    if pinned is not None:
+        pin_struct, keep = _pinned_struct(pinned, d, dev)
+    main = torch.cuda.current_stream(dev)
+    s_in, s_out = _side_streams(dev)
+    streams = (ctypes.c_void_p * 3)(main.cuda_stream, s_in.cuda_stream, s_out.cuda_stream)
+    e0 = e1 = None
+    if collect_trace:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+    N.check(lib.isa_forward_host(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), _ptr(inp.q), _ptr(inp.k),
+                                 _ptr(inp.v), _ptr(out), int(heads_per_chunk), _ptr(stage), st_b.value, _ptr(ws),
+                                 ws_b.value, ctypes.byref(pin_struct) if pin_struct else None,
+                                 ctypes.byref(rout) if rout else None, _ptr(err), streams))
+    if collect_trace:
+        e1.record(main)
+    # host results must be complete on return (CPU tensors carry no stream order)
+    if validate:
+        _raise_flags(err)
+    else:
+        main.synchronize()
+    # stage/ws return to the caching allocator on the main stream, which has
+    # joined both copy streams: later reuse is ordered after their last use
+    trace = None
+    if collect_trace:
+        times = _LazyStageTimes({"kernel": (e0, e1)})
+        for name in ("coarse", "select", "split", "reconstruct"):
+            dict.__setitem__(times, name, 0.0)  # not separable: stages of all chunks interleave
+        routing = _make_routing(d, bufs)
+        trace = IsaTrace(coarse_summary={"host_streamed": True}, selection=routing.selection,
+                         split=routing.split, mask=routing.mask, flops=d.flops(), stage_times_us=times)
+    del keep
+    if inp.numpy_io:
+        out = out.float().numpy()
+    return out, trace, bufs
+
+
+def _run(inp: _Inputs, collect_trace: bool, pinned=None, out: Optional[torch.Tensor] = None, validate=True,
+         heads_per_chunk: int = 0):
+    if inp.host:
+        return _run_host(inp, collect_trace, pinned=pinned, out=out, validate=validate,
+                         heads_per_chunk=heads_per_chunk)
     lib = N.load()
     d = inp.dims
     dev = inp.q.device
@@ -237,20 +341,26 @@ def _run(inp: _Inputs, collect_trace: bool, pinned=None, out: Optional[torch.Ten
     return out, trace, bufs
 
 
-def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = True, *, out=None, validate=True):
+def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = True, *, out=None, validate=True,
+                heads_per_chunk: int = 0):
     """Run the full pipeline; returns (output, IsaTrace or None) (pipeline.py:307-316).
 
     The output has the input dtype (bf16 in -> bf16 out; fp32 in -> fp32 out,
     computed with bf16 tensor cores and fp32 accumulation). Routing decisions
     are exact float64 restatements of the reference and match it bit-for-bit.
+    Host inputs (numpy / CPU tensors) are streamed through the GPU in chunks of
+    `heads_per_chunk` heads (0 = B*H/8); the result is complete on return.
     """
-    res, trace, _ = _run(_Inputs(q, k, v, icl, cfg), collect_trace, out=out, validate=validate)
+    res, trace, _ = _run(_Inputs(q, k, v, icl, cfg), collect_trace, out=out, validate=validate,
+                         heads_per_chunk=heads_per_chunk)
     return res, trace
 
 
 def isa_routing(q, k, v, icl: IclLayout, cfg: IsaConfig) -> IsaRouting:
     """Stages 1-3 only (pipeline.py:302-304); index tensors stay on the GPU."""
     inp = _Inputs(q, k, v, icl, cfg)
+    if inp.host:  # routing reads all of Q/K/V once: one plain upload
+        inp = _Inputs(*(t.cuda() for t in (inp.q, inp.k, inp.v)), icl, cfg)
     lib = N.load()
     d = inp.dims
     ws, nbytes = inp.workspace()

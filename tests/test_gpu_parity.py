@@ -250,3 +250,48 @@ def test_nonfinite_input_raises():
     q[0, 0, 5, 3] = float("nan")
     with pytest.raises(P.InputError):
         P.isa_forward(q, k, v, P.IclLayout(128, 128), P.IsaConfig())
+
+
+# ------------------------------------------------------------------ host-streamed path (isa_forward_host)
+@pytest.mark.parametrize("hpc", [0, 1, 4])
+def test_host_streamed_matches_device_path(hpc):
+    """CPU (pinned) bf16 tensors stream through the GPU in head chunks; the
+    result and the routing equal the all-device call bit-for-bit (heads are
+    independent, reference.py:159-160). hpc=4 leaves a ragged last chunk."""
+    P = _api()
+    rng = np.random.default_rng(11)
+    H, S, D = 6, 2048, 128
+    q, k, v = (torch.from_numpy(O.round_bf16(rng.standard_normal((1, H, S, D)).astype(np.float32)))
+               .to(torch.bfloat16) for _ in range(3))
+    icl, cfg = P.IclLayout(1024, 1024), P.IsaConfig()
+    ref, rtr = P.isa_forward(q.cuda(), k.cuda(), v.cuda(), icl, cfg)
+    qh, kh, vh = (t.pin_memory() for t in (q, k, v))
+    out, tr = P.isa_forward(qh, kh, vh, icl, cfg, heads_per_chunk=hpc)
+    assert not out.is_cuda and out.dtype == torch.bfloat16
+    assert torch.equal(out, ref.cpu())
+    assert torch.equal(tr.selection.indices, rtr.selection.indices)
+    assert torch.equal(tr.split.sharp, rtr.split.sharp) and torch.equal(tr.split.flat, rtr.split.flat)
+    assert torch.equal(tr.mask.indices, rtr.mask.indices)
+    assert tr.stage_times_us["kernel"] > 0
+
+
+def test_host_streamed_unpinned_and_pinned_routing():
+    """Pageable host memory works too (no overlap); isa_forward_with_routing on
+    host data takes the reference's numpy routing."""
+    P = _api()
+    c = GoldenCase("cfg1_iid_s0")
+    q, k, v = c.inputs()
+    icl, cfg = P.IclLayout(1024, 1024), P.IsaConfig()
+    qt, kt, vt = (torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16) for x in (q, k, v))
+    out, _ = P.isa_forward(qt, kt, vt, icl, cfg, heads_per_chunk=1)
+    _close(out, c.data["out"])
+    r = P.isa_routing(_bf16(q), _bf16(k), _bf16(v), icl, cfg)
+    a = P.isa_forward_with_routing(qt, kt, vt, icl, cfg, r)
+    assert torch.equal(a, out)
+
+
+def test_mixed_host_and_device_inputs_rejected():
+    P = _api()
+    x = torch.zeros(1, 1, 128, 64, dtype=torch.bfloat16)
+    with pytest.raises(P.LayoutError):
+        P.isa_forward(x, x.cuda(), x, P.IclLayout(64, 64), P.IsaConfig())

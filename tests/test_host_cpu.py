@@ -169,9 +169,40 @@ def test_native_missing_library_fails_loudly(tmp_path):
 
 
 def test_cpu_tensors_are_rejected_no_fallback():
+    """Host data is only ever streamed through the GPU: without one the call
+    fails loudly instead of computing on the CPU."""
     torch = pytest.importorskip("torch")
     import paper_2605_04569_b200 as P
 
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present: host data takes the streamed path")
     x = torch.zeros(1, 1, 128, 64)
     with pytest.raises(E.LayoutError):
         P.isa_forward(x, x, x, P.IclLayout(64, 64), P.IsaConfig())
+    with pytest.raises(E.LayoutError):
+        P.isa_forward(x.numpy(), x.numpy(), x.numpy(), P.IclLayout(64, 64), P.IsaConfig())
+
+
+def test_host_stream_plan_on_cpu():
+    """isa_forward_host_bytes: staging = 2 slots x (3 inputs + 1 output) chunks;
+    the chunk workspace equals isa_workspace_bytes of a (1, hc, S, D) problem."""
+    from paper_2605_04569_b200 import _native as N
+
+    lib = N.load()
+    kn = N.IsaKnobs(1 / math.sqrt(128), 64, 512, 36, 1, 0)
+    st, ws = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    assert lib.isa_forward_host_bytes(ctypes.byref(_shape(N)), ctypes.byref(kn), 5, ctypes.byref(st),
+                                      ctypes.byref(ws)) == 0
+    assert st.value == 2 * 4 * 5 * 65536 * 128 * 2
+    one = ctypes.c_size_t(0)
+    assert lib.isa_workspace_bytes(ctypes.byref(_shape(N, H=5)), ctypes.byref(kn), ctypes.byref(one)) == 0
+    assert ws.value == one.value
+    # default chunking: ceil(B*H/8) heads
+    assert lib.isa_forward_host_bytes(ctypes.byref(_shape(N)), ctypes.byref(kn), 0, ctypes.byref(st),
+                                      ctypes.byref(ws)) == 0
+    assert st.value == 2 * 4 * 5 * 65536 * 128 * 2
+    # non-contiguous host layouts are rejected (LayoutError)
+    sh = _shape(N)
+    sh.stride_s = 256
+    rc = lib.isa_forward_host_bytes(ctypes.byref(sh), ctypes.byref(kn), 5, ctypes.byref(st), ctypes.byref(ws))
+    assert E.STATUS_TO_ERROR[rc] is E.LayoutError
