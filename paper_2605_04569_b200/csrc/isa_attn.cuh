@@ -59,6 +59,9 @@ struct AttnParams {
   int* err_flag;
 };
 
+#ifndef ISA_TRACE_Q
+#define ISA_TRACE_Q 0  // softmax warp quadrant stamped by ISA_TRACE builds
+#endif
 constexpr int kThreads = 384;
 constexpr int kKvStages = 5;  // K/V ring slots (D=128: 64 KB Q + 5 x 32 KB = 224 KB)
 constexpr int kSoftmaxRegs = 208;
@@ -309,26 +312,31 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       const uint32_t sq = smem_u32(sQ);
       const uint32_t skv = smem_u32(sKV);
       const bool leader = elect_one();
+      // Shared-memory descriptors: one base per operand tile, per-k steps are
+      // constant 64-bit adds (keeps the issuing warp's instruction count low;
+      // it shares an SM sub-partition with two softmax warps).
+      const uint64_t dq_base = sdesc_sw128_base(sq, 16, 1024);
+      const uint64_t dk_base = sdesc_sw128_base(skv, 16, 1024);
+      const uint64_t dv_base = sdesc_sw128_base(skv, 16384, 1024);
       auto issue_qk = [&](int s, int slot) {
         if (leader) {
-          const uint32_t a0 = sq + s * L::kTileBytes;
-          const uint32_t b0 = skv + slot * L::kTileBytes;
+          const uint64_t da = dq_base + static_cast<uint64_t>((s * L::kTileBytes) >> 4);
+          const uint64_t db = dk_base + static_cast<uint64_t>((slot * L::kTileBytes) >> 4);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            mma_ss(tmem + s * 128, sdesc_sw128(a0 + off, 16, 1024), sdesc_sw128(b0 + off, 16, 1024), idesc_qk,
-                   kk > 0);
+            const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+            mma_ss(tmem + s * 128, da + off, db + off, idesc_qk, kk > 0);
           }
         }
         __syncwarp();
       };
       auto issue_pv = [&](int s, int slot, uint32_t acc) {
         if (leader) {
-          const uint32_t b0 = skv + slot * L::kTileBytes;
+          const uint64_t db = dv_base + static_cast<uint64_t>((slot * L::kTileBytes) >> 4);
           const uint32_t ta = tmem + s * 128 + 64;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            mma_ts(tmem + 256 + s * 128, ta + kk * 8, sdesc_sw128(b0 + kk * 2048, 16384, 1024), idesc_pv,
+            mma_ts(tmem + 256 + s * 128, ta + kk * 8, db + static_cast<uint64_t>((kk * 2048) >> 4), idesc_pv,
                    (acc | kk) != 0);
         }
         __syncwarp();
@@ -392,14 +400,17 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           const int ev = 2 * i - 1, ek = 2 * i;
           wait_entry(ev);
           wait_entry(ek);
+          if (leader) ISA_TSTAMP(i, 0, 5);
           if (leader) progress(1, 1000 * i + 1);
           for (int s = 0; s < 2; ++s) {
             mbar_wait(&p_full[s], (i - 1) & 1);
+            if (leader) ISA_TSTAMP(i, s, 6);
             __syncwarp();
             tc_fence_after();
             issue_pv(s, ev % kKvStages, i > 1);
             issue_qk(s, ek % kKvStages);
             commit(&s_full[s]);
+            if (leader) ISA_TSTAMP(i, s, 7);
           }
           release(ev);
           release(ek);
@@ -487,6 +498,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         t.bits0 = t.bits1 = 0xF;
       }
       mbar_wait(&s_full[s], i & 1);
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 0);
       __syncwarp();  // reconverge before .sync.aligned tcgen05 ops
       tc_fence_after();
 #ifdef ISA_EXP_NOSOFTMAX
@@ -501,6 +513,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[s]);
+        if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 4);
         l += 1.f;
         continue;
       }
@@ -518,6 +531,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       }
       tmem_ld_wait();
 #endif
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 1);
 #ifdef ISA_EXP_LOADONLY
       {
         float mm = -INFINITY;
@@ -532,6 +546,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[s]);
+        if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 4);
         l += 1.f;
         continue;
       }
@@ -571,6 +586,64 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       float mx[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+      bool force_rescale = false;
+#ifndef ISA_NO_SPEC_MAX
+      // Speculative hot path (dense tiles after the first): exponentiate
+      // against the running max m right away; the tile max is reduced in the
+      // same pass (off the S -> P dependency chain) and checked once at the
+      // end. If it exceeds m + 8 (the lazy-rescale threshold below; rare after
+      // the first tiles) the tile is redone by the general path with a
+      // rescale to the new max (x[] still holds the raw scores).
+      if (i > 0 && dense && !special) {
+        const float2 sl2x2 = make_float2(sl2, sl2), nb2 = make_float2(bias - m, bias - m);
+        float2 sp2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const int cc = 32 * ch + 2 * c;
+#ifndef ISA_SPEC_SUMCHECK
+            mx[c & 7] = fmax3(mx[c & 7], x[cc], x[cc + 1]);
+#endif
+            const float2 tt = ffma2(make_float2(x[cc], x[cc + 1]), sl2x2, nb2);
+            float2 pp;
+            if (kEmuEvery > 0 && (c % kEmuEvery) == kEmuEvery - 1) {
+              pp = ex2_emu2(tt);
+            } else {
+              pp.x = ex2_approx(tt.x);
+              pp.y = ex2_approx(tt.y);
+            }
+            sp2[c & 3] = fadd2(sp2[c & 3], pp);
+            pk[c] = pack_p(pp.x, pp.y);
+          }
+          tmem_st16(t_p + 16 * ch, pk);
+        }
+#ifdef ISA_SPEC_SUMCHECK
+        // every p <= sum: sum <= 2^8 bounds the tile max by m + 8
+        const float2 s2c = fadd2(fadd2(sp2[0], sp2[1]), fadd2(sp2[2], sp2[3]));
+        const bool redo = !(s2c.x + s2c.y <= 256.f);
+#else
+        const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        const bool redo = (m == -INFINITY) || (fmaf(mt, sl2, bias) > m + 8.f);
+#endif
+        tmem_st_wait();
+        if (!__any_sync(0xffffffffu, redo)) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[s]);
+          if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 4);
+          const float2 s2 = fadd2(fadd2(sp2[0], sp2[1]), fadd2(sp2[2], sp2[3]));
+          l += s2.x + s2.y;
+          if ((threadIdx.x & 127) == 0) progress(2 + s, i + 1);
+          continue;
+        }
+        // rare: the general path below recomputes the max and P from x[]
+        force_rescale = true;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+      }
+#endif
       if (special) {  // rare: per-column weights, scaled in place
         const int j0 = t.cidx * 128;
 #pragma unroll
@@ -604,7 +677,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       bool need = false;
       if (i == 0) {
         m = m_new;
-      } else if (m_new > m + 8.f) {
+      } else if (m_new > m + (force_rescale ? 0.f : 8.f)) {
         o_scale = ex2_approx(m - m_new);  // m == -inf -> 0 (O and l are 0 then)
         need = true;
         m = m_new;
@@ -621,6 +694,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           tmem_st32(t_o + c * 32, orr);
         }
       }
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 2);
       const float mu = (m == -INFINITY) ? 0.f : m;
       float sm[4] = {0.f, 0.f, 0.f, 0.f};
       float2 sm2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -686,13 +760,14 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           tmem_st16(t_p + 16 * ch, pk);
         }
       }
-      const float2 s2 = fadd2(fadd2(sm2[0], sm2[1]), fadd2(sm2[2], sm2[3]));
-      const float sum = ((sm[0] + sm[1]) + (sm[2] + sm[3])) + (s2.x + s2.y);
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 3);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[s]);
-      l += sum;
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 4);
+      const float2 s2 = fadd2(fadd2(sm2[0], sm2[1]), fadd2(sm2[2], sm2[3]));
+      l += ((sm[0] + sm[1]) + (sm[2] + sm[3])) + (s2.x + s2.y);
       if ((threadIdx.x & 127) == 0) progress(2 + s, i + 1);
     }
     // -------------------------------------------------------------- epilogue

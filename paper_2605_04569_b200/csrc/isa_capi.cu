@@ -889,4 +889,12 @@ int isa_forward_host(const IsaShape* shape, const IsaKnobs* knobs, const void* q
   return ISA_OK;
 }
 
+#ifdef ISA_TRACE
+// Debug build only (not in the header): copy the timeline stamps to host.
+int isa_debug_trace_copy(void* host, size_t bytes) {
+  ISA_CUDA(cudaMemcpyFromSymbol(host, isa::g_isa_trace, bytes < sizeof(isa::g_isa_trace) ? bytes : sizeof(isa::g_isa_trace)));
+  return ISA_OK;
+}
+#endif
+
 }  // extern "C"

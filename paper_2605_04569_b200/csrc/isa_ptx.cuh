@@ -58,6 +58,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
       : "memory");
 }
 
+#ifndef ISA_WAIT_HINT_NS
+#define ISA_WAIT_HINT_NS 20000
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -66,6 +69,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       "selp.b32 %0, 1, 0, P1;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes (or the hint elapses) instead of spinning on the issue port
+// it shares with the softmax warps of the same SM sub-partition.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ISA_WAIT_HINT_NS)
       : "memory");
   return ok != 0;
 }
@@ -79,6 +97,22 @@ __device__ __forceinline__ uint64_t global_ns() {
 // Progress words written by each warp role (debug aid printed on a wait
 // timeout): [cta % 1024][role] with roles 0 = TMA, 1 = MMA, 2/3 = softmax 0/1.
 __device__ volatile int g_isa_progress[1024][4];
+
+// Timeline instrumentation (build with -DISA_TRACE only): SM-clock stamps of
+// one CTA's softmax / MMA events, read back by isa_debug_trace_copy.
+#ifdef ISA_TRACE
+constexpr int kTraceSteps = 96;
+__device__ long long g_isa_trace[kTraceSteps][2][8];
+__device__ __forceinline__ bool trace_cta() { return blockIdx.x == ISA_TRACE && blockIdx.y == 0; }
+#define ISA_TSTAMP(step, stage, slot)                                               \
+  do {                                                                              \
+    if (trace_cta() && (step) < kTraceSteps) g_isa_trace[(step)][(stage)][(slot)] = clock64(); \
+  } while (0)
+#else
+#define ISA_TSTAMP(step, stage, slot) \
+  do {                                \
+  } while (0)
+#endif
 
 __device__ __forceinline__ void progress(int role, int v) {
   g_isa_progress[(blockIdx.y * gridDim.x + blockIdx.x) & 1023][role] = v;
@@ -94,8 +128,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = global_ns();
   uint32_t n = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if ((++n & 1023u) == 0 && global_ns() - t0 > 3000000000ull) {
+  while (!mbar_try_wait_sleep(bar, parity)) {
+    if ((++n & 63u) == 0 && global_ns() - t0 > 3000000000ull) {
 #ifdef ISA_DEBUG_WAIT
       const int c = (blockIdx.y * gridDim.x + blockIdx.x) & 1023;
       printf("isa: wait timeout cta(%d,%d) tid %d bar@%u parity %u prog tma=%d mma=%d s0=%d s1=%d\n", blockIdx.x,
@@ -159,6 +193,15 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
   d |= static_cast<uint64_t>(1) << 46;  // version (sm_100)
   d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
   return d;
+}
+
+// Same descriptor without masking: shared-window addresses are < 2^18, so
+// (addr >> 4) fits the 14-bit field and descriptors of addr + off (16-byte
+// multiples) are plain 64-bit adds of (off >> 4) to the base descriptor.
+__device__ __forceinline__ uint64_t sdesc_sw128_base(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  return (static_cast<uint64_t>(2) << 61) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(sbo_bytes >> 4) << 32) | (static_cast<uint64_t>(lbo_bytes >> 4) << 16) |
+         static_cast<uint64_t>(saddr >> 4);
 }
 
 // Instruction descriptor, kind::f16 with bf16 inputs and f32 accumulate.
@@ -255,6 +298,18 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
+}
+
+// P packing for the MMA: round-to-nearest (F2FP) or, with -DISA_P_TRUNC,
+// truncation of the fp32 bits (one PRMT per pair).
+__device__ __forceinline__ uint32_t pack_p(float lo, float hi) {
+#ifdef ISA_P_TRUNC
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(lo)), "r"(__float_as_uint(hi)));
+  return r;
+#else
+  return pack_bf16x2(lo, hi);
+#endif
 }
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {

@@ -145,6 +145,25 @@ def test_dense_attention_vs_torch_fp32(D, S):
     _close(out, ref.cpu().numpy())
 
 
+@pytest.mark.parametrize("growth", [0.5, 4.0, 40.0])
+def test_dense_attention_rising_scores_vs_torch_fp32(growth):
+    """Key norms grow along the sequence, so the running row max keeps jumping:
+    exercises the speculative softmax path's fallback (tile max > m + 8 ->
+    recompute with a forced rescale) on every few tiles, incl. jumps far
+    beyond the exp2 range of a stale max (growth 40)."""
+    P = _api()
+    torch.manual_seed(7)
+    S, D = 2048, 128
+    q, k, v = (torch.randn(1, 2, S, D, device="cuda") for _ in range(3))
+    ramp = torch.linspace(0.05, 1.0, S, device="cuda").pow(2) * growth
+    k = k * ramp[None, None, :, None]
+    q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
+    out = P.dense_attention(q, k, v)
+    ref = torch.softmax(q.float() @ k.float().transpose(-1, -2) / math.sqrt(D), dim=-1) @ v.float()
+    assert torch.isfinite(out.float()).all()
+    _close(out, ref.cpu().numpy())
+
+
 # ------------------------------------------------------------------ routing vs reference golden vectors
 @pytest.mark.parametrize("name", case_names())
 def test_routing_bit_exact_vs_reference(name):
