@@ -62,6 +62,9 @@ struct AttnParams {
 #ifndef ISA_TRACE_Q
 #define ISA_TRACE_Q 0  // softmax warp quadrant stamped by ISA_TRACE builds
 #endif
+#ifndef ISA_TRACE_MODE
+#define ISA_TRACE_MODE 0  // 2: stamp the Taylor branch instead of dense/exact
+#endif
 constexpr int kThreads = 384;
 constexpr int kKvStages = 5;  // K/V ring slots (D=128: 64 KB Q + 5 x 32 KB = 224 KB)
 constexpr int kSoftmaxRegs = 208;
@@ -111,52 +114,50 @@ __device__ __forceinline__ int num_kv_tiles(const AttnParams& p, int bh, int ite
   return (p.t_new + 1) >> 1;
 }
 
-// K/V tile i of the stream that Q tile `s` consumes. DENSE/EXACT: one stream
-// shared by both Q tiles (K_new blocks 2i, 2i+1). TAYLOR: each Q tile (pair of
-// flat query blocks) has its own exact-union stream, padded to a common
-// length with empty tiles, followed by the shared centroid tiles.
+// Source rows of K/V tile i of the stream that Q tile `s` consumes, for the
+// TMA producer. DENSE/EXACT: one stream shared by both Q tiles (K_new blocks
+// 2i, 2i+1, through the block table). TAYLOR: each Q tile (pair of flat query
+// blocks) has its own exact-union stream of planned entries (token rows
+// resolved by taylor_plan_kernel), padded to a common length with empty tiles,
+// followed by the shared centroid tiles. The raw table words are loaded one
+// tile ahead of use (tile_raw), so no dependent global load sits between two
+// TMA issues.
+struct TileSrc {
+  int tok0, tok1;  // first token row per 64-row half (or centroid row); a missing half repeats tok0
+  int centroid;
+};
+
 template <int MODE>
-__device__ __forceinline__ TileInfo kv_tile(const AttnParams& p, int bh, int item, int i, int s) {
-  TileInfo t;
-  t.centroid = 0;
-  t.cidx = 0;
-  t.bits0 = t.bits1 = 0xF;
-  int kn0, kn1;
+__device__ __forceinline__ int4 tile_raw(const AttnParams& p, int bh, int item, int i, int s, int ne) {
   if (MODE == MODE_TAYLOR) {
-    const int ne = p.n_tiles[bh * p.n_items + item];
+    if (i < ne) return __ldg(p.tiles + (((long long)bh * p.n_items + item) * 2 + s) * p.max_tiles + i);
+    return make_int4(0, 0, 0, 0);
+  }
+  if (MODE == MODE_EXACT) {
+    const int* tab = p.kv_blk + (long long)bh * p.t_new;
+    const int kn0 = 2 * i, kn1 = 2 * i + 1;
+    return make_int4(kn0 < p.t_new ? __ldg(tab + kn0) : 0, kn1 < p.t_new ? __ldg(tab + kn1) : -1, 0, 0);
+  }
+  return make_int4(2 * i, 2 * i + 1 < p.t_new ? 2 * i + 1 : -1, 0, 0);
+}
+
+template <int MODE>
+__device__ __forceinline__ TileSrc tile_src(const AttnParams& p, int4 raw, int i, int ne) {
+  TileSrc t;
+  t.centroid = 0;
+  if (MODE == MODE_TAYLOR) {
     if (i >= ne) {
       t.centroid = 1;
-      t.cidx = i - ne;
-      t.tok0 = t.cidx * 128;
+      t.tok0 = (i - ne) * 128;
       t.tok1 = t.tok0 + 64;
-      t.valid0 = t.valid1 = 64;
       return t;
     }
-    const int4 e = p.tiles[(((long long)bh * p.n_items + item) * 2 + s) * p.max_tiles + i];
-    kn0 = e.x;
-    kn1 = e.y;
-    t.bits0 = e.z;
-    t.bits1 = e.w;
-  } else {
-    kn0 = 2 * i;
-    kn1 = 2 * i + 1 < p.t_new ? 2 * i + 1 : -1;
+    t.tok0 = raw.x >= 0 ? raw.x : 0;  // empty padding tile: load rows 0.., fully masked
+    t.tok1 = raw.y >= 0 ? raw.y : t.tok0;
+    return t;
   }
-  int u0 = kn0, u1 = kn1;
-  if (MODE != MODE_DENSE) {
-    const int* tab = p.kv_blk + (long long)bh * p.t_new;
-    u0 = kn0 >= 0 ? tab[kn0] : 0;  // empty padding tile: load block 0, fully masked
-    u1 = kn1 >= 0 ? tab[kn1] : -1;
-  }
-  t.tok0 = blk_tok0(p, u0);
-  t.valid0 = kn0 >= 0 ? blk_valid(p, u0) : 0;
-  if (u1 >= 0) {
-    t.tok1 = blk_tok0(p, u1);
-    t.valid1 = blk_valid(p, u1);
-  } else {  // missing half: reload block 0 (finite data), fully masked
-    t.tok1 = t.tok0;
-    t.valid1 = 0;
-    t.bits1 = 0;
-  }
+  t.tok0 = blk_tok0(p, raw.x);
+  t.tok1 = raw.y >= 0 ? blk_tok0(p, raw.y) : t.tok0;  // missing half: reload (finite), masked
   return t;
 }
 
@@ -274,10 +275,12 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           }
         }
       }
-      const int n_entries = (MODE == MODE_TAYLOR ? 4 : 2) * n_kv;
-      for (int c = 0; c < n_entries; ++c) {
-        const Entry en = ring_entry<MODE>(c, n_kv);
-        const TileInfo t = kv_tile<MODE>(p, bh, item, en.tile, en.stage);
+      // Entries in ring order (see ring_entry): per step i the V tiles of
+      // step i-1 and the K tiles of step i; tile descriptors one step ahead.
+      const int ne = (MODE == MODE_TAYLOR) ? p.n_tiles[bh * p.n_items + item] : 0;
+      constexpr int kStages = (MODE == MODE_TAYLOR) ? 2 : 1;
+      int c = 0;
+      auto push = [&](const TileSrc& t, int is_v) {
         const int slot = c % kKvStages;
         const int use = c / kKvStages;
         if (use > 0) mbar_wait(&kv_empty[slot], (use - 1) & 1);
@@ -288,11 +291,11 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           const CUtensorMap* tm;
           int c2, c3;
           if (t.centroid) {
-            tm = en.is_v ? &tm_vc : &tm_kc;
+            tm = is_v ? &tm_vc : &tm_kc;
             c2 = bh;
             c3 = 0;
           } else {
-            tm = en.is_v ? &tm_v : &tm_k;
+            tm = is_v ? &tm_v : &tm_k;
             c2 = hh;
             c3 = bb;
           }
@@ -302,6 +305,37 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
               tma_load_4d(dst + pl * 16384 + half * 8192, tm, &kv_full[slot], pl * 64, tok, c2, c3, pol_kv);
           }
           progress(0, c + 1);
+        }
+        ++c;
+      };
+      int4 raw[kStages];
+#pragma unroll
+      for (int st = 0; st < kStages; ++st) raw[st] = tile_raw<MODE>(p, bh, item, 0, st, ne);
+      TileSrc cur[kStages], prv[kStages];
+#pragma unroll
+      for (int st = 0; st < kStages; ++st) cur[st] = prv[st] = TileSrc{0, 0, 0};
+      for (int i = 0; i <= n_kv; ++i) {
+        if (i < n_kv) {
+#pragma unroll
+          for (int st = 0; st < kStages; ++st) {
+            prv[st] = cur[st];
+#ifdef ISA_PRODUCER_NOPREFETCH
+            raw[st] = tile_raw<MODE>(p, bh, item, i, st, ne);
+#endif
+            cur[st] = tile_src<MODE>(p, raw[st], i, ne);
+#ifndef ISA_PRODUCER_NOPREFETCH
+            if (i + 1 < n_kv) raw[st] = tile_raw<MODE>(p, bh, item, i + 1, st, ne);
+#endif
+          }
+        }
+#pragma unroll
+        for (int st = 0; st < kStages; ++st) {
+          if (i == n_kv) {
+            push(cur[st], 1);  // last V
+          } else {
+            if (i > 0) push(prv[st], 1);
+            push(cur[st], 0);
+          }
         }
       }
     } else if (warp == 8) {
@@ -363,7 +397,9 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           for (int s = 0; s < 2; ++s) {
             const int ev = base + 2 * s, ek = ev + 1;
             mbar_wait(&p_full[s], (i - 1) & 1);
+            if (leader && ISA_TRACE_MODE == 2) ISA_TSTAMP(i, s, 6);
             wait_entry(ev);
+            if (leader && ISA_TRACE_MODE == 2) ISA_TSTAMP(i, s, 5);
             __syncwarp();
             tc_fence_after();
             issue_pv(s, ev % kKvStages, i > 1);
@@ -373,6 +409,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
             tc_fence_after();
             issue_qk(s, ek % kKvStages);
             commit(&s_full[s]);
+            if (leader && ISA_TRACE_MODE == 2) ISA_TSTAMP(i, s, 7);
             release(ek);
           }
           if (leader) progress(1, 1000 * i + 1);
@@ -400,17 +437,17 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           const int ev = 2 * i - 1, ek = 2 * i;
           wait_entry(ev);
           wait_entry(ek);
-          if (leader) ISA_TSTAMP(i, 0, 5);
+          if (leader && ISA_TRACE_MODE != 2) ISA_TSTAMP(i, 0, 5);
           if (leader) progress(1, 1000 * i + 1);
           for (int s = 0; s < 2; ++s) {
             mbar_wait(&p_full[s], (i - 1) & 1);
-            if (leader) ISA_TSTAMP(i, s, 6);
+            if (leader && ISA_TRACE_MODE != 2) ISA_TSTAMP(i, s, 6);
             __syncwarp();
             tc_fence_after();
             issue_pv(s, ev % kKvStages, i > 1);
             issue_qk(s, ek % kKvStages);
             commit(&s_full[s]);
-            if (leader) ISA_TSTAMP(i, s, 7);
+            if (leader && ISA_TRACE_MODE != 2) ISA_TSTAMP(i, s, 7);
           }
           release(ev);
           release(ek);
@@ -482,10 +519,10 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         if (i < n_exact) {
           const int4 e = e_next;
           if (i + 1 < n_exact) e_next = tlist[i + 1];
-          t.valid0 = kn_valid(e.x);
-          t.valid1 = kn_valid(e.y);
-          t.bits0 = e.z;
-          t.bits1 = e.w;
+          t.valid0 = e.z >> 8;  // planned: visibility bits | valid rows << 8
+          t.valid1 = e.w >> 8;
+          t.bits0 = e.z & 0xF;
+          t.bits1 = e.w & 0xF;
         } else {
           t.centroid = 1;
           t.cidx = i - n_exact;
@@ -498,7 +535,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         t.bits0 = t.bits1 = 0xF;
       }
       mbar_wait(&s_full[s], i & 1);
-      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 0);
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 0);
       __syncwarp();  // reconverge before .sync.aligned tcgen05 ops
       tc_fence_after();
 #ifdef ISA_EXP_NOSOFTMAX
@@ -513,7 +550,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[s]);
-        if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 4);
+        if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 4);
         l += 1.f;
         continue;
       }
@@ -531,7 +568,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       }
       tmem_ld_wait();
 #endif
-      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 1);
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 1);
 #ifdef ISA_EXP_LOADONLY
       {
         float mm = -INFINITY;
@@ -546,7 +583,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[s]);
-        if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 4);
+        if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 4);
         l += 1.f;
         continue;
       }
@@ -594,11 +631,42 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       // end. If it exceeds m + 8 (the lazy-rescale threshold below; rare after
       // the first tiles) the tile is redone by the general path with a
       // rescale to the new max (x[] still holds the raw scores).
-      if (i > 0 && dense && !special) {
+      // Each 64-column half must be wholly kept or wholly excluded (always
+      // true for K6 tiles and for the Taylor union tiles of full blocks: the
+      // visibility bits are per (query block, key block)); excluded halves
+      // get P = 0 with no exponentials.
+      const bool half0 = (mw[0] | mw[1]) == 0u, half1 = (mw[2] | mw[3]) == 0u;
+      // (K6/K8 take only fully dense tiles here: their code has a single,
+      // straight-line schedule; partial tiles use the general path.)
+      const bool halfwise =
+          MODE == MODE_TAYLOR ? ((half0 || skip0) && (half1 || skip1) && (half0 || half1)) : dense;
+      if (MODE == MODE_TAYLOR && !t.centroid && skip0 && skip1) {
+        // Union tile none of whose blocks this row block lists: P = 0, no
+        // state change (warp-uniform).
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) pk[c] = 0u;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) tmem_st16(t_p + 16 * ch, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[s]);
+        continue;
+      }
+      // Taylor centroid tiles (taylor.py:153-159) also take the speculative
+      // path: excluded centroids (the row block's own exact members, columns
+      // past t_new) are set to -inf first, so they contribute p = 0.
+      const bool cmask = MODE == MODE_TAYLOR && t.centroid;
+      if (i > 0 && (halfwise || cmask) && !special) {
+        if (cmask) {
+#pragma unroll
+          for (int cc = 0; cc < 128; ++cc)
+            if ((mw[cc >> 5] >> (cc & 31)) & 1u) x[cc] = -INFINITY;
+        }
         const float2 sl2x2 = make_float2(sl2, sl2), nb2 = make_float2(bias - m, bias - m);
         float2 sp2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
+        auto chunk = [&](const int ch) {
           uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
@@ -618,6 +686,22 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
             pk[c] = pack_p(pp.x, pp.y);
           }
           tmem_st16(t_p + 16 * ch, pk);
+        };
+        if (MODE != MODE_TAYLOR || dense || cmask) {  // every K6/K8 tile: one straight-line schedule
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) chunk(ch);
+        } else {      // Taylor union tiles: per-half (warp-uniform) choice
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            if (ch < 2 ? half0 : half1) {
+              chunk(ch);
+            } else {
+              uint32_t pk[16];
+#pragma unroll
+              for (int c = 0; c < 16; ++c) pk[c] = 0u;
+              tmem_st16(t_p + 16 * ch, pk);
+            }
+          }
         }
 #ifdef ISA_SPEC_SUMCHECK
         // every p <= sum: sum <= 2^8 bounds the tile max by m + 8
@@ -632,7 +716,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[s]);
-          if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 4);
+          if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 4);
           const float2 s2 = fadd2(fadd2(sp2[0], sp2[1]), fadd2(sp2[2], sp2[3]));
           l += s2.x + s2.y;
           if ((threadIdx.x & 127) == 0) progress(2 + s, i + 1);
@@ -694,7 +778,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           tmem_st32(t_o + c * 32, orr);
         }
       }
-      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 2);
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 2);
       const float mu = (m == -INFINITY) ? 0.f : m;
       float sm[4] = {0.f, 0.f, 0.f, 0.f};
       float2 sm2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -760,12 +844,12 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           tmem_st16(t_p + 16 * ch, pk);
         }
       }
-      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 3);
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 3);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[s]);
-      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && MODE != MODE_TAYLOR) ISA_TSTAMP(i, s, 4);
+      if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 4);
       const float2 s2 = fadd2(fadd2(sm2[0], sm2[1]), fadd2(sm2[2], sm2[3]));
       l += ((sm[0] + sm[1]) + (sm[2] + sm[3])) + (s2.x + s2.y);
       if ((threadIdx.x & 127) == 0) progress(2 + s, i + 1);

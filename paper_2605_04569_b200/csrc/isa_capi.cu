@@ -533,6 +533,7 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   }
   if (d.n_flat) {
     isa::taylor_plan_kernel<<<dim3(d.items_f, d.BH), 64, 0, st>>>(w.bits, d.n_flat, d.W, d.items_f, d.max_tiles,
+                                                                   w.kv_blk, d.t_new, d.t_src, d.l_src, d.l_ctx,
                                                                    w.tiles, w.n_tiles);
     ISA_LAUNCHED("taylor_plan_kernel");
   }

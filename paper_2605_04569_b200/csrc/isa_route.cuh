@@ -596,9 +596,28 @@ __global__ void centroid_kernel(const float* __restrict__ kc, const float* __res
 // tiles (kn = -1) so both stages share one step count. grid (n_items, BH),
 // block 64 (one warp per stage).
 // ----------------------------------------------------------------------------
+// Entries are resolved for the attention kernel's TMA producer: {tok0, tok1,
+// meta0, meta1} with tok = first source token row of the K_new block (-1 =
+// none) and meta = visibility bits (bits 0-3, one per query block of the CTA)
+// | valid key rows << 8, so the producer issues its loads with no dependent
+// table lookups.
+__device__ __forceinline__ void plan_entry(int* e, int half, int j, int vis, const int* kv_tab, int t_src, int l_src,
+                                           int l_ctx) {
+  int tok = -1, valid = 0;
+  if (j >= 0) {
+    const int u = kv_tab[j];
+    tok = u < t_src ? u * 64 : l_src + (u - t_src) * 64;
+    const int r = u < t_src ? l_src - u * 64 : l_ctx - (u - t_src) * 64;
+    valid = r < 64 ? r : 64;
+  }
+  e[half] = tok;
+  e[2 + half] = vis | (valid << 8);
+}
+
 __global__ void __launch_bounds__(64) taylor_plan_kernel(const uint32_t* __restrict__ member_bits, int n_flat,
-                                                         int W, int n_items, int max_tiles, int4* __restrict__ tiles,
-                                                         int* __restrict__ n_tiles) {
+                                                         int W, int n_items, int max_tiles, const int* __restrict__ kv_blk,
+                                                         int t_new, int t_src, int l_src, int l_ctx,
+                                                         int4* __restrict__ tiles, int* __restrict__ n_tiles) {
   __shared__ int counts[2];
   const int item = blockIdx.x, bh = blockIdx.y;
   const int s = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -608,6 +627,7 @@ __global__ void __launch_bounds__(64) taylor_plan_kernel(const uint32_t* __restr
     mb[h] = f < n_flat ? member_bits + ((long long)bh * n_flat + f) * W : nullptr;
   }
   int4* out = tiles + (((long long)bh * n_items + item) * 2 + s) * max_tiles;
+  const int* kv_tab = kv_blk + (long long)bh * t_new;
   int base = 0;
   for (int w0 = 0; w0 < W; w0 += 32) {
     const int w = w0 + lane;
@@ -631,14 +651,7 @@ __global__ void __launch_bounds__(64) taylor_plan_kernel(const uint32_t* __restr
       wb &= wb - 1;
       const int j = w * 32 + bpos;
       const int vis = (int)(((wq[0] >> bpos) & 1u) | (((wq[1] >> bpos) & 1u) << 1)) << (2 * s);
-      int* e = reinterpret_cast<int*>(out + (p >> 1));
-      if (p & 1) {
-        e[1] = j;
-        e[3] = vis;
-      } else {
-        e[0] = j;
-        e[2] = vis;
-      }
+      plan_entry(reinterpret_cast<int*>(out + (p >> 1)), p & 1, j, vis, kv_tab, t_src, l_src, l_ctx);
       ++p;
     }
     base += __shfl_sync(0xffffffffu, incl, 31);
@@ -648,11 +661,7 @@ __global__ void __launch_bounds__(64) taylor_plan_kernel(const uint32_t* __restr
   const int nt = max((counts[0] + 1) >> 1, (counts[1] + 1) >> 1);
   // close this stage's stream: odd tail half, then empty padding tiles
   const int mine = counts[s];
-  if (lane == 0 && (mine & 1)) {
-    int* e = reinterpret_cast<int*>(out + (mine >> 1));
-    e[1] = -1;
-    e[3] = 0;
-  }
+  if (lane == 0 && (mine & 1)) plan_entry(reinterpret_cast<int*>(out + (mine >> 1)), 1, -1, 0, kv_tab, t_src, l_src, l_ctx);
   for (int t = ((mine + 1) >> 1) + lane; t < nt; t += 32) out[t] = make_int4(-1, -1, 0, 0);
   if (threadIdx.x == 0) n_tiles[bh * n_items + item] = nt;
 }

@@ -47,22 +47,29 @@ def run(args):
 
     H, S, D = args.heads, args.seq, 128
     q, k, v = (torch.randn(1, H, S, D, device="cuda", dtype=torch.bfloat16) for _ in range(3))
-    for _ in range(3):
-        P.dense_attention(q, k, v)
+    if args.isa:  # ISA forward, branches launched separately (trace CTA of the branch built for)
+        prep = P.prepare(q, k, v, P.IclLayout(S // 2, S // 2), P.IsaConfig(), separate_branches=True)
+        for _ in range(3):
+            prep()
+    else:
+        for _ in range(3):
+            P.dense_attention(q, k, v)
     torch.cuda.synchronize()
     buf = np.zeros((96, 2, 8), dtype=np.int64)
     N.check(lib.isa_debug_trace_copy(buf.ctypes.data, buf.nbytes))
     t = buf - buf[1, 0, 0]
-    print("step st |  S_rdy   ld   exps st_wait arrv | mma_see issue | S_rdy(i+1)-issue | step_dt   (spec path stamps)")
+    print("step st |  S_rdy   ld  S->P(arrive) | mma_see issue | S_rdy(i+1)-issue | step_dt")
     for i in range(args.first, min(args.first + args.n, 95)):
         for s in range(2):
             a = t[i, s]
             nxt = t[i + 1, s, 0] - t[i + 1, s, 7] if i + 1 < 96 else 0
             dt = t[i + 1, s, 0] - a[0]
-            print(f"{i:4d} {s}  | {a[0]:7d} {a[1]-a[0]:4d} {a[2]-a[1]:5d} {a[3]-a[2]:5d} {a[4]-a[3]:5d} |"
+            print(f"{i:4d} {s}  | {a[0]:7d} {a[1]-a[0]:4d} {a[4]-a[0]:6d} |"
                   f" {t[i+1, s, 6]-a[4]:6d} {t[i+1, s, 7]-t[i+1, s, 6]:5d} | {nxt:6d} | {dt:6d}")
     steps = t[args.first + args.n, 0, 0] - t[args.first, 0, 0]
     print(f"avg clk/step over {args.n} steps: {steps / args.n:.0f} (ideal MMA 2048 at D=128)")
+    if args.isa:
+        return
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(5):
@@ -81,6 +88,7 @@ if __name__ == "__main__":
     ap.add_argument("--heads", type=int, default=8)
     ap.add_argument("--seq", type=int, default=16384)
     ap.add_argument("--first", type=int, default=20)
+    ap.add_argument("--isa", action="store_true", help="trace an isa_forward (separate branches) instead of dense")
     ap.add_argument("--n", type=int, default=24)
     a = ap.parse_args()
     if a.build:
