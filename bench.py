@@ -317,7 +317,7 @@ def _call_with_events(prep, ev_struct, flags=0):
 
     inp = prep.inp
     kn = N.IsaKnobs(inp.knobs.scale, inp.knobs.k_ctx, inp.knobs.n_flat, inp.knobs.k_mask, inp.knobs.softmax_first,
-                    flags)
+                    flags, inp.knobs.gamma, inp.knobs.residual_softmax)
     N.check(N.load().isa_forward(ctypes.byref(inp.shape), ctypes.byref(kn), _ptr(inp.q), _ptr(inp.k),
                                  _ptr(inp.v), _ptr(prep.out), _ptr(prep.ws), prep.nbytes, None, None, _ptr(prep.err),
                                  ctypes.byref(ev_struct), torch.cuda.current_stream().cuda_stream))

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define ISA_ABI_VERSION 1
+#define ISA_ABI_VERSION 2
 
 typedef enum IsaStatus {
   ISA_OK = 0,
@@ -70,6 +70,9 @@ typedef struct IsaKnobs {
   int32_t k_mask;
   int32_t softmax_first; /* coarse.py:194 */
   int32_t flags;         /* ISA_FLAG_* bits, 0 = defaults */
+  double gamma;          /* coarse residual weight, 0 = off (pipeline.py:354-356) */
+  int32_t residual_softmax; /* residual weights: 1 softmax(S_coarse), 0 raw Qc.Kc (pipeline.py:261-267) */
+  int32_t reserved;      /* 0 */
 } IsaKnobs;
 
 /* IsaKnobs.flags: launch the exact (sharp) and Taylor (flat) attention

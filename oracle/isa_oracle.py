@@ -218,8 +218,10 @@ class OracleAssembly:
     """Stages 1-3 of _Assembly (pipeline.py:133-228), storage dtype fp32."""
 
     def __init__(self, q, k, v, l_src, l_ctx, *, alpha_s=0.125, alpha_ns=0.0625, alpha_f=0.5,
-                 block_size=64, scale=None, softmax_first=True, routing: Optional[OracleRouting] = None):
+                 block_size=64, scale=None, softmax_first=True, gamma=0.0, residual_softmax=True,
+                 routing: Optional[OracleRouting] = None):
         b = block_size
+        self.gamma, self.residual_softmax = gamma, residual_softmax
         self.q, self.k, self.v = (np.asarray(x, dtype=np.float32) for x in (q, k, v))  # pipeline.py:150-151
         B, H, S, D = self.q.shape
         self.b, self.l_src, self.l_ctx = b, l_src, l_ctx
@@ -281,8 +283,17 @@ class OracleAssembly:
             ctx_scores = self.s_coarse[:, :, : self.t_src, self.t_src:].mean(axis=2)
         return OracleRouting(self.sel, self.sharp, self.flat, self.sharpness, self.mask, ctx_scores, self.s_flat)
 
+    def coarse_residual(self) -> np.ndarray:
+        """O_coarse, one row per query block, float64 (pipeline.py:261-267)."""
+        if self.residual_softmax:
+            p = softmax_rows(self.s_coarse)
+        else:
+            p = self.s_coarse / self.scale  # raw, unscaled scores
+        return p @ self.vc.astype(np.float64)
+
     def forward(self, block_fraction: float = 1.0) -> np.ndarray:
-        """Stages 4-5 of _forward (pipeline.py:331-358), gamma = 0.
+        """Stages 4-5 of _forward (pipeline.py:331-358), incl. the gamma
+        coarse residual (pipeline.py:354-356).
 
         block_fraction < 1 computes only the first ceil(f*n) sharp and flat
         query blocks of each head (bench.py's bounded CPU sample; rows are
@@ -310,7 +321,11 @@ class OracleAssembly:
                                     self.vc_new[bi, hi].astype(np.float64), self.mask[bi, hi, :nf],
                                     self.valid_new[bi, hi], self.scale, b)
                     ob[bi, hi, sel] = o.reshape(-1, b, D)
-        out = out_pad.astype(np.float32)[:, :, self.orig_rows]  # pipeline.py:357 (storage dtype fp32)
+        out_pad = out_pad.astype(np.float32)  # scatter into the storage-dtype buffer (pipeline.py:350-353)
+        if self.gamma:  # pipeline.py:354-356
+            residual = np.repeat(self.coarse_residual(), b, axis=2)
+            out_pad = (out_pad.astype(np.float64) + self.gamma * residual).astype(np.float32)
+        out = out_pad[:, :, self.orig_rows]  # pipeline.py:357 (storage dtype fp32)
         return out
 
 

@@ -16,7 +16,7 @@ from .errors import ISA_OK, STATUS_TO_ERROR, NativeError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libisa_b200.so")
 
-ISA_ABI_VERSION = 1
+ISA_ABI_VERSION = 2
 ISA_DTYPE_BF16 = 0
 ISA_DTYPE_F32 = 1
 
@@ -61,6 +61,9 @@ class IsaKnobs(ctypes.Structure):
         ("k_mask", ctypes.c_int32),
         ("softmax_first", ctypes.c_int32),
         ("flags", ctypes.c_int32),
+        ("gamma", ctypes.c_double),
+        ("residual_softmax", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
     ]
 
 

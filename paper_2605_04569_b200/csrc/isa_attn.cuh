@@ -57,6 +57,10 @@ struct AttnParams {
   int out_fp32;
   long long o_sb, o_sh, o_ss;
   int* err_flag;
+  // gamma coarse residual (pipeline.py:354-356): out += gamma * resid[bh][u]
+  const float* resid;  // [BH][T][D] or null
+  float gamma;
+  int T;
 };
 
 #ifndef ISA_TRACE_Q
@@ -866,12 +870,18 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
     const int hh = bh % p.H, bb = bh / p.H;
     const long long obase =
         bb * p.o_sb + hh * p.o_sh + (long long)(write ? blk_tok0(p, u) + rr : 0) * p.o_ss;
+    const float* res_row = (p.resid && write) ? p.resid + ((long long)bh * p.T + u) * D : nullptr;
 #pragma unroll 1
     for (int c = 0; c < D / 32; ++c) {
       uint32_t orr[32];
       __syncwarp();
       tmem_ld32(t_o + c * 32, orr);
       tmem_ld_wait();
+      if (res_row) {  // O/l + gamma * O_coarse, folded so the stores below stay unchanged
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          orr[j] = __float_as_uint(__uint_as_float(orr[j]) + p.gamma * __ldg(res_row + c * 32 + j) * l);
+      }
       if (write) {
         if (p.out_fp32) {
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + obase + c * 32);

@@ -113,6 +113,8 @@ struct Dims {
   int k_ctx, t_new, n_flat, n_sharp, k;
   int tn_pad, W, items_s, items_f, max_tiles;
   double scale;
+  double gamma;       // coarse residual weight (0 = off)
+  int resid_softmax;  // residual weights softmax(S_coarse) (1) or raw Qc.Kc (0)
 };
 
 int derive(const IsaShape* sh, const IsaKnobs* kn, Dims* d) {
@@ -154,6 +156,9 @@ int derive(const IsaShape* sh, const IsaKnobs* kn, Dims* d) {
   d->max_tiles = (u + 1) / 2;
   if (d->max_tiles < 1) d->max_tiles = 1;
   d->scale = kn->scale;
+  if (!(kn->gamma >= 0.0)) return fail(ISA_ERR_CONFIG, "gamma must be >= 0, got %g", kn->gamma);
+  d->gamma = kn->gamma;
+  d->resid_softmax = kn->residual_softmax != 0;
   return ISA_OK;
 }
 
@@ -177,6 +182,7 @@ struct Workspace {
   int* ctx_short;     // [BH]
   int4* tiles;        // [BH][items_f][max_tiles]
   int* n_tiles;       // [BH][items_f]
+  float* resid;       // [BH][T][D] coarse residual rows (gamma > 0 only)
   size_t bytes;
 };
 
@@ -210,6 +216,7 @@ Workspace carve(const Dims& d, int dtype, uint8_t* base) {
   w.ctx_short = reinterpret_cast<int*>(take(4ull * BH));
   w.tiles = reinterpret_cast<int4*>(take(16ull * BH * d.items_f * 2 * d.max_tiles));
   w.n_tiles = reinterpret_cast<int*>(take(4ull * BH * d.items_f));
+  w.resid = d.gamma > 0.0 ? reinterpret_cast<float*>(take(4ull * BH * d.T * d.D)) : nullptr;
   w.bytes = off;
   return w;
 }
@@ -301,7 +308,7 @@ int launch_attention_d(int D, const CUtensorMap& tq, const CUtensorMap& tk, cons
                        const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& p, int items, int BH,
                        cudaStream_t st) {
   if constexpr (MODE != isa::MODE_TAYLOR) {
-    if (pipe_mode() == 2) {
+    if (pipe_mode() == 2 && !p.resid) {  // the p2 epilogue has no gamma residual
       if (D == 128) return launch_attention_p2<128, MODE>(tq, tk, tv, p, items, BH, st);
       return launch_attention_p2<64, MODE>(tq, tk, tv, p, items, BH, st);
     }
@@ -459,6 +466,14 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
     isa::ctx_score_kernel<<<dim3((d.t_ctx + 7) / 8, d.BH), 256, 0, st>>>(w.qsum, kc, d.T, d.t_src, d.t_ctx, d.D,
                                                                          d.scale, w.ctx);
     ISA_LAUNCHED("ctx_score_kernel");
+  }
+  if (d.gamma > 0.0) {  // coarse residual rows (pipeline.py:261-267), consumed by the attention epilogues
+    dim3 g((d.T + 15) / 16, d.BH);
+    if (d.D == 128)
+      isa::coarse_residual_kernel<128><<<g, 128, 0, st>>>(qc, kc, vc, d.T, (float)d.scale, d.resid_softmax, w.resid);
+    else
+      isa::coarse_residual_kernel<64><<<g, 128, 0, st>>>(qc, kc, vc, d.T, (float)d.scale, d.resid_softmax, w.resid);
+    ISA_LAUNCHED("coarse_residual_kernel");
   }
   record(ev, 1, st);
   // ---- stage 2: select (context top-k, K_new block table, fp64 scores vs K_new, centroids)
@@ -670,6 +685,9 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
   p.o_sb = (long long)d.H * d.S * d.D;
   p.o_ss = d.D;
   p.err_flag = err_word;
+  p.resid = w.resid;  // null unless gamma > 0
+  p.gamma = static_cast<float>(d.gamma);
+  p.T = d.T;
   isa::AttnParams ps = p;
   ps.n_qblk = d.n_sharp;
   ps.qlist = w.sharp;

@@ -666,6 +666,84 @@ __global__ void __launch_bounds__(64) taylor_plan_kernel(const uint32_t* __restr
   if (threadIdx.x == 0) n_tiles[bh * n_items + item] = nt;
 }
 
+// ----------------------------------------------------------------------------
+// Coarse residual O_coarse (pipeline.py:261-267): per query block u,
+//   softmax variant  O_u = sum_j softmax_j(scale * qc_u . kc_j) vc_j
+//   raw variant      O_u = sum_j (qc_u . kc_j) vc_j
+// over all T key blocks, fp32 with an online softmax. Added to every row of
+// block u as out += gamma * O_u in the attention epilogues
+// (pipeline.py:354-356). grid (ceil(T/16), BH), 128 threads: each warp owns 4
+// query blocks, each lane D/32 columns; key blocks staged 32 at a time.
+// ----------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(128) coarse_residual_kernel(const float* __restrict__ qc,
+                                                             const float* __restrict__ kc,
+                                                             const float* __restrict__ vc, int T, float scale,
+                                                             int use_softmax, float* __restrict__ out) {
+  constexpr int kC = D / 32;  // columns per lane
+  constexpr int kJ = 32;      // key blocks per stage
+  __shared__ float sk[kJ][D];
+  __shared__ float sv[kJ][D];
+  const int bh = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long base = (long long)bh * T * D;
+  float q[4][kC], acc[4][kC], m[4], l[4];
+  int rows[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    rows[r] = blockIdx.x * 16 + warp * 4 + r;
+    const int u = rows[r] < T ? rows[r] : T - 1;
+#pragma unroll
+    for (int c = 0; c < kC; ++c) {
+      q[r][c] = qc[base + (long long)u * D + c * 32 + lane];
+      acc[r][c] = 0.f;
+    }
+    m[r] = -INFINITY;
+    l[r] = 0.f;
+  }
+  for (int j0 = 0; j0 < T; j0 += kJ) {
+    const int nj = T - j0 < kJ ? T - j0 : kJ;
+    __syncthreads();
+    for (int e = threadIdx.x; e < nj * D; e += 128) {
+      sk[e / D][e % D] = kc[base + (long long)j0 * D + e];
+      sv[e / D][e % D] = vc[base + (long long)j0 * D + e];
+    }
+    __syncthreads();
+    for (int j = 0; j < nj; ++j) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        float sdot = 0.f;
+#pragma unroll
+        for (int c = 0; c < kC; ++c) sdot = fmaf(q[r][c], sk[j][c * 32 + lane], sdot);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+        float w;
+        if (use_softmax) {
+          const float sv_ = sdot * scale;
+          const float mn = fmaxf(m[r], sv_);
+          const float corr = __expf(m[r] - mn);  // m = -inf -> 0
+          w = __expf(sv_ - mn);
+          l[r] = l[r] * corr + w;
+#pragma unroll
+          for (int c = 0; c < kC; ++c) acc[r][c] *= corr;
+          m[r] = mn;
+        } else {
+          w = sdot;  // raw, unscaled scores
+        }
+#pragma unroll
+        for (int c = 0; c < kC; ++c) acc[r][c] = fmaf(w, sv[j][c * 32 + lane], acc[r][c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if (rows[r] >= T) continue;
+    const float inv = use_softmax ? 1.f / l[r] : 1.f;
+#pragma unroll
+    for (int c = 0; c < kC; ++c) out[base + (long long)rows[r] * D + c * 32 + lane] = acc[r][c] * inv;
+  }
+}
+
 // int32 -> int64 export of routing lists (caller-facing int64 API, pipeline types).
 __global__ void widen_kernel(const int* __restrict__ src, int64_t* __restrict__ dst, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)

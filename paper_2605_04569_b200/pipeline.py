@@ -90,7 +90,8 @@ class _Inputs:
         self.shape = N.IsaShape(d.B, d.H, d.S, d.D, self.icl.l_src, self.icl.l_ctx, b,
                                 N.ISA_DTYPE_BF16 if q.dtype == torch.bfloat16 else N.ISA_DTYPE_F32,
                                 q.stride(0), q.stride(1), q.stride(2))
-        self.knobs = N.IsaKnobs(d.scale, d.k_ctx, d.n_flat, max(d.k, 1), int(bool(self.cfg.softmax_first)), 0)
+        self.knobs = N.IsaKnobs(d.scale, d.k_ctx, d.n_flat, max(d.k, 1), int(bool(self.cfg.softmax_first)), 0,
+                                float(self.cfg.gamma), int(bool(self.cfg.residual_softmax)))
 
     @staticmethod
     def _to_host(x, name):

@@ -81,8 +81,6 @@ class IsaConfig:
             raise ConfigError(
                 f"block_size={self.block_size} is not supported by the sm_100a kernels (only {SUPPORTED_BLOCK})"
             )
-        if self.gamma != 0.0:
-            raise ConfigError("gamma > 0 (coarse residual) is not implemented on the B200 path yet")
         if self.precision != "single":
             raise ConfigError("precision='double' is not available on the bf16 tensor-core path")
         return self
@@ -344,6 +342,7 @@ class IsaDims:
     n_sharp: int
     k: int  # exact blocks per flat query block (0 when n_flat == 0)
     scale: float
+    gamma: float = 0.0  # coarse residual weight (pipeline.py:354-356)
 
     @staticmethod
     def derive(shape, icl: IclLayout, cfg: IsaConfig) -> "IsaDims":
@@ -358,7 +357,8 @@ class IsaDims:
         n_sharp = T - n_flat
         k = min(t_new, max(1, int(math.floor(cfg.alpha_ns * t_new)))) if n_flat else 0
         scale = cfg.scale if cfg.scale is not None else 1.0 / math.sqrt(D)
-        return IsaDims(B, H, S, D, b, icl.l_src, icl.l_ctx, t_src, t_ctx, T, k_ctx, t_new, n_flat, n_sharp, k, scale)
+        return IsaDims(B, H, S, D, b, icl.l_src, icl.l_ctx, t_src, t_ctx, T, k_ctx, t_new, n_flat, n_sharp, k, scale,
+                       float(cfg.gamma))
 
     def flops(self) -> FlopCount:
         """Reference accounting (pipeline.py:269-289 with taylor.py:299-316)."""
@@ -373,6 +373,8 @@ class IsaDims:
         overhead = 2 * B * H * self.T * self.T * D
         if self.n_flat:
             overhead += 2 * B * H * self.n_flat * self.t_new * D
+        if self.gamma:
+            overhead += 2 * B * H * self.T * self.T * D  # residual P V^c (pipeline.py:284-285)
         return FlopCount(
             exact_mas=exact,
             taylor_mas=taylor,

@@ -50,6 +50,10 @@ CASES = [
     ("rawvar_clustered_s9", "clustered", 2, 1, 2048, 64, 1024, 1024, 9, {"softmax_first": False}),
     ("ragged_clustered_s10", "clustered", 1, 2, 1500, 128, 900, 600, 10,
      {"strict": False, "alpha_s": 0.5, "alpha_ns": 0.25}),
+    # gamma coarse residual (pipeline.py:261-267, 354-356), softmax and raw-score variants
+    ("gamma_clustered_s14", "clustered", 1, 2, 2048, 64, 1024, 1024, 14, {"gamma": 0.5}),
+    ("gamma_raw_iid_s15", "iid-gaussian", 1, 2, 2100, 128, 1000, 1100, 15,
+     {"gamma": 0.05, "residual_softmax": False, "strict": False}),
     # routing-only cases (no stored output): larger T so the block mask has k > 1
     ("mid_iid_s11", "iid-gaussian", 1, 2, 8192, 64, 4096, 4096, 11, {"_routing_only": True}),
     ("mid_clustered_s12", "clustered", 1, 2, 8192, 128, 4096, 4096, 12, {"_routing_only": True}),

@@ -42,7 +42,7 @@ class GoldenCase:
     def oracle_kwargs(self) -> dict:
         c = self.cfg
         kw = {}
-        for key in ("alpha_s", "alpha_ns", "alpha_f", "softmax_first", "scale"):
+        for key in ("alpha_s", "alpha_ns", "alpha_f", "softmax_first", "scale", "gamma", "residual_softmax"):
             if key in c:
                 kw[key] = c[key]
         return kw

@@ -50,10 +50,13 @@ def test_config_defaults_match_reference():
 
 
 def test_b200_limits_raise_config_error():
-    for kw in (dict(block_size=32), dict(gamma=0.5), dict(precision="double")):
+    for kw in (dict(block_size=32), dict(precision="double")):
         with pytest.raises(E.ConfigError):
             IsaConfig(**kw).validate_b200()
     IsaConfig().validate_b200()
+    IsaConfig(gamma=0.5, residual_softmax=False).validate_b200()  # coarse residual is implemented
+    with pytest.raises(E.ConfigError):
+        IsaConfig(gamma=-1.0).validate_b200()
 
 
 def test_layouts_match_reference():
