@@ -50,13 +50,15 @@ typedef enum IsaDtype { ISA_DTYPE_BF16 = 0, ISA_DTYPE_F32 = 1 } IsaDtype;
 
 /* Geometry of Q/K/V (B,H,S,D) and the IclLayout (tensor.py:78-93). Q, K and V
  * share shape and element strides; the D stride must be 1. `out` is written
- * contiguous (B,H,S,D) in the input dtype. */
+ * in the input dtype with the out_stride_* element strides (D contiguous; all
+ * zero = contiguous (B,H,S,D)), e.g. straight into a (B,S,H*D) activation. */
 typedef struct IsaShape {
   int32_t batch, heads, seq_len, head_dim;
   int32_t l_src, l_ctx;  /* source tokens first, then context */
   int32_t block;         /* b (only 64 is implemented) */
   int32_t dtype;         /* IsaDtype of q, k, v and out */
   int64_t stride_b, stride_h, stride_s; /* element strides of q, k, v */
+  int64_t out_stride_b, out_stride_h, out_stride_s; /* element strides of out; all 0 = contiguous (B,H,S,D) */
 } IsaShape;
 
 /* Host-derived integers, computed by the caller with the reference's float
@@ -154,6 +156,13 @@ int isa_routing(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
  * sequence is a single segment. */
 int isa_dense_attention(const IsaShape* shape, double scale, const void* q, const void* k, const void* v,
                         void* out, void* stream);
+
+/* Decoupled rotary embedding (pipeline.py:469-490, apply_decoupled_rope):
+ * pairs (2i, 2i+1) of each token rotate by pos * base^(-2i/D) with positions
+ * 0..L_src-1 for the source segment and 0..L_ctx-1 for the context segment.
+ * x and out share shape (B,H,S,D); x uses the shape's strides, out the out
+ * strides; dtype bf16 or fp32; angles in fp64, rotation in fp32. */
+int isa_decoupled_rope(const IsaShape* shape, double base, const void* x, void* out, void* stream);
 
 /* ---- stage primitives (test hooks; same kernels as the pipeline) ---- */
 

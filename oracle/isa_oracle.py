@@ -417,3 +417,19 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
     u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
     u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
     return u.astype(np.uint32).view(np.float32)
+
+
+def apply_decoupled_rope(x: np.ndarray, l_src: int, l_ctx: int, base: float = 10000.0) -> np.ndarray:
+    """Rotary rotation, positions restarting at 0 for the context segment;
+    fp64 math, result in x's dtype (pipeline.py:469-490)."""
+    B, H, S, D = x.shape
+    pos = np.concatenate([np.arange(l_src), np.arange(l_ctx)]).astype(np.float64)
+    inv_freq = base ** (-np.arange(0, D, 2, dtype=np.float64) / D)
+    theta = pos[:, None] * inv_freq[None, :]
+    cos, sin = np.cos(theta), np.sin(theta)
+    xf = x.astype(np.float64).reshape(B, H, S, D // 2, 2)
+    even, odd = xf[..., 0], xf[..., 1]
+    out = np.empty_like(xf)
+    out[..., 0] = even * cos - odd * sin
+    out[..., 1] = even * sin + odd * cos
+    return out.reshape(B, H, S, D).astype(x.dtype)

@@ -40,7 +40,8 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # The operator entry points import torch; keep `import paper_2605_04569_b200`
     # light for host-only consumers (types, errors, build).
-    if name in ("isa_forward", "isa_routing", "isa_forward_with_routing", "dense_attention", "prepare"):
+    if name in ("isa_forward", "isa_routing", "isa_forward_with_routing", "dense_attention", "prepare",
+                "apply_decoupled_rope"):
         from . import pipeline
 
         return getattr(pipeline, name)
@@ -48,4 +49,8 @@ def __getattr__(name):
         from . import parallel
 
         return getattr(parallel, name)
+    if name in ("DiTAttentionLayer", "DiTAttentionStack"):
+        from . import stack
+
+        return getattr(stack, name)
     raise AttributeError(name)

@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "isa_split_rows_f64",
     "isa_forward_host_bytes",
     "isa_forward_host",
+    "isa_decoupled_rope",
 )
 
 
@@ -50,6 +51,9 @@ class IsaShape(ctypes.Structure):
         ("stride_b", ctypes.c_int64),
         ("stride_h", ctypes.c_int64),
         ("stride_s", ctypes.c_int64),
+        ("out_stride_b", ctypes.c_int64),
+        ("out_stride_h", ctypes.c_int64),
+        ("out_stride_s", ctypes.c_int64),
     ]
 
 
@@ -112,6 +116,7 @@ _SIGS = {
     "isa_topk_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _I, _P]),
     "isa_sharpness_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P]),
     "isa_split_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P, _P]),
+    "isa_decoupled_rope": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.c_double, _P, _P, _P]),
     "isa_forward_host_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _I,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
     "isa_forward_host": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _P, _P, _P, _P, _I, _P,

@@ -347,6 +347,28 @@ int check_io(const IsaShape* sh, const void* q, const void* k, const void* v) {
   return ISA_OK;
 }
 
+// Output element strides: caller's (D contiguous) or contiguous (B,H,S,D).
+void out_strides(const IsaShape* sh, const Dims& d, isa::AttnParams* p) {
+  if (sh->out_stride_b || sh->out_stride_h || sh->out_stride_s) {
+    p->o_sb = sh->out_stride_b;
+    p->o_sh = sh->out_stride_h;
+    p->o_ss = sh->out_stride_s;
+  } else {
+    p->o_sh = (long long)d.S * d.D;
+    p->o_sb = (long long)d.H * d.S * d.D;
+    p->o_ss = d.D;
+  }
+}
+
+int check_out(const IsaShape* sh, const void* out) {
+  const int elem = sh->dtype == ISA_DTYPE_BF16 ? 2 : 4;
+  if (!out || (reinterpret_cast<uintptr_t>(out) & 15)) return fail(ISA_ERR_LAYOUT, "out must be 16-byte aligned");
+  const long long st[3] = {sh->out_stride_b, sh->out_stride_h, sh->out_stride_s};
+  for (long long s : st)
+    if ((s * elem) & 15) return fail(ISA_ERR_LAYOUT, "out strides must be multiples of 16 bytes");
+  return ISA_OK;
+}
+
 void record(const IsaEvents* ev, int i, cudaStream_t st) {
   if (ev && ev->ev[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev->ev[i]), st);
 }
@@ -579,6 +601,7 @@ IsaShape chunk_shape(const IsaShape* sh, int heads) {
   c.stride_s = sh->head_dim;
   c.stride_h = (long long)sh->seq_len * sh->head_dim;
   c.stride_b = c.stride_h * heads;
+  c.out_stride_b = c.out_stride_h = c.out_stride_s = 0;
   return c;
 }
 
@@ -660,7 +683,7 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
   int rc = derive(shape, knobs, &d);
   if (rc) return rc;
   if ((rc = check_io(shape, q, k, v))) return rc;
-  if (!out || (reinterpret_cast<uintptr_t>(out) & 15)) return fail(ISA_ERR_LAYOUT, "out must be 16-byte aligned");
+  if ((rc = check_out(shape, out))) return rc;
   Workspace w = carve(d, shape->dtype, static_cast<uint8_t*>(workspace));
   if (!workspace || workspace_bytes < w.bytes)
     return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, w.bytes);
@@ -681,9 +704,7 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
   p.kv_blk = w.kv_blk;
   p.out = out;
   p.out_fp32 = shape->dtype == ISA_DTYPE_F32;
-  p.o_sh = (long long)d.S * d.D;
-  p.o_sb = (long long)d.H * d.S * d.D;
-  p.o_ss = d.D;
+  out_strides(shape, d, &p);
   p.err_flag = err_word;
   p.resid = w.resid;  // null unless gamma > 0
   p.gamma = static_cast<float>(d.gamma);
@@ -751,11 +772,43 @@ int isa_dense_attention(const IsaShape* shape, double scale, const void* q, cons
   p.scale_log2 = static_cast<float>(scale * 1.4426950408889634);
   p.out = out;
   p.out_fp32 = 0;
-  p.o_sh = (long long)d.S * d.D;
-  p.o_sb = (long long)d.H * d.S * d.D;
-  p.o_ss = d.D;
+  out_strides(shape, d, &p);
   return launch_attention_d<isa::MODE_DENSE>(d.D, tq, tk, tv, tq, tq, p, (d.T + 3) / 4, d.BH,
                                              static_cast<cudaStream_t>(stream));
+}
+
+int isa_decoupled_rope(const IsaShape* shape, double base, const void* x, void* out, void* stream) {
+  g_launches = 0;
+  if (!shape) return fail(ISA_ERR_CONFIG, "null shape");
+  const IsaShape* sh = shape;
+  if (sh->batch < 1 || sh->heads < 1 || sh->seq_len < 1 || sh->head_dim < 8 || sh->head_dim % 8)
+    return fail(ISA_ERR_CONFIG, "decoupled rope needs D a multiple of 8, got D=%d", sh->head_dim);
+  if (sh->l_src < 0 || sh->l_ctx < 0 || sh->l_src + sh->l_ctx != sh->seq_len)
+    return fail(ISA_ERR_LAYOUT, "sequence length %d != icl total %d", sh->seq_len, sh->l_src + sh->l_ctx);
+  if (!(base > 0.0)) return fail(ISA_ERR_CONFIG, "rope base must be > 0");
+  if (sh->dtype != ISA_DTYPE_BF16 && sh->dtype != ISA_DTYPE_F32) return fail(ISA_ERR_CONFIG, "bad dtype");
+  int rc;
+  if ((rc = check_io(sh, x, x, x))) return rc;
+  if ((rc = check_out(sh, out))) return rc;
+  const long long D = sh->head_dim, S = sh->seq_len, H = sh->heads;
+  const long long ob = sh->out_stride_b ? sh->out_stride_b : H * S * D;
+  const long long oh = sh->out_stride_h ? sh->out_stride_h : S * D;
+  const long long os = sh->out_stride_s ? sh->out_stride_s : D;
+  const long long n = S * (D / 8);
+  const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const double lb = std::log2(base);
+  if (sh->dtype == ISA_DTYPE_BF16)
+    isa::decoupled_rope_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(out), sh->batch, sh->heads, sh->seq_len,
+        sh->head_dim, sh->l_src, sh->stride_b, sh->stride_h, sh->stride_s, ob, oh, os, lb);
+  else
+    isa::decoupled_rope_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), static_cast<float*>(out),
+                                                           sh->batch, sh->heads, sh->seq_len, sh->head_dim,
+                                                           sh->l_src, sh->stride_b, sh->stride_h, sh->stride_s, ob,
+                                                           oh, os, lb);
+  ISA_LAUNCHED("decoupled_rope_kernel");
+  return ISA_OK;
 }
 
 int isa_pool_means(const IsaShape* shape, const void* q, const void* k, const void* v, float* means,

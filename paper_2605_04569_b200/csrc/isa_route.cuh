@@ -744,6 +744,73 @@ __global__ void __launch_bounds__(128) coarse_residual_kernel(const float* __res
   }
 }
 
+// ----------------------------------------------------------------------------
+// Decoupled RoPE (pipeline.py:469-490): position = token index within its
+// segment (source 0..L_src-1, context 0..L_ctx-1); pair i of D/2 rotates by
+// pos * base^(-2i/D). One thread per (token, 4 pairs): the angles are formed
+// once in fp64 and applied to every (b, h) row; HBM-bound streaming.
+// ----------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) decoupled_rope_kernel(const T* __restrict__ x, T* __restrict__ out, int B,
+                                                            int H, int S, int D, int l_src, long long xb,
+                                                            long long xh, long long xs, long long ob, long long oh,
+                                                            long long os, double log2_base) {
+  const int per_tok = D / 8;
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)S * per_tok) return;
+  const int tok = static_cast<int>(gid / per_tok);
+  const int c0 = static_cast<int>(gid % per_tok) * 8;  // first element of this thread's 4 pairs
+  const double pos = tok < l_src ? tok : tok - l_src;
+  float cs[4], sn[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int i = c0 / 2 + j;
+    const double theta = pos * exp2(-log2_base * (2.0 * i) / D);  // pos * base^(-2i/D)
+    double sd, cd;
+    sincos(theta, &sd, &cd);
+    cs[j] = static_cast<float>(cd);
+    sn[j] = static_cast<float>(sd);
+  }
+  for (int b = 0; b < B; ++b) {
+    for (int h = 0; h < H; ++h) {
+      const T* src = x + b * xb + h * xh + tok * xs + c0;
+      T* dst = out + b * ob + h * oh + tok * os + c0;
+      float v[8];
+      if constexpr (sizeof(T) == 2) {
+        const uint4 w = *reinterpret_cast<const uint4*>(src);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          v[2 * j] = __uint_as_float(ws[j] << 16);
+          v[2 * j + 1] = __uint_as_float(ws[j] & 0xffff0000u);
+        }
+      } else {
+        const float4 a = *reinterpret_cast<const float4*>(src);
+        const float4 c = *reinterpret_cast<const float4*>(src + 4);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = c.x; v[5] = c.y; v[6] = c.z; v[7] = c.w;
+      }
+      float r[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float e = v[2 * j], o = v[2 * j + 1];
+        r[2 * j] = e * cs[j] - o * sn[j];
+        r[2 * j + 1] = e * sn[j] + o * cs[j];
+      }
+      if constexpr (sizeof(T) == 2) {
+        uint4 w;
+        w.x = pack_bf16x2(r[0], r[1]);
+        w.y = pack_bf16x2(r[2], r[3]);
+        w.z = pack_bf16x2(r[4], r[5]);
+        w.w = pack_bf16x2(r[6], r[7]);
+        *reinterpret_cast<uint4*>(dst) = w;
+      } else {
+        *reinterpret_cast<float4*>(dst) = make_float4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<float4*>(dst + 4) = make_float4(r[4], r[5], r[6], r[7]);
+      }
+    }
+  }
+}
+
 // int32 -> int64 export of routing lists (caller-facing int64 API, pipeline types).
 __global__ void widen_kernel(const int* __restrict__ src, int64_t* __restrict__ dst, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)

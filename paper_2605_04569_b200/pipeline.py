@@ -45,7 +45,8 @@ from .types import (
     icl_from_any,
 )
 
-__all__ = ["isa_forward", "isa_routing", "isa_forward_with_routing", "dense_attention", "prepare"]
+__all__ = ["isa_forward", "isa_routing", "isa_forward_with_routing", "dense_attention", "prepare",
+           "apply_decoupled_rope"]
 
 
 def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
@@ -291,6 +292,18 @@ def _run_host(inp: _Inputs, collect_trace: bool, pinned=None, out=None, validate
     return out, trace, bufs
 
 
+def _set_out_strides(shape: N.IsaShape, out, d: IsaDims, dtype):
+    """Caller-provided output: any (B,H,S,D) view with a contiguous D axis and
+    16-byte aligned strides (e.g. a permuted (B,S,H*D) activation buffer)."""
+    if not (isinstance(out, torch.Tensor) and out.is_cuda and tuple(out.shape) == (d.B, d.H, d.S, d.D)
+            and out.dtype == dtype and out.stride(3) == 1):
+        raise LayoutError("out must be a CUDA (B,H,S,D) tensor of the input dtype with a contiguous D axis")
+    e = out.element_size()
+    if out.data_ptr() % 16 or any((st * e) % 16 for st in out.stride()[:3]):
+        raise LayoutError("out strides must be multiples of 16 bytes")
+    shape.out_stride_b, shape.out_stride_h, shape.out_stride_s = out.stride()[:3]
+
+
 def _run(inp: _Inputs, collect_trace: bool, pinned=None, out: Optional[torch.Tensor] = None, validate=True,
          heads_per_chunk: int = 0):
     if inp.host:
@@ -302,8 +315,8 @@ def _run(inp: _Inputs, collect_trace: bool, pinned=None, out: Optional[torch.Ten
     ws, nbytes = inp.workspace()
     if out is None:
         out = torch.empty((d.B, d.H, d.S, d.D), dtype=inp.q.dtype, device=dev)
-    elif not (out.is_contiguous() and tuple(out.shape) == (d.B, d.H, d.S, d.D) and out.dtype == inp.q.dtype):
-        raise LayoutError("out must be a contiguous (B,H,S,D) tensor of the input dtype")
+    else:
+        _set_out_strides(inp.shape, out, d, inp.q.dtype)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     bufs = _routing_buffers(d, dev) if collect_trace else None
     rout = _routing_struct(bufs) if bufs is not None else None
@@ -400,6 +413,45 @@ def dense_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: Op
     shape = N.IsaShape(B, H, S, D, S, 0, 64, N.ISA_DTYPE_BF16, q.stride(0), q.stride(1), q.stride(2))
     N.check(N.load().isa_dense_attention(ctypes.byref(shape), scale, _ptr(q), _ptr(k), _ptr(v), _ptr(out),
                                          torch.cuda.current_stream(q.device).cuda_stream))
+    return out
+
+
+def apply_decoupled_rope(x, icl: IclLayout, base: float = 10000.0, *, out: Optional[torch.Tensor] = None):
+    """Rotary rotation with positions restarting at zero for the context
+    segment (pipeline.py:469-490, same signature). Pairs (2i, 2i+1) rotate by
+    pos * base^(-2i/D). Angles in fp64, rotation in fp32 on the GPU; returns a
+    new tensor of x's dtype (numpy in -> numpy out, like the reference), or
+    writes `out` (any (B,H,S,D) view with a contiguous D axis)."""
+    icl = icl_from_any(icl)
+    numpy_io = isinstance(x, np.ndarray)
+    if numpy_io:
+        if x.ndim != 4:
+            raise LayoutError(f"rope input: expected 4 axes (B,H,S,D), got shape {x.shape}")
+        x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dim() == 4):
+        raise LayoutError("rope input must be a CUDA (B,H,S,D) tensor or a numpy array")
+    B, H, S, D = x.shape
+    if D % 2:
+        raise ConfigError(f"decoupled rope needs an even head dim, got D={D}")
+    if S != icl.total:
+        raise LayoutError(f"sequence length {S} != icl total {icl.total}")
+    if x.dtype not in (torch.bfloat16, torch.float32):
+        x = x.float()
+    if x.stride(3) != 1 or any((st * x.element_size()) % 16 for st in x.stride()[:3]) or x.data_ptr() % 16:
+        x = x.contiguous()
+    if out is None:
+        out = torch.empty((B, H, S, D), dtype=x.dtype, device=x.device)
+    shape = N.IsaShape(B, H, S, D, icl.l_src, icl.l_ctx, 64,
+                       N.ISA_DTYPE_BF16 if x.dtype == torch.bfloat16 else N.ISA_DTYPE_F32,
+                       x.stride(0), x.stride(1), x.stride(2))
+    if not (isinstance(out, torch.Tensor) and out.is_cuda and tuple(out.shape) == (B, H, S, D)
+            and out.dtype == x.dtype and out.stride(3) == 1):
+        raise LayoutError("out must be a CUDA (B,H,S,D) tensor of x's dtype with a contiguous D axis")
+    shape.out_stride_b, shape.out_stride_h, shape.out_stride_s = out.stride()[:3]
+    N.check(N.load().isa_decoupled_rope(ctypes.byref(shape), float(base), _ptr(x), _ptr(out),
+                                        torch.cuda.current_stream(x.device).cuda_stream))
+    if numpy_io:
+        return out.cpu().numpy()
     return out
 
 

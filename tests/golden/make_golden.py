@@ -99,8 +99,37 @@ def make_case(name, kind, B, H, S, D, l_src, l_ctx, seed, over):
           f"n_flat={payload['flat'].shape[2]} k={payload['mask'].shape[3]}")
 
 
+ROPE_CASES = [
+    # name, B, H, l_src, l_ctx, D, base, seed
+    ("rope_small", 1, 2, 100, 60, 64, 10000.0, 0),
+    ("rope_ragged_d128", 2, 1, 300, 257, 128, 500.0, 1),
+    ("rope_long_positions", 1, 1, 50000, 64, 128, 10000.0, 2),
+]
+
+
+def make_rope(name, B, H, l_src, l_ctx, D, base, seed):
+    """Golden vectors for the reference apply_decoupled_rope (pipeline.py:469-490)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((B, H, l_src + l_ctx, D)).astype(np.float32)
+    out = isattn.apply_decoupled_rope(x, isattn.IclLayout(l_src, l_ctx), base=base)
+    # store a row sample (ends of both segments + strided interior); x is
+    # regenerated from the seed and pinned by its checksum
+    S = l_src + l_ctx
+    rows = np.unique(np.concatenate([np.arange(min(S, 96)), np.arange(max(0, l_src - 96), min(S, l_src + 96)),
+                                     np.arange(max(0, S - 96), S), np.arange(0, S, 997)]))
+    meta = {"name": name, "B": B, "H": H, "D": D, "l_src": l_src, "l_ctx": l_ctx, "base": base, "seed": seed,
+            "x_sum": float(x.astype(np.float64).sum())}
+    np.savez_compressed(os.path.join(HERE, "rope", f"{name}.npz"), meta=json.dumps(meta), rows=rows,
+                        out=out[:, :, rows])
+    print(f"{name}: {x.shape}, {rows.size} rows stored")
+
+
 if __name__ == "__main__":
     only = set(sys.argv[1:])
     for case in CASES:
         if not only or case[0] in only:
             make_case(*case)
+    os.makedirs(os.path.join(HERE, "rope"), exist_ok=True)
+    for case in ROPE_CASES:
+        if not only or case[0] in only:
+            make_rope(*case)
