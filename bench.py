@@ -174,7 +174,7 @@ def run_ours(args, rank, world, local_rank):
     H, D = args.heads, WORKLOAD["head_dim"]
     S = args.l_src + args.l_ctx
     icl = P.IclLayout(args.l_src, args.l_ctx)
-    cfg = P.IsaConfig()
+    cfg = P.IsaConfig(strict=(args.l_src % 64 == 0 and args.l_ctx % 64 == 0))  # ragged segments (cfg5) allowed
     my_heads = head_shard(H, rank, world)
     Hl = len(my_heads)
     g = torch.Generator(device=dev).manual_seed(0)

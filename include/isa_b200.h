@@ -145,6 +145,18 @@ int isa_forward_host(const IsaShape* shape, const IsaKnobs* knobs, const void* q
                      void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
                      int32_t* err_word, void* const* streams);
 
+/* Backward with frozen routing (isa_backward, pipeline.py:373-466; gamma = 0):
+ * recomputes the forward (routing from q/k, or `pinned`) with its per-row
+ * softmax statistics, then the sharp-branch (reference.py:173-225) and Taylor
+ * (taylor.py:225-296) gradients, scattered back through the K_new gather
+ * (pipeline.py:423-433). q/k/v/dout: bf16 with the shape's strides; dq/dk/dv:
+ * fp32 contiguous (B,H,S,D), fully written (rows of unselected context blocks
+ * get 0). Workspace sized by isa_backward_workspace_bytes. */
+int isa_backward_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* bytes);
+int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
+                 const void* dout, float* dq, float* dk, float* dv, void* workspace, size_t workspace_bytes,
+                 const IsaRoutingIn* pinned, int32_t* err_word, void* stream);
+
 /* Stages 1-3 only (isa_routing, pipeline.py:302-304). */
 int isa_routing(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
                 void* workspace, size_t workspace_bytes, IsaRoutingOut* routing, int32_t* err_word,

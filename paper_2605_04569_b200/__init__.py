@@ -25,6 +25,7 @@ from .types import (
     BlockLayout,
     BlockMask,
     FlopCount,
+    GradBundle,
     IclLayout,
     IsaConfig,
     IsaDims,
@@ -40,8 +41,8 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # The operator entry points import torch; keep `import paper_2605_04569_b200`
     # light for host-only consumers (types, errors, build).
-    if name in ("isa_forward", "isa_routing", "isa_forward_with_routing", "dense_attention", "prepare",
-                "apply_decoupled_rope"):
+    if name in ("isa_forward", "isa_routing", "isa_forward_with_routing", "isa_backward", "dense_attention",
+                "prepare", "apply_decoupled_rope"):
         from . import pipeline
 
         return getattr(pipeline, name)

@@ -35,6 +35,8 @@ EXPORTED_SYMBOLS = (
     "isa_forward_host_bytes",
     "isa_forward_host",
     "isa_decoupled_rope",
+    "isa_backward_workspace_bytes",
+    "isa_backward",
 )
 
 
@@ -116,6 +118,10 @@ _SIGS = {
     "isa_topk_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _I, _P]),
     "isa_sharpness_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P]),
     "isa_split_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P, _P]),
+    "isa_backward_workspace_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs),
+                                                    ctypes.POINTER(ctypes.c_size_t)]),
+    "isa_backward": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _P, _P, _P, _P, _P, _P, _P,
+                                    _P, ctypes.c_size_t, ctypes.POINTER(IsaRoutingIn), _P, _P]),
     "isa_decoupled_rope": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.c_double, _P, _P, _P]),
     "isa_forward_host_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _I,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),

@@ -61,6 +61,10 @@ struct AttnParams {
   const float* resid;  // [BH][T][D] or null
   float gamma;
   int T;
+  // backward support: per-row log2-domain normaliser m + log2(l) of the
+  // (surrogate) softmax, [BH][S] by original token row, or null
+  float* lse;
+  int S;
 };
 
 #ifndef ISA_TRACE_Q
@@ -866,6 +870,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
     const int rr = row & 63;
     const bool write = u >= 0 && rr < blk_valid(p, u);
     if (write && !(l > 0.f) && p.err_flag) atomicOr(p.err_flag, 2);
+    if (write && p.lse) p.lse[(long long)bh * p.S + blk_tok0(p, u) + rr] = l > 0.f ? m + log2f(l) : -INFINITY;
     const float inv = l > 0.f ? 1.f / l : 0.f;
     const int hh = bh % p.H, bb = bh / p.H;
     const long long obase =

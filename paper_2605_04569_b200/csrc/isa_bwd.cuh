@@ -1,0 +1,460 @@
+// ISA backward with frozen routing (isa_backward, pipeline.py:373-466):
+// gradients of the sharp branch (full_attention_backward, reference.py:173-225)
+// and of the Taylor branch (taylor_sparse_backward, taylor.py:225-296), with
+// the K_new gather adjoint (pipeline.py:423-433) fused into the key-major
+// kernel's stores. gamma = 0.
+//
+// Softmax statistics come from the forward kernels (AttnParams::lse, log2
+// domain: P = exp2(scale*log2e * q.k + log2(w) - lse)); rho = rowsum(dO * O).
+// Three kernels, all mma.sync m16n8k16 bf16 -> fp32 (round-1 baseline; the
+// tcgen05 rewrite is the next step):
+//   bwd_dkv_kernel<CENTROID=1>: per tile of 64 K_new centroids, over all flat
+//       query blocks: dkc, dvc (taylor.py:286-289), fp32 [BH][t_new][D]
+//   bwd_dkv_kernel<CENTROID=0>: per K_new block j, over the sharp blocks and
+//       the flat blocks listing j: dK_j, dV_j (+ the centroid part spread over
+//       the block's valid rows, taylor.py:290-292), stored at the block's
+//       original token rows (unselected context rows stay 0)
+//   bwd_dq_kernel: per query block, over its key tiles (all K_new blocks for a
+//       sharp block; its exact blocks then every centroid tile for a flat one)
+#pragma once
+#include "isa_ptx.cuh"
+
+namespace isa {
+
+struct BwdParams {
+  int H, S, D;
+  int l_src, l_ctx, t_src, t_ctx, t_new;
+  int n_sharp, n_flat, k, W, tn_pad;
+  float sl2;    // scale * log2(e)
+  float scale;  // softmax scale (dS -> dQ/dK factor)
+  const __nv_bfloat16 *q, *kx, *v, *dout;  // token-major with element strides below
+  long long sb, sh, ss;                    // q/k/v strides
+  long long db, dh, ds;                    // dout strides
+  const float* lse;                        // [BH][S]
+  const float* rho;                        // [BH][S]
+  const int* sharp;                        // [BH][n_sharp]
+  const int* flat;                         // [BH][n_flat]
+  const int* mask;                         // [BH][n_flat][k] K_new indices
+  const int* kv_blk;                       // [BH][t_new]
+  const uint32_t* bits;                    // [BH][n_flat][W] member bits
+  const __nv_bfloat16 *kc, *vc;            // [BH][tn_pad][D] K_new centroids
+  float *dkc, *dvc;                        // [BH][t_new][D]
+  float *dq, *dk, *dv;                     // [BH][S][D]
+};
+
+__device__ __forceinline__ int bw_tok0(const BwdParams& p, int u) {
+  return u < p.t_src ? u * 64 : p.l_src + (u - p.t_src) * 64;
+}
+__device__ __forceinline__ int bw_valid(const BwdParams& p, int u) {
+  const int r = u < p.t_src ? p.l_src - u * 64 : p.l_ctx - (u - p.t_src) * 64;
+  return r < 64 ? r : 64;
+}
+
+// ---------------------------------------------------------------- mma.sync helpers
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm4t(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+// 64-row x D bf16 tile in shared memory, 16-byte chunks XOR-swizzled by row
+// (conflict-free ldmatrix on 8 consecutive rows).
+template <int D>
+struct SmTile {
+  static constexpr int kChunks = D / 8;
+  __device__ __forceinline__ static uint32_t addr(uint32_t base, int row, int chunk) {
+    return base + (uint32_t)(row * D * 2 + ((chunk ^ (row & 7)) << 4));
+  }
+};
+
+// Cooperative load of `rows` valid rows (the rest zero) of a token-major bf16
+// matrix (row stride `rs` elements) into a swizzled tile. 128 threads.
+template <int D>
+__device__ __forceinline__ void load_tile(uint8_t* sm, const __nv_bfloat16* src, long long rs, int rows) {
+  constexpr int C = D / 8;
+  const uint32_t base = smem_u32(sm);
+  for (int e = threadIdx.x; e < 64 * C; e += 128) {
+    const int r = e / C, c = e % C;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (r < rows) val = *reinterpret_cast<const uint4*>(src + r * rs + c * 8);
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(SmTile<D>::addr(base, r, c)), "r"(val.x), "r"(val.y),
+                 "r"(val.z), "r"(val.w));
+  }
+}
+
+// A fragments (16 rows from row0, 16 columns from col0) of a swizzled tile.
+template <int D>
+__device__ __forceinline__ void frag_a(uint32_t (&a)[4], uint32_t base, int row0, int col0) {
+  const int t = threadIdx.x & 31;
+  ldsm4(a, SmTile<D>::addr(base, row0 + (t & 15), (col0 >> 3) + (t >> 4)));
+}
+// B fragments of two n8 tiles (n0, n0+8) x k16 from a [n][k] row-major tile.
+template <int D>
+__device__ __forceinline__ void frag_b(uint32_t (&b)[4], uint32_t base, int n0, int k0) {
+  const int t = threadIdx.x & 31;
+  ldsm4(b, SmTile<D>::addr(base, n0 + (t & 7) + ((t >> 4) << 3), (k0 >> 3) + ((t >> 3) & 1)));
+}
+// B fragments of two n8 tiles (n0, n0+8) x k16 from a [k][n] row-major tile.
+template <int D>
+__device__ __forceinline__ void frag_bt(uint32_t (&b)[4], uint32_t base, int k0, int n0) {
+  const int t = threadIdx.x & 31;
+  ldsm4t(b, SmTile<D>::addr(base, k0 + (t & 7) + (((t >> 3) & 1) << 3), (n0 >> 3) + (t >> 4)));
+}
+
+// ---------------------------------------------------------------- rho
+// rho[bh][row] = sum_d dO * O (taylor.py:274; reference.py:218 in closed form).
+__global__ void bwd_rho_kernel(const __nv_bfloat16* __restrict__ dout, long long db, long long dh, long long ds,
+                               const __nv_bfloat16* __restrict__ o, int H, int S, int D, float* __restrict__ rho,
+                               long long n_rows) {
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n_rows) return;
+  const int bh = static_cast<int>(w / S), tok = static_cast<int>(w % S);
+  const __nv_bfloat16* a = dout + (bh / H) * db + (bh % H) * dh + tok * ds;
+  const __nv_bfloat16* b = o + w * D;
+  float acc = 0.f;
+  for (int d = lane * 2; d < D; d += 64) {
+    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + d));
+    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(b + d));
+    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) rho[w] = acc;
+}
+
+// ---------------------------------------------------------------- dQ (query-major)
+// CTA = one query block (64 rows), 4 warps x 16 rows. smem: Q, dO, K, V tiles.
+template <int D>
+__global__ void __launch_bounds__(128) bwd_dq_kernel(const BwdParams p) {
+  extern __shared__ __align__(128) uint8_t smem_bw[];
+  constexpr int TB = 64 * D * 2;
+  uint8_t* sQ = smem_bw;
+  uint8_t* sO = smem_bw + TB;  // dO
+  uint8_t* sK = smem_bw + 2 * TB;
+  uint8_t* sV = smem_bw + 3 * TB;
+  const int bh = blockIdx.y, x = blockIdx.x;
+  const int hh = bh % p.H, bb = bh / p.H;
+  const bool is_flat = x >= p.n_sharp;
+  const int f = x - p.n_sharp;
+  const int u = is_flat ? p.flat[bh * p.n_flat + f] : p.sharp[bh * p.n_sharp + x];
+  const int tok = bw_tok0(p, u), vq = bw_valid(p, u);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  load_tile<D>(sQ, p.q + bb * p.sb + hh * p.sh + tok * p.ss, p.ss, vq);
+  load_tile<D>(sO, p.dout + bb * p.db + hh * p.dh + tok * p.ds, p.ds, vq);
+  const int r0 = warp * 16 + g, r1 = r0 + 8;
+  const long long rowbase = (long long)bh * p.S + tok;
+  const float lse0 = r0 < vq ? p.lse[rowbase + r0] : 0.f, lse1 = r1 < vq ? p.lse[rowbase + r1] : 0.f;
+  const float rho0 = r0 < vq ? p.rho[rowbase + r0] : 0.f, rho1 = r1 < vq ? p.rho[rowbase + r1] : 0.f;
+  float acc[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+  const uint32_t bq = smem_u32(sQ), bo = smem_u32(sO), bk = smem_u32(sK), bv = smem_u32(sV);
+  const int n_exact = is_flat ? p.k : p.t_new;
+  const int n_cent = is_flat ? p.tn_pad / 64 : 0;
+  const uint32_t* mb = is_flat ? p.bits + ((long long)bh * p.n_flat + f) * p.W : nullptr;
+  for (int it = 0; it < n_exact + n_cent; ++it) {
+    const bool cent = it >= n_exact;
+    int vk = 64, j0 = 0;
+    __syncthreads();  // previous K/V consumed
+    if (!cent) {
+      const int j = is_flat ? p.mask[((long long)bh * p.n_flat + f) * p.k + it] : it;
+      const int uk = p.kv_blk[(long long)bh * p.t_new + j];
+      vk = bw_valid(p, uk);
+      const long long off = bb * p.sb + hh * p.sh + (long long)bw_tok0(p, uk) * p.ss;
+      load_tile<D>(sK, p.kx + off, p.ss, vk);
+      load_tile<D>(sV, p.v + off, p.ss, vk);
+    } else {
+      j0 = (it - n_exact) * 64;
+      const long long off = ((long long)bh * p.tn_pad + j0) * D;
+      load_tile<D>(sK, p.kc + off, D, 64);
+      load_tile<D>(sV, p.vc + off, D, 64);
+    }
+    __syncthreads();
+    // S = Q K^T and dP = dO V^T for this warp's 16 rows x 64 keys
+    float sc[8][4], dp[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[n][e] = dp[n][e] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      uint32_t aq[4], ao[4];
+      frag_a<D>(aq, bq, warp * 16, kk * 16);
+      frag_a<D>(ao, bo, warp * 16, kk * 16);
+#pragma unroll
+      for (int n = 0; n < 8; n += 2) {
+        uint32_t b[4];
+        frag_b<D>(b, bk, n * 8, kk * 16);
+        mma16816(sc[n], aq, b[0], b[1]);
+        mma16816(sc[n + 1], aq, b[2], b[3]);
+        frag_b<D>(b, bv, n * 8, kk * 16);
+        mma16816(dp[n], ao, b[0], b[1]);
+        mma16816(dp[n + 1], ao, b[2], b[3]);
+      }
+    }
+    // P and dS = P * (dP - rho); pack dS as the A operand of dQ += dS K
+    uint32_t ads[4][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      float dsv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int col = n * 8 + tig * 2 + (e & 1);
+        const bool hi = e >= 2;
+        float bias = 0.f;
+        bool ok;
+        if (!cent) {
+          ok = col < vk;
+        } else {
+          const int jj = j0 + col;  // taylor.py:153-156: members excluded, weight = valid rows
+          ok = jj < p.t_new && !((mb[jj >> 5] >> (jj & 31)) & 1u);
+          if (ok) bias = __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + jj]));
+        }
+        const float lse = hi ? lse1 : lse0, rh = hi ? rho1 : rho0;
+        const float pr = (ok && lse > -INFINITY) ? exp2f(fmaf(sc[n][e], p.sl2, bias - lse)) : 0.f;
+        dsv[e] = pr * (dp[n][e] - rh);
+      }
+      const int kk = n >> 1;
+      if ((n & 1) == 0) {
+        ads[kk][0] = pack_bf16x2(dsv[0], dsv[1]);
+        ads[kk][1] = pack_bf16x2(dsv[2], dsv[3]);
+      } else {
+        ads[kk][2] = pack_bf16x2(dsv[0], dsv[1]);
+        ads[kk][3] = pack_bf16x2(dsv[2], dsv[3]);
+      }
+    }
+    // dQ += dS K  (K as [k=key][n=d])
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int n = 0; n < D / 8; n += 2) {
+        uint32_t b[4];
+        frag_bt<D>(b, bk, kk * 16, n * 8);
+        mma16816(acc[n], ads[kk], b[0], b[1]);
+        mma16816(acc[n + 1], ads[kk], b[2], b[3]);
+      }
+  }
+  // dQ = scale * acc at the block's original rows
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n) {
+    const int col = n * 8 + tig * 2;
+    if (r0 < vq) {
+      float* dst = p.dq + (rowbase + r0) * D + col;
+      dst[0] = p.scale * acc[n][0];
+      dst[1] = p.scale * acc[n][1];
+    }
+    if (r1 < vq) {
+      float* dst = p.dq + (rowbase + r1) * D + col;
+      dst[0] = p.scale * acc[n][2];
+      dst[1] = p.scale * acc[n][3];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- dK/dV (key-major)
+// CTA = 64 keys (a K_new block, or a tile of 64 centroids), 4 warps x 16 keys;
+// loops over the query blocks that see those keys.
+template <int D, int CENTROID>
+__global__ void __launch_bounds__(128) bwd_dkv_kernel(const BwdParams p) {
+  extern __shared__ __align__(128) uint8_t smem_bw[];
+  constexpr int TB = 64 * D * 2;
+  uint8_t* sK = smem_bw;
+  uint8_t* sV = smem_bw + TB;
+  uint8_t* sQ = smem_bw + 2 * TB;
+  uint8_t* sO = smem_bw + 3 * TB;
+  float* sLse = reinterpret_cast<float*>(smem_bw + 4 * TB);
+  float* sRho = sLse + 64;
+  int* sList = reinterpret_cast<int*>(sRho + 64);  // query-block list (positions), up to n_sharp + n_flat
+  __shared__ int s_count;
+  const int bh = blockIdx.y;
+  const int hh = bh % p.H, bb = bh / p.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  int vk = 64, uk = 0, j = 0, c0 = 0;
+  if (!CENTROID) {
+    j = blockIdx.x;
+    uk = p.kv_blk[(long long)bh * p.t_new + j];
+    vk = bw_valid(p, uk);
+    const long long off = bb * p.sb + hh * p.sh + (long long)bw_tok0(p, uk) * p.ss;
+    load_tile<D>(sK, p.kx + off, p.ss, vk);
+    load_tile<D>(sV, p.v + off, p.ss, vk);
+  } else {
+    c0 = blockIdx.x * 64;
+    const long long off = ((long long)bh * p.tn_pad + c0) * D;
+    load_tile<D>(sK, p.kc + off, D, 64);
+    load_tile<D>(sV, p.vc + off, D, 64);
+  }
+  // query blocks: [sharp ...] (exact only) then the flat ones (exact: listing j; centroid: all)
+  if (threadIdx.x == 0) s_count = 0;
+  __syncthreads();
+  if (!CENTROID)
+    for (int x = threadIdx.x; x < p.n_sharp; x += 128) sList[x] = x;
+  const int base = CENTROID ? 0 : p.n_sharp;
+  for (int f = threadIdx.x; f < p.n_flat; f += 128) {
+    bool take = true;
+    if (!CENTROID) take = (p.bits[((long long)bh * p.n_flat + f) * p.W + (j >> 5)] >> (j & 31)) & 1u;
+    if (take) sList[base + atomicAdd(&s_count, 1)] = p.n_sharp + f;
+  }
+  __syncthreads();
+  const int n_list = base + s_count;
+  // per-key bias (log2 of the centroid weight) and validity for this warp's rows
+  const int kr0 = warp * 16 + g, kr1 = kr0 + 8;
+  float kb0 = 0.f, kb1 = 0.f;
+  bool kv0 = kr0 < vk, kv1 = kr1 < vk;
+  if (CENTROID) {
+    kv0 = c0 + kr0 < p.t_new;
+    kv1 = c0 + kr1 < p.t_new;
+    if (kv0) kb0 = __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + c0 + kr0]));
+    if (kv1) kb1 = __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + c0 + kr1]));
+  }
+  float dk[D / 8][4], dv[D / 8][4];
+#pragma unroll
+  for (int n = 0; n < D / 8; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dk[n][e] = dv[n][e] = 0.f;
+  const uint32_t bq = smem_u32(sQ), bo = smem_u32(sO), bk = smem_u32(sK), bvv = smem_u32(sV);
+  for (int li = 0; li < n_list; ++li) {
+    const int x = sList[li];
+    const bool is_flat = x >= p.n_sharp;
+    const int f = x - p.n_sharp;
+    const int u = is_flat ? p.flat[bh * p.n_flat + f] : p.sharp[bh * p.n_sharp + x];
+    const int tok = bw_tok0(p, u), vq = bw_valid(p, u);
+    const long long rowbase = (long long)bh * p.S + tok;
+    __syncthreads();  // previous Q/dO consumed
+    load_tile<D>(sQ, p.q + bb * p.sb + hh * p.sh + tok * p.ss, p.ss, vq);
+    load_tile<D>(sO, p.dout + bb * p.db + hh * p.dh + tok * p.ds, p.ds, vq);
+    if (threadIdx.x < 64) {
+      const int r = threadIdx.x;
+      sLse[r] = r < vq ? p.lse[rowbase + r] : -INFINITY;
+      sRho[r] = r < vq ? p.rho[rowbase + r] : 0.f;
+    }
+    __syncthreads();
+    const uint32_t* mb = (CENTROID && is_flat) ? p.bits + ((long long)bh * p.n_flat + f) * p.W : nullptr;
+    // S^T = K Q^T, dP^T = V dO^T (16 keys x 64 queries per warp)
+    float sc[8][4], dp[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[n][e] = dp[n][e] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      uint32_t ak[4], av[4];
+      frag_a<D>(ak, bk, warp * 16, kk * 16);
+      frag_a<D>(av, bvv, warp * 16, kk * 16);
+#pragma unroll
+      for (int n = 0; n < 8; n += 2) {
+        uint32_t b[4];
+        frag_b<D>(b, bq, n * 8, kk * 16);
+        mma16816(sc[n], ak, b[0], b[1]);
+        mma16816(sc[n + 1], ak, b[2], b[3]);
+        frag_b<D>(b, bo, n * 8, kk * 16);
+        mma16816(dp[n], av, b[0], b[1]);
+        mma16816(dp[n + 1], av, b[2], b[3]);
+      }
+    }
+    uint32_t ap[4][4], ads[4][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      float pv[4], dsv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int q = n * 8 + tig * 2 + (e & 1);
+        const bool hi = e >= 2;
+        bool ok = (hi ? kv1 : kv0) && q < vq;
+        if (CENTROID && ok) {
+          const int jj = c0 + (hi ? kr1 : kr0);
+          ok = !((mb[jj >> 5] >> (jj & 31)) & 1u);
+        }
+        const float lse = sLse[q];
+        const float pr = (ok && lse > -INFINITY) ? exp2f(fmaf(sc[n][e], p.sl2, (hi ? kb1 : kb0) - lse)) : 0.f;
+        pv[e] = pr;
+        dsv[e] = pr * (dp[n][e] - sRho[q]);
+      }
+      const int kk = n >> 1;
+      const int o = (n & 1) ? 2 : 0;
+      ap[kk][o] = pack_bf16x2(pv[0], pv[1]);
+      ap[kk][o + 1] = pack_bf16x2(pv[2], pv[3]);
+      ads[kk][o] = pack_bf16x2(dsv[0], dsv[1]);
+      ads[kk][o + 1] = pack_bf16x2(dsv[2], dsv[3]);
+    }
+    // dV += P^T dO, dK += dS^T Q (B operands as [k=query][n=d])
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int n = 0; n < D / 8; n += 2) {
+        uint32_t b[4];
+        frag_bt<D>(b, bo, kk * 16, n * 8);
+        mma16816(dv[n], ap[kk], b[0], b[1]);
+        mma16816(dv[n + 1], ap[kk], b[2], b[3]);
+        frag_bt<D>(b, bq, kk * 16, n * 8);
+        mma16816(dk[n], ads[kk], b[0], b[1]);
+        mma16816(dk[n + 1], ads[kk], b[2], b[3]);
+      }
+  }
+  // stores
+  if (CENTROID) {
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      const int col = n * 8 + tig * 2;
+      if (kv0) {
+        const long long o = ((long long)bh * p.t_new + c0 + kr0) * D + col;
+        p.dkc[o] = p.scale * dk[n][0];
+        p.dkc[o + 1] = p.scale * dk[n][1];
+        p.dvc[o] = dv[n][0];
+        p.dvc[o + 1] = dv[n][1];
+      }
+      if (kv1) {
+        const long long o = ((long long)bh * p.t_new + c0 + kr1) * D + col;
+        p.dkc[o] = p.scale * dk[n][2];
+        p.dkc[o + 1] = p.scale * dk[n][3];
+        p.dvc[o] = dv[n][2];
+        p.dvc[o + 1] = dv[n][3];
+      }
+    }
+  } else {
+    // + block-mean adjoint of the centroid gradients (taylor.py:290-292), then
+    // the K_new gather adjoint: rows go back to the block's original positions
+    const float invw = 1.f / (float)vk;
+    const long long cb = ((long long)bh * p.t_new + j) * D;
+    const long long rowbase = (long long)bh * p.S + bw_tok0(p, uk);
+#pragma unroll
+    for (int n = 0; n < D / 8; ++n) {
+      const int col = n * 8 + tig * 2;
+      float ck0 = 0.f, ck1 = 0.f, cv0 = 0.f, cv1 = 0.f;
+      if (p.n_flat) {
+        ck0 = p.dkc[cb + col] * invw;
+        ck1 = p.dkc[cb + col + 1] * invw;
+        cv0 = p.dvc[cb + col] * invw;
+        cv1 = p.dvc[cb + col + 1] * invw;
+      }
+      if (kv0) {
+        const long long o = (rowbase + kr0) * D + col;
+        p.dk[o] = p.scale * dk[n][0] + ck0;
+        p.dk[o + 1] = p.scale * dk[n][1] + ck1;
+        p.dv[o] = dv[n][0] + cv0;
+        p.dv[o + 1] = dv[n][1] + cv1;
+      }
+      if (kv1) {
+        const long long o = (rowbase + kr1) * D + col;
+        p.dk[o] = p.scale * dk[n][2] + ck0;
+        p.dk[o + 1] = p.scale * dk[n][3] + ck1;
+        p.dv[o] = dv[n][2] + cv0;
+        p.dv[o + 1] = dv[n][3] + cv1;
+      }
+    }
+  }
+}
+
+}  // namespace isa

@@ -25,6 +25,7 @@
 #include "../../include/isa_b200.h"
 #include "isa_attn.cuh"
 #include "isa_attn_p2.cuh"
+#include "isa_bwd.cuh"
 #include "isa_route.cuh"
 
 namespace {
@@ -675,19 +676,16 @@ int isa_routing(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
                      static_cast<cudaStream_t>(stream));
 }
 
-int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v, void* out,
-                void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
-                int32_t* err_word, const IsaEvents* events, void* stream) {
-  g_launches = 0;
-  Dims d;
-  int rc = derive(shape, knobs, &d);
-  if (rc) return rc;
-  if ((rc = check_io(shape, q, k, v))) return rc;
-  if ((rc = check_out(shape, out))) return rc;
-  Workspace w = carve(d, shape->dtype, static_cast<uint8_t*>(workspace));
-  if (!workspace || workspace_bytes < w.bytes)
-    return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, w.bytes);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+}  // extern "C"
+
+namespace {
+
+// Stages 1-5 into `out`; `lse` (nullable, [BH][S] fp32) receives the per-row
+// log2-domain softmax normaliser for the backward.
+int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, const void* q, const void* k,
+                 const void* v, void* out, const Workspace& w, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
+                 int32_t* err_word, const IsaEvents* events, float* lse, cudaStream_t st) {
+  int rc;
   record(events, 0, st);
   if ((rc = run_routing(shape, d, knobs, q, k, v, w, pinned, routing, err_word, events, st))) return rc;
   // ---- stage 4 (+ fused stage 5)
@@ -709,6 +707,8 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
   p.resid = w.resid;  // null unless gamma > 0
   p.gamma = static_cast<float>(d.gamma);
   p.T = d.T;
+  p.lse = lse;
+  p.S = d.S;
   isa::AttnParams ps = p;
   ps.n_qblk = d.n_sharp;
   ps.qlist = w.sharp;
@@ -747,6 +747,159 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
   }
   record(events, 5, st);
   return ISA_OK;
+}
+
+// Backward workspace: forward workspace, then O (bf16), lse, rho, dkc, dvc.
+struct BwdWs {
+  Workspace fw;
+  __nv_bfloat16* o;
+  float *lse, *rho, *dkc, *dvc;
+  size_t bytes;
+};
+
+BwdWs carve_bwd(const Dims& d, uint8_t* base) {
+  BwdWs b{};
+  b.fw = carve(d, ISA_DTYPE_BF16, base);
+  size_t off = b.fw.bytes;
+  auto take = [&](size_t n) {
+    uint8_t* p = base ? base + off : nullptr;
+    off += align256(n ? n : 1);
+    return p;
+  };
+  const long long BH = d.BH;
+  b.o = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.S * d.D));
+  b.lse = reinterpret_cast<float*>(take(4ull * BH * d.S));
+  b.rho = reinterpret_cast<float*>(take(4ull * BH * d.S));
+  b.dkc = reinterpret_cast<float*>(take(4ull * BH * d.t_new * d.D));
+  b.dvc = reinterpret_cast<float*>(take(4ull * BH * d.t_new * d.D));
+  b.bytes = off;
+  return b;
+}
+
+template <int D>
+int launch_bwd(const isa::BwdParams& bp, const Dims& d, cudaStream_t st) {
+  const size_t tiles = 4ull * 64 * D * 2;
+  const size_t sm_dkv = tiles + 2 * 64 * 4 + 4ull * (d.n_sharp + d.n_flat);
+  static size_t cur_dq = 48 * 1024, cur_e = 48 * 1024, cur_c = 48 * 1024;
+  int rc;
+  if ((rc = ensure_smem((const void*)isa::bwd_dq_kernel<D>, tiles, &cur_dq))) return rc;
+  if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 0>, sm_dkv, &cur_e))) return rc;
+  if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 1>, sm_dkv, &cur_c))) return rc;
+  if (d.n_flat) {
+    isa::bwd_dkv_kernel<D, 1><<<dim3(d.tn_pad / 64, d.BH), 128, sm_dkv, st>>>(bp);
+    ISA_LAUNCHED("bwd_dkv_kernel<centroid>");
+  }
+  isa::bwd_dkv_kernel<D, 0><<<dim3(d.t_new, d.BH), 128, sm_dkv, st>>>(bp);
+  ISA_LAUNCHED("bwd_dkv_kernel<exact>");
+  isa::bwd_dq_kernel<D><<<dim3(d.n_sharp + d.n_flat, d.BH), 128, tiles, st>>>(bp);
+  ISA_LAUNCHED("bwd_dq_kernel");
+  return ISA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v, void* out,
+                void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
+                int32_t* err_word, const IsaEvents* events, void* stream) {
+  g_launches = 0;
+  Dims d;
+  int rc = derive(shape, knobs, &d);
+  if (rc) return rc;
+  if ((rc = check_io(shape, q, k, v))) return rc;
+  if ((rc = check_out(shape, out))) return rc;
+  Workspace w = carve(d, shape->dtype, static_cast<uint8_t*>(workspace));
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, w.bytes);
+  return forward_impl(shape, knobs, d, q, k, v, out, w, pinned, routing, err_word, events, nullptr,
+                      static_cast<cudaStream_t>(stream));
+}
+
+int isa_backward_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* bytes) {
+  Dims d;
+  int rc = derive(shape, knobs, &d);
+  if (rc) return rc;
+  if (!bytes) return fail(ISA_ERR_CONFIG, "null bytes");
+  *bytes = carve_bwd(d, nullptr).bytes;
+  return ISA_OK;
+}
+
+int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
+                 const void* dout, float* dq, float* dk, float* dv, void* workspace, size_t workspace_bytes,
+                 const IsaRoutingIn* pinned, int32_t* err_word, void* stream) {
+  g_launches = 0;
+  Dims d;
+  int rc = derive(shape, knobs, &d);
+  if (rc) return rc;
+  if (shape->dtype != ISA_DTYPE_BF16) return fail(ISA_ERR_CONFIG, "isa_backward takes bf16 q/k/v/dO");
+  if (d.gamma > 0.0) return fail(ISA_ERR_CONFIG, "isa_backward: gamma > 0 is not implemented");
+  if ((rc = check_io(shape, q, k, v))) return rc;
+  if ((rc = check_io(shape, dout, dout, dout))) return rc;
+  if (!dq || !dk || !dv) return fail(ISA_ERR_LAYOUT, "null gradient buffers");
+  BwdWs b = carve_bwd(d, static_cast<uint8_t*>(workspace));
+  if (!workspace || workspace_bytes < b.bytes)
+    return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, b.bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // forward recompute with the softmax statistics (routing frozen by determinism or `pinned`)
+  IsaShape os = *shape;
+  os.out_stride_b = os.out_stride_h = os.out_stride_s = 0;  // O into the workspace, contiguous
+  if ((rc = forward_impl(&os, knobs, d, q, k, v, b.o, b.fw, pinned, nullptr, err_word, nullptr, b.lse, st)))
+    return rc;
+  int launches = g_launches;
+  const size_t gbytes = 4ull * d.BH * d.S * d.D;
+  ISA_CUDA(cudaMemsetAsync(dk, 0, gbytes, st));  // rows of unselected context blocks get no gradient
+  ISA_CUDA(cudaMemsetAsync(dv, 0, gbytes, st));
+  const long long n_rows = (long long)d.BH * d.S;
+  isa::bwd_rho_kernel<<<grid1d(n_rows * 32, 256), 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(dout), shape->stride_b, shape->stride_h, shape->stride_s, b.o, d.H, d.S, d.D,
+      b.rho, n_rows);
+  ++launches;
+  ISA_CUDA(cudaGetLastError());
+  isa::BwdParams bp{};
+  bp.H = d.H;
+  bp.S = d.S;
+  bp.D = d.D;
+  bp.l_src = d.l_src;
+  bp.l_ctx = d.l_ctx;
+  bp.t_src = d.t_src;
+  bp.t_ctx = d.t_ctx;
+  bp.t_new = d.t_new;
+  bp.n_sharp = d.n_sharp;
+  bp.n_flat = d.n_flat;
+  bp.k = d.k;
+  bp.W = d.W;
+  bp.tn_pad = d.tn_pad;
+  bp.sl2 = static_cast<float>(d.scale * 1.4426950408889634);
+  bp.scale = static_cast<float>(d.scale);
+  bp.q = static_cast<const __nv_bfloat16*>(q);
+  bp.kx = static_cast<const __nv_bfloat16*>(k);
+  bp.v = static_cast<const __nv_bfloat16*>(v);
+  bp.dout = static_cast<const __nv_bfloat16*>(dout);
+  bp.sb = shape->stride_b;
+  bp.sh = shape->stride_h;
+  bp.ss = shape->stride_s;
+  bp.db = shape->stride_b;
+  bp.dh = shape->stride_h;
+  bp.ds = shape->stride_s;
+  bp.lse = b.lse;
+  bp.rho = b.rho;
+  bp.sharp = b.fw.sharp;
+  bp.flat = b.fw.flat;
+  bp.mask = b.fw.mask;
+  bp.kv_blk = b.fw.kv_blk;
+  bp.bits = b.fw.bits;
+  bp.kc = b.fw.kc_bf;
+  bp.vc = b.fw.vc_bf;
+  bp.dkc = b.dkc;
+  bp.dvc = b.dvc;
+  bp.dq = dq;
+  bp.dk = dk;
+  bp.dv = dv;
+  g_launches = 0;
+  rc = d.D == 128 ? launch_bwd<128>(bp, d, st) : launch_bwd<64>(bp, d, st);
+  g_launches += launches;
+  return rc;
 }
 
 int isa_dense_attention(const IsaShape* shape, double scale, const void* q, const void* k, const void* v, void* out,

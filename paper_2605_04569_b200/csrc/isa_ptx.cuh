@@ -364,10 +364,16 @@ __device__ __forceinline__ float2 ex2_emu2(float2 x) {
   x.y = fmaxf(x.y, -127.f);
   const float2 r = fadd2_rm(x, make_float2(kRound, kRound));
   const float2 f = fsub2(x, fsub2(r, make_float2(kRound, kRound)));
+#ifdef ISA_EMU_DEG2
+  // degree-2 minimax (max relative error 2.1e-3, about half a bf16 ulp)
+  float2 p = ffma2(make_float2(0.3299208f, 0.3299208f), f, make_float2(0.66596746f, 0.66596746f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+#else
   float2 p = ffma2(make_float2(0.0770670473575592f, 0.0770670473575592f), f,
                    make_float2(0.22764497995376587f, 0.22764497995376587f));
   p = ffma2(p, f, make_float2(0.6951168179512024f, 0.6951168179512024f));
   p = ffma2(p, f, make_float2(1.f, 1.f));
+#endif
   float2 o;
   o.x = __int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23));
   o.y = __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23));

@@ -32,6 +32,7 @@ from . import _native as N
 from .errors import ConfigError, DegenerateRowError, InputError, LayoutError
 from .types import (
     BlockMask,
+    GradBundle,
     IclLayout,
     IsaConfig,
     IsaDims,
@@ -45,7 +46,7 @@ from .types import (
     icl_from_any,
 )
 
-__all__ = ["isa_forward", "isa_routing", "isa_forward_with_routing", "dense_attention", "prepare",
+__all__ = ["isa_forward", "isa_routing", "isa_forward_with_routing", "isa_backward", "dense_attention", "prepare",
            "apply_decoupled_rope"]
 
 
@@ -393,6 +394,47 @@ def isa_forward_with_routing(q, k, v, icl: IclLayout, cfg: IsaConfig, routing) -
     IsaRouting or the reference's (numpy index arrays)."""
     res, _, _ = _run(_Inputs(q, k, v, icl, cfg), False, pinned=routing)
     return res
+
+
+def isa_backward(q, k, v, icl: IclLayout, cfg: IsaConfig, do, *, routing=None) -> GradBundle:
+    """Gradients of isa_forward with routing frozen at this forward's decisions
+    (pipeline.py:373-466, same signature; gamma = 0). `routing` optionally pins
+    the decisions (ours or the reference's IsaRouting). Computes in bf16 tensor
+    arithmetic with fp32 accumulation; returns tensors in q's dtype (numpy fp32
+    for numpy inputs)."""
+    numpy_io = isinstance(q, np.ndarray)
+    inp = _Inputs(q, k, v, icl, cfg)
+    if inp.host:
+        inp = _Inputs(*(t.cuda() for t in (inp.q, inp.k, inp.v)), icl, cfg)
+    out_dtype = inp.q.dtype
+    if inp.q.dtype != torch.bfloat16:  # the backward kernels take bf16 operands
+        inp = _Inputs(*(t.to(torch.bfloat16) for t in (inp.q, inp.k, inp.v)), icl, cfg)
+    d = inp.dims
+    if isinstance(do, np.ndarray):
+        do = torch.from_numpy(np.ascontiguousarray(do, dtype=np.float32))
+    if not isinstance(do, torch.Tensor) or tuple(do.shape) != (d.B, d.H, d.S, d.D):
+        raise LayoutError(f"dO shape {tuple(getattr(do, 'shape', ()))} != output shape {(d.B, d.H, d.S, d.D)}")
+    do = do.to(device=inp.q.device, dtype=torch.bfloat16)
+    if do.stride() != inp.q.stride():
+        do = torch.empty_strided(inp.q.shape, inp.q.stride(), dtype=torch.bfloat16, device=inp.q.device).copy_(do)
+    lib = N.load()
+    nbytes = ctypes.c_size_t(0)
+    N.check(lib.isa_backward_workspace_bytes(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), ctypes.byref(nbytes)))
+    ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=inp.q.device)
+    grads = [torch.empty((d.B, d.H, d.S, d.D), dtype=torch.float32, device=inp.q.device) for _ in range(3)]
+    err = torch.zeros(1, dtype=torch.int32, device=inp.q.device)
+    pin_struct, keep = (None, None)
+    if routing is not None:
+        pin_struct, keep = _pinned_struct(routing, d, inp.q.device)
+    N.check(lib.isa_backward(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), _ptr(inp.q), _ptr(inp.k),
+                             _ptr(inp.v), _ptr(do), *(_ptr(g) for g in grads), _ptr(ws), nbytes.value,
+                             ctypes.byref(pin_struct) if pin_struct else None, _ptr(err),
+                             torch.cuda.current_stream(inp.q.device).cuda_stream))
+    _raise_flags(err)
+    del keep
+    if numpy_io:
+        return GradBundle(*(g.cpu().numpy() for g in grads))
+    return GradBundle(*(g.to(out_dtype) for g in grads))
 
 
 def dense_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: Optional[float] = None,

@@ -37,6 +37,15 @@ SUPPORTED_HEAD_DIMS = (64, 128)
 
 
 @dataclass
+class GradBundle:
+    """Gradients w.r.t. the attention primals; dims match Q/K/V (reference.py:20-25)."""
+
+    dq: object
+    dk: object
+    dv: object
+
+
+@dataclass
 class IsaConfig:
     """Sparsity knobs and behavioral flags (pipeline.py:51-71, same defaults)."""
 

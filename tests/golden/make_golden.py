@@ -124,8 +124,40 @@ def make_rope(name, B, H, l_src, l_ctx, D, base, seed):
     print(f"{name}: {x.shape}, {rows.size} rows stored")
 
 
+BWD_CASES = [
+    # name, kind, B, H, S, D, l_src, l_ctx, seed, cfg overrides
+    ("bwd_cfg1_iid_s20", "iid-gaussian", 1, 2, 2048, 64, 1024, 1024, 20, {}),
+    ("bwd_clustered_d128_s21", "clustered", 1, 1, 2048, 128, 1024, 1024, 21, {}),
+    ("bwd_ragged_s22", "iid-gaussian", 1, 2, 1500, 64, 900, 600, 22, {"strict": False, "alpha_s": 0.5}),
+    ("bwd_knobs_s23", "lowrank", 2, 1, 2048, 64, 1024, 1024, 23, {"alpha_f": 0.75, "alpha_ns": 0.25}),
+]
+
+
+def make_bwd(name, kind, B, H, S, D, l_src, l_ctx, seed, over):
+    """Golden gradients of the reference isa_backward (pipeline.py:373-466). dO is
+    regenerated from the seed (numpy default_rng) and pinned by its checksum."""
+    spec = isattn.WorkloadSpec(batch=B, heads=H, seq_len=S, dim=D, l_src=l_src, l_ctx=l_ctx, kind=kind, seed=seed)
+    q, k, v, icl = isattn.generate(spec)
+    q, k, v = (round_bf16(x) for x in (q, k, v))
+    do = round_bf16(np.random.default_rng(seed).standard_normal((B, H, S, D)).astype(np.float32))
+    cfg = isattn.IsaConfig(**over)
+    t0 = time.perf_counter()
+    g = isattn.isa_backward(q, k, v, icl, cfg, do)
+    t = time.perf_counter() - t0
+    meta = {"name": name, "kind": kind, "B": B, "H": H, "S": S, "D": D, "l_src": l_src, "l_ctx": l_ctx,
+            "seed": seed, "cfg": over, "ref_backward_seconds": t,
+            "input_sums": [float(x.astype(np.float64).sum()) for x in (q, k, v, do)]}
+    np.savez_compressed(os.path.join(HERE, "bwd", f"{name}.npz"), meta=json.dumps(meta),
+                        dq=g.dq.astype(np.float32), dk=g.dk.astype(np.float32), dv=g.dv.astype(np.float32))
+    print(f"{name}: isa_backward {t:.2f}s")
+
+
 if __name__ == "__main__":
     only = set(sys.argv[1:])
+    os.makedirs(os.path.join(HERE, "bwd"), exist_ok=True)
+    for case in BWD_CASES:
+        if not only or case[0] in only:
+            make_bwd(*case)
     for case in CASES:
         if not only or case[0] in only:
             make_case(*case)

@@ -1,0 +1,67 @@
+"""isa_backward (pipeline.py:373-466) vs golden gradients of the reference
+(tests/golden/bwd/*.npz, made by tests/golden/make_golden.py from `isattn`).
+bf16 tensor arithmetic with fp32 accumulation: per tensor cosine >= 0.999 and
+max-abs error <= 3e-2 x max |reference gradient|."""
+
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import isa_oracle as O
+
+BWD_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "bwd")
+BWD_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(BWD_DIR, "*.npz")))
+
+
+def _case(name):
+    z = np.load(os.path.join(BWD_DIR, name + ".npz"))
+    m = json.loads(str(z["meta"]))
+    q, k, v = (O.round_bf16(x) for x in O.workload(m["kind"], m["B"], m["H"], m["S"], m["D"], m["seed"]))
+    do = O.round_bf16(np.random.default_rng(m["seed"]).standard_normal(q.shape).astype(np.float32))
+    sums = [float(x.astype(np.float64).sum()) for x in (q, k, v, do)]
+    assert np.allclose(sums, m["input_sums"], rtol=0, atol=1e-6 * max(1.0, max(abs(s) for s in sums)))
+    return m, (q, k, v, do), {n: z[n] for n in ("dq", "dk", "dv")}
+
+
+def test_backward_golden_inputs_regenerate():
+    for name in BWD_CASES:
+        _case(name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", BWD_CASES)
+def test_backward_vs_reference(name):
+    import torch
+
+    import paper_2605_04569_b200 as P
+
+    m, (q, k, v, do), ref = _case(name)
+    dev = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k, v, do)]
+    g = P.isa_backward(*dev[:3], P.IclLayout(m["l_src"], m["l_ctx"]), P.IsaConfig(**m["cfg"]), dev[3])
+    for n in ("dq", "dk", "dv"):
+        a = getattr(g, n).float().cpu().numpy().astype(np.float64).ravel()
+        b = ref[n].astype(np.float64).ravel()
+        err = float(np.max(np.abs(a - b)))
+        cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b) + 1e-300))
+        assert cos >= 0.999 and err <= 3e-2 * np.abs(b).max(), f"{n}: max_abs={err:.3e} (|ref|max {np.abs(b).max():.3e}) cos={cos:.6f}"
+
+
+@pytest.mark.gpu
+def test_backward_numpy_io_and_pinned_routing():
+    import torch
+
+    import paper_2605_04569_b200 as P
+
+    m, (q, k, v, do), ref = _case(BWD_CASES[0])
+    icl, cfg = P.IclLayout(m["l_src"], m["l_ctx"]), P.IsaConfig(**m["cfg"])
+    g = P.isa_backward(q, k, v, icl, cfg, do)
+    assert isinstance(g.dq, np.ndarray) and g.dq.dtype == np.float32
+    dev = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k, v, do)]
+    r = P.isa_routing(*dev[:3], icl, cfg)
+    g2 = P.isa_backward(*dev[:3], icl, cfg, dev[3], routing=r)
+    g3 = P.isa_backward(*dev[:3], icl, cfg, dev[3])
+    for n in ("dq", "dk", "dv"):
+        assert torch.equal(getattr(g2, n), getattr(g3, n))

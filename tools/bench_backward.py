@@ -1,0 +1,35 @@
+"""isa_backward at cfg3 (H=40, 32K+32K, D=128, bf16) on one B200: total time
+(forward recompute + gradients) and the backward-only part, CUDA events.
+FLOP convention: backward = 2.5 x the forward's algorithmic FLOPs (FA
+convention: 5 GEMMs vs 2; our two-kernel scheme recomputes S and dP once more,
+so it executes 7/2 x); reported as algorithmic TFLOP/s."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2605_04569_b200 as P
+
+H = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+L = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
+q, k, v, do = (torch.randn(1, H, 2 * L, 128, device="cuda").to(torch.bfloat16) for _ in range(4))
+icl, cfg = P.IclLayout(L, L), P.IsaConfig()
+P.isa_backward(q, k, v, icl, cfg, do)
+prep = P.prepare(q, k, v, icl, cfg)
+prep()
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(2):
+    P.isa_backward(q, k, v, icl, cfg, do)
+b.record()
+torch.cuda.synchronize()
+bwd = a.elapsed_time(b) / 2
+a.record()
+for _ in range(2):
+    prep()
+b.record()
+torch.cuda.synchronize()
+fwd = a.elapsed_time(b) / 2
+f = P.IsaDims.derive(q.shape, icl, cfg).flops()
+fl = 2.5 * (f.exact_mas + f.taylor_mas)
+print(json.dumps({"workload": f"isa_backward H={H} {L}+{L} D=128 bf16", "backward_total_ms": bwd, "forward_ms": fwd,
+                  "gradient_kernels_ms": bwd - fwd, "alg_tflops_gradients": fl / (bwd - fwd) / 1e9}))

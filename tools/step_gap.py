@@ -1,0 +1,41 @@
+"""Where does a bench step go? Per-step CUDA events around stages vs the
+back-to-back loop time (cfg3 by default)."""
+import os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2605_04569_b200 as P
+from paper_2605_04569_b200 import _native as N
+from bench import _call_with_events
+
+H, L = 40, 32768
+q, k, v = (torch.randn(1, H, 2 * L, 128, device="cuda").to(torch.bfloat16) for _ in range(3))
+prep = P.prepare(q, k, v, P.IclLayout(L, L), P.IsaConfig())
+for _ in range(3):
+    prep()
+torch.cuda.synchronize()
+n = 10
+evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(n)]
+structs = []
+for i in range(n):
+    s = N.IsaEvents()
+    for j, e in enumerate(evs[i]):
+        e.record()
+        s.ev[j] = e.cuda_event
+    structs.append(s)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for i in range(n):
+    _call_with_events(prep, structs[i], 0)
+b.record()
+torch.cuda.synchronize()
+tot = a.elapsed_time(b) / n
+inner = sum(evs[i][0].elapsed_time(evs[i][5]) for i in range(n)) / n
+gaps = [evs[i][5].elapsed_time(evs[i + 1][0]) for i in range(n - 1)]
+a.record()
+for i in range(n):
+    prep()
+b.record()
+torch.cuda.synchronize()
+print(json.dumps({"loop_ms_per_step_with_events": tot, "ev0_to_ev5_ms": inner, "gap_between_steps_ms": gaps,
+                  "loop_ms_per_step_plain": a.elapsed_time(b) / n}))

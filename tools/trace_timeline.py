@@ -18,7 +18,16 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-LIB = os.path.join(ROOT, "paper_2605_04569_b200", "libisa_b200_trace{}.so")
+_LIB = os.path.join(ROOT, "paper_2605_04569_b200", "libisa_b200_trace{}.so")
+
+
+class _Lib:
+    @staticmethod
+    def format(variant):  # file-name-safe variant tag (nvcc rejects ',' in output paths)
+        return _LIB.format(variant.replace(",", "_").replace("=", "_"))
+
+
+LIB = _Lib
 
 
 def build(cta, variant):
