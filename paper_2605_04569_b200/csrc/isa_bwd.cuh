@@ -94,6 +94,24 @@ __device__ __forceinline__ void load_tile(uint8_t* sm, const __nv_bfloat16* src,
   }
 }
 
+// Same tile load through cp.async (16-byte, zero-fill past `rows`); the
+// caller commits / waits the group.
+template <int D>
+__device__ __forceinline__ void load_tile_async(uint8_t* sm, const __nv_bfloat16* src, long long rs, int rows) {
+  constexpr int C = D / 8;
+  const uint32_t base = smem_u32(sm);
+  for (int e = threadIdx.x; e < 64 * C; e += 128) {
+    const int r = e / C, c = e % C;
+    const __nv_bfloat16* g = src + (r < rows ? r : 0) * rs + c * 8;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(SmTile<D>::addr(base, r, c)), "l"(g),
+                 "r"(r < rows ? 16 : 0)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // A fragments (16 rows from row0, 16 columns from col0) of a swizzled tile.
 template <int D>
 __device__ __forceinline__ void frag_a(uint32_t (&a)[4], uint32_t base, int row0, int col0) {
@@ -136,15 +154,17 @@ __global__ void bwd_rho_kernel(const __nv_bfloat16* __restrict__ dout, long long
 }
 
 // ---------------------------------------------------------------- dQ (query-major)
-// CTA = one query block (64 rows), 4 warps x 16 rows. smem: Q, dO, K, V tiles.
+// CTA = one query block (64 rows), 4 warps x 16 rows. smem: Q, dO, and a
+// double-buffered K/V tile pair (cp.async prefetch of tile i+1 under tile i),
+// plus per-buffer column biases (0 / log2(centroid weight) / -inf = excluded).
 template <int D>
-__global__ void __launch_bounds__(128) bwd_dq_kernel(const BwdParams p) {
+__global__ void __launch_bounds__(128, 2) bwd_dq_kernel(const BwdParams p) {
   extern __shared__ __align__(128) uint8_t smem_bw[];
   constexpr int TB = 64 * D * 2;
   uint8_t* sQ = smem_bw;
   uint8_t* sO = smem_bw + TB;  // dO
-  uint8_t* sK = smem_bw + 2 * TB;
-  uint8_t* sV = smem_bw + 3 * TB;
+  uint8_t* sKV = smem_bw + 2 * TB;  // [2 buffers][K, V]
+  float* sBias = reinterpret_cast<float*>(smem_bw + 6 * TB);  // [2][64]
   const int bh = blockIdx.y, x = blockIdx.x;
   const int hh = bh % p.H, bb = bh / p.H;
   const bool is_flat = x >= p.n_sharp;
@@ -152,37 +172,60 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const BwdParams p) {
   const int u = is_flat ? p.flat[bh * p.n_flat + f] : p.sharp[bh * p.n_sharp + x];
   const int tok = bw_tok0(p, u), vq = bw_valid(p, u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
-  load_tile<D>(sQ, p.q + bb * p.sb + hh * p.sh + tok * p.ss, p.ss, vq);
-  load_tile<D>(sO, p.dout + bb * p.db + hh * p.dh + tok * p.ds, p.ds, vq);
+  const int n_exact = is_flat ? p.k : p.t_new;
+  const int n_tiles = n_exact + (is_flat ? p.tn_pad / 64 : 0);
+  const uint32_t* mb = is_flat ? p.bits + ((long long)bh * p.n_flat + f) * p.W : nullptr;
+  // issue the loads of tile `it` into buffer `buf`
+  auto prefetch = [&](int it, int buf) {
+    uint8_t* sK = sKV + buf * 2 * TB;
+    uint8_t* sV = sK + TB;
+    if (it < n_exact) {
+      const int j = is_flat ? p.mask[((long long)bh * p.n_flat + f) * p.k + it] : it;
+      const int uk = p.kv_blk[(long long)bh * p.t_new + j];
+      const int vk = bw_valid(p, uk);
+      const long long off = bb * p.sb + hh * p.sh + (long long)bw_tok0(p, uk) * p.ss;
+      load_tile_async<D>(sK, p.kx + off, p.ss, vk);
+      load_tile_async<D>(sV, p.v + off, p.ss, vk);
+      if (threadIdx.x < 64) sBias[buf * 64 + threadIdx.x] = threadIdx.x < vk ? 0.f : -INFINITY;
+    } else {
+      const int j0 = (it - n_exact) * 64;
+      const long long off = ((long long)bh * p.tn_pad + j0) * D;
+      load_tile_async<D>(sK, p.kc + off, D, 64);
+      load_tile_async<D>(sV, p.vc + off, D, 64);
+      if (threadIdx.x < 64) {  // taylor.py:153-156: members excluded, weight = valid rows
+        const int jj = j0 + threadIdx.x;
+        float bias = -INFINITY;
+        if (jj < p.t_new && !((mb[jj >> 5] >> (jj & 31)) & 1u))
+          bias = __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + jj]));
+        sBias[buf * 64 + threadIdx.x] = bias;
+      }
+    }
+    cp_commit();
+  };
+  load_tile_async<D>(sQ, p.q + bb * p.sb + hh * p.sh + tok * p.ss, p.ss, vq);
+  load_tile_async<D>(sO, p.dout + bb * p.db + hh * p.dh + tok * p.ds, p.ds, vq);
+  cp_commit();
+  if (n_tiles > 0) prefetch(0, 0);
   const int r0 = warp * 16 + g, r1 = r0 + 8;
   const long long rowbase = (long long)bh * p.S + tok;
   const float lse0 = r0 < vq ? p.lse[rowbase + r0] : 0.f, lse1 = r1 < vq ? p.lse[rowbase + r1] : 0.f;
   const float rho0 = r0 < vq ? p.rho[rowbase + r0] : 0.f, rho1 = r1 < vq ? p.rho[rowbase + r1] : 0.f;
+  const bool ok0 = r0 < vq && lse0 > -INFINITY, ok1 = r1 < vq && lse1 > -INFINITY;
   float acc[D / 8][4];
 #pragma unroll
   for (int n = 0; n < D / 8; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
-  const uint32_t bq = smem_u32(sQ), bo = smem_u32(sO), bk = smem_u32(sK), bv = smem_u32(sV);
-  const int n_exact = is_flat ? p.k : p.t_new;
-  const int n_cent = is_flat ? p.tn_pad / 64 : 0;
-  const uint32_t* mb = is_flat ? p.bits + ((long long)bh * p.n_flat + f) * p.W : nullptr;
-  for (int it = 0; it < n_exact + n_cent; ++it) {
-    const bool cent = it >= n_exact;
-    int vk = 64, j0 = 0;
-    __syncthreads();  // previous K/V consumed
-    if (!cent) {
-      const int j = is_flat ? p.mask[((long long)bh * p.n_flat + f) * p.k + it] : it;
-      const int uk = p.kv_blk[(long long)bh * p.t_new + j];
-      vk = bw_valid(p, uk);
-      const long long off = bb * p.sb + hh * p.sh + (long long)bw_tok0(p, uk) * p.ss;
-      load_tile<D>(sK, p.kx + off, p.ss, vk);
-      load_tile<D>(sV, p.v + off, p.ss, vk);
+  const uint32_t bq = smem_u32(sQ), bo = smem_u32(sO);
+  for (int it = 0; it < n_tiles; ++it) {
+    const int buf = it & 1;
+    if (it + 1 < n_tiles) {
+      prefetch(it + 1, buf ^ 1);
+      cp_wait<1>();
     } else {
-      j0 = (it - n_exact) * 64;
-      const long long off = ((long long)bh * p.tn_pad + j0) * D;
-      load_tile<D>(sK, p.kc + off, D, 64);
-      load_tile<D>(sV, p.vc + off, D, 64);
+      cp_wait<0>();
     }
     __syncthreads();
+    const uint32_t bk = smem_u32(sKV + buf * 2 * TB), bv = bk + TB;
+    const float* bias = sBias + buf * 64;
     // S = Q K^T and dP = dO V^T for this warp's 16 rows x 64 keys
     float sc[8][4], dp[8][4];
 #pragma unroll
@@ -214,27 +257,13 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const BwdParams p) {
       for (int e = 0; e < 4; ++e) {
         const int col = n * 8 + tig * 2 + (e & 1);
         const bool hi = e >= 2;
-        float bias = 0.f;
-        bool ok;
-        if (!cent) {
-          ok = col < vk;
-        } else {
-          const int jj = j0 + col;  // taylor.py:153-156: members excluded, weight = valid rows
-          ok = jj < p.t_new && !((mb[jj >> 5] >> (jj & 31)) & 1u);
-          if (ok) bias = __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + jj]));
-        }
-        const float lse = hi ? lse1 : lse0, rh = hi ? rho1 : rho0;
-        const float pr = (ok && lse > -INFINITY) ? exp2f(fmaf(sc[n][e], p.sl2, bias - lse)) : 0.f;
-        dsv[e] = pr * (dp[n][e] - rh);
+        const float pr = (hi ? ok1 : ok0) ? exp2f(fmaf(sc[n][e], p.sl2, bias[col] - (hi ? lse1 : lse0))) : 0.f;
+        dsv[e] = pr * (dp[n][e] - (hi ? rho1 : rho0));
       }
       const int kk = n >> 1;
-      if ((n & 1) == 0) {
-        ads[kk][0] = pack_bf16x2(dsv[0], dsv[1]);
-        ads[kk][1] = pack_bf16x2(dsv[2], dsv[3]);
-      } else {
-        ads[kk][2] = pack_bf16x2(dsv[0], dsv[1]);
-        ads[kk][3] = pack_bf16x2(dsv[2], dsv[3]);
-      }
+      const int o = (n & 1) ? 2 : 0;
+      ads[kk][o] = pack_bf16x2(dsv[0], dsv[1]);
+      ads[kk][o + 1] = pack_bf16x2(dsv[2], dsv[3]);
     }
     // dQ += dS K  (K as [k=key][n=d])
 #pragma unroll
@@ -246,6 +275,7 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const BwdParams p) {
         mma16816(acc[n], ads[kk], b[0], b[1]);
         mma16816(acc[n + 1], ads[kk], b[2], b[3]);
       }
+    __syncthreads();  // buffer `buf` is refilled by the prefetch of tile it + 2
   }
   // dQ = scale * acc at the block's original rows
 #pragma unroll
@@ -266,18 +296,19 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const BwdParams p) {
 
 // ---------------------------------------------------------------- dK/dV (key-major)
 // CTA = 64 keys (a K_new block, or a tile of 64 centroids), 4 warps x 16 keys;
-// loops over the query blocks that see those keys.
+// loops over the query blocks that see those keys, Q/dO tiles double-buffered
+// with cp.async (plus per-buffer lse, rho and the centroid exclusion mask).
 template <int D, int CENTROID>
-__global__ void __launch_bounds__(128) bwd_dkv_kernel(const BwdParams p) {
+__global__ void __launch_bounds__(128, 2) bwd_dkv_kernel(const BwdParams p) {
   extern __shared__ __align__(128) uint8_t smem_bw[];
   constexpr int TB = 64 * D * 2;
   uint8_t* sK = smem_bw;
   uint8_t* sV = smem_bw + TB;
-  uint8_t* sQ = smem_bw + 2 * TB;
-  uint8_t* sO = smem_bw + 3 * TB;
-  float* sLse = reinterpret_cast<float*>(smem_bw + 4 * TB);
-  float* sRho = sLse + 64;
-  int* sList = reinterpret_cast<int*>(sRho + 64);  // query-block list (positions), up to n_sharp + n_flat
+  uint8_t* sQO = smem_bw + 2 * TB;  // [2 buffers][Q, dO]
+  float* sLse = reinterpret_cast<float*>(smem_bw + 6 * TB);  // [2][64]
+  float* sRho = sLse + 128;                                    // [2][64]
+  uint32_t* sMem = reinterpret_cast<uint32_t*>(sRho + 128);  // [2][2] centroid member words
+  int* sList = reinterpret_cast<int*>(sMem + 4);             // query-block list (positions)
   __shared__ int s_count;
   const int bh = blockIdx.y;
   const int hh = bh % p.H, bb = bh / p.H;
@@ -288,14 +319,15 @@ __global__ void __launch_bounds__(128) bwd_dkv_kernel(const BwdParams p) {
     uk = p.kv_blk[(long long)bh * p.t_new + j];
     vk = bw_valid(p, uk);
     const long long off = bb * p.sb + hh * p.sh + (long long)bw_tok0(p, uk) * p.ss;
-    load_tile<D>(sK, p.kx + off, p.ss, vk);
-    load_tile<D>(sV, p.v + off, p.ss, vk);
+    load_tile_async<D>(sK, p.kx + off, p.ss, vk);
+    load_tile_async<D>(sV, p.v + off, p.ss, vk);
   } else {
     c0 = blockIdx.x * 64;
     const long long off = ((long long)bh * p.tn_pad + c0) * D;
-    load_tile<D>(sK, p.kc + off, D, 64);
-    load_tile<D>(sV, p.vc + off, D, 64);
+    load_tile_async<D>(sK, p.kc + off, D, 64);
+    load_tile_async<D>(sV, p.vc + off, D, 64);
   }
+  cp_commit();
   // query blocks: [sharp ...] (exact only) then the flat ones (exact: listing j; centroid: all)
   if (threadIdx.x == 0) s_count = 0;
   __syncthreads();
@@ -309,39 +341,53 @@ __global__ void __launch_bounds__(128) bwd_dkv_kernel(const BwdParams p) {
   }
   __syncthreads();
   const int n_list = base + s_count;
-  // per-key bias (log2 of the centroid weight) and validity for this warp's rows
+  auto prefetch = [&](int li, int buf) {
+    const int x = sList[li];
+    const bool is_flat = x >= p.n_sharp;
+    const int f = x - p.n_sharp;
+    const int u = is_flat ? p.flat[bh * p.n_flat + f] : p.sharp[bh * p.n_sharp + x];
+    const int tok = bw_tok0(p, u), vq = bw_valid(p, u);
+    uint8_t* sQ = sQO + buf * 2 * TB;
+    load_tile_async<D>(sQ, p.q + bb * p.sb + hh * p.sh + tok * p.ss, p.ss, vq);
+    load_tile_async<D>(sQ + TB, p.dout + bb * p.db + hh * p.dh + tok * p.ds, p.ds, vq);
+    const long long rowbase = (long long)bh * p.S + tok;
+    if (threadIdx.x < 64) {
+      const int r = threadIdx.x;
+      sLse[buf * 64 + r] = r < vq ? p.lse[rowbase + r] : -INFINITY;
+      sRho[buf * 64 + r] = r < vq ? p.rho[rowbase + r] : 0.f;
+    } else if (CENTROID && threadIdx.x < 66) {  // this query block's members among the 64 centroids
+      const int w = threadIdx.x - 64;
+      const uint32_t* mb = p.bits + ((long long)bh * p.n_flat + f) * p.W;
+      sMem[buf * 2 + w] = mb[(c0 >> 5) + w];
+    }
+    cp_commit();
+  };
+  // per-key bias (log2 of the centroid weight; -inf = invalid key row)
   const int kr0 = warp * 16 + g, kr1 = kr0 + 8;
-  float kb0 = 0.f, kb1 = 0.f;
-  bool kv0 = kr0 < vk, kv1 = kr1 < vk;
+  float kb0 = kr0 < vk ? 0.f : -INFINITY, kb1 = kr1 < vk ? 0.f : -INFINITY;
   if (CENTROID) {
-    kv0 = c0 + kr0 < p.t_new;
-    kv1 = c0 + kr1 < p.t_new;
-    if (kv0) kb0 = __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + c0 + kr0]));
-    if (kv1) kb1 = __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + c0 + kr1]));
+    kb0 = c0 + kr0 < p.t_new ? __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + c0 + kr0])) : -INFINITY;
+    kb1 = c0 + kr1 < p.t_new ? __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + c0 + kr1])) : -INFINITY;
   }
   float dk[D / 8][4], dv[D / 8][4];
 #pragma unroll
   for (int n = 0; n < D / 8; ++n)
 #pragma unroll
     for (int e = 0; e < 4; ++e) dk[n][e] = dv[n][e] = 0.f;
-  const uint32_t bq = smem_u32(sQ), bo = smem_u32(sO), bk = smem_u32(sK), bvv = smem_u32(sV);
+  if (n_list > 0) prefetch(0, 0);
+  const uint32_t bk = smem_u32(sK), bvv = smem_u32(sV);
   for (int li = 0; li < n_list; ++li) {
-    const int x = sList[li];
-    const bool is_flat = x >= p.n_sharp;
-    const int f = x - p.n_sharp;
-    const int u = is_flat ? p.flat[bh * p.n_flat + f] : p.sharp[bh * p.n_sharp + x];
-    const int tok = bw_tok0(p, u), vq = bw_valid(p, u);
-    const long long rowbase = (long long)bh * p.S + tok;
-    __syncthreads();  // previous Q/dO consumed
-    load_tile<D>(sQ, p.q + bb * p.sb + hh * p.sh + tok * p.ss, p.ss, vq);
-    load_tile<D>(sO, p.dout + bb * p.db + hh * p.dh + tok * p.ds, p.ds, vq);
-    if (threadIdx.x < 64) {
-      const int r = threadIdx.x;
-      sLse[r] = r < vq ? p.lse[rowbase + r] : -INFINITY;
-      sRho[r] = r < vq ? p.rho[rowbase + r] : 0.f;
+    const int buf = li & 1;
+    if (li + 1 < n_list) {
+      prefetch(li + 1, buf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
     }
     __syncthreads();
-    const uint32_t* mb = (CENTROID && is_flat) ? p.bits + ((long long)bh * p.n_flat + f) * p.W : nullptr;
+    const uint32_t bq = smem_u32(sQO + buf * 2 * TB), bo = bq + TB;
+    const float* lse = sLse + buf * 64;
+    const float* rho = sRho + buf * 64;
     // S^T = K Q^T, dP^T = V dO^T (16 keys x 64 queries per warp)
     float sc[8][4], dp[8][4];
 #pragma unroll
@@ -364,6 +410,11 @@ __global__ void __launch_bounds__(128) bwd_dkv_kernel(const BwdParams p) {
         mma16816(dp[n + 1], av, b[2], b[3]);
       }
     }
+    float b0 = kb0, b1 = kb1;
+    if (CENTROID) {  // the row block's own exact members are excluded (taylor.py:154)
+      if ((sMem[buf * 2 + (kr0 >> 5)] >> (kr0 & 31)) & 1u) b0 = -INFINITY;
+      if ((sMem[buf * 2 + (kr1 >> 5)] >> (kr1 & 31)) & 1u) b1 = -INFINITY;
+    }
     uint32_t ap[4][4], ads[4][4];
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
@@ -371,16 +422,10 @@ __global__ void __launch_bounds__(128) bwd_dkv_kernel(const BwdParams p) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int q = n * 8 + tig * 2 + (e & 1);
-        const bool hi = e >= 2;
-        bool ok = (hi ? kv1 : kv0) && q < vq;
-        if (CENTROID && ok) {
-          const int jj = c0 + (hi ? kr1 : kr0);
-          ok = !((mb[jj >> 5] >> (jj & 31)) & 1u);
-        }
-        const float lse = sLse[q];
-        const float pr = (ok && lse > -INFINITY) ? exp2f(fmaf(sc[n][e], p.sl2, (hi ? kb1 : kb0) - lse)) : 0.f;
+        const float ls = lse[q];
+        const float pr = ls > -INFINITY ? exp2f(fmaf(sc[n][e], p.sl2, (e >= 2 ? b1 : b0) - ls)) : 0.f;
         pv[e] = pr;
-        dsv[e] = pr * (dp[n][e] - sRho[q]);
+        dsv[e] = pr * (dp[n][e] - rho[q]);
       }
       const int kk = n >> 1;
       const int o = (n & 1) ? 2 : 0;
@@ -402,7 +447,10 @@ __global__ void __launch_bounds__(128) bwd_dkv_kernel(const BwdParams p) {
         mma16816(dk[n], ads[kk], b[0], b[1]);
         mma16816(dk[n + 1], ads[kk], b[2], b[3]);
       }
+    __syncthreads();  // buffer `buf` is refilled by the prefetch of block li + 2
   }
+  const bool kv0 = CENTROID ? c0 + kr0 < p.t_new : kr0 < vk;
+  const bool kv1 = CENTROID ? c0 + kr1 < p.t_new : kr1 < vk;
   // stores
   if (CENTROID) {
 #pragma unroll

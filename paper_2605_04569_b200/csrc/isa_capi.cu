@@ -778,11 +778,12 @@ BwdWs carve_bwd(const Dims& d, uint8_t* base) {
 
 template <int D>
 int launch_bwd(const isa::BwdParams& bp, const Dims& d, cudaStream_t st) {
-  const size_t tiles = 4ull * 64 * D * 2;
-  const size_t sm_dkv = tiles + 2 * 64 * 4 + 4ull * (d.n_sharp + d.n_flat);
+  const size_t tiles = 6ull * 64 * D * 2;  // 2 resident + 2 x 2 double-buffered tiles
+  const size_t sm_dq = tiles + 2 * 64 * 4;
+  const size_t sm_dkv = tiles + 4 * 64 * 4 + 16 + 4ull * (d.n_sharp + d.n_flat);
   static size_t cur_dq = 48 * 1024, cur_e = 48 * 1024, cur_c = 48 * 1024;
   int rc;
-  if ((rc = ensure_smem((const void*)isa::bwd_dq_kernel<D>, tiles, &cur_dq))) return rc;
+  if ((rc = ensure_smem((const void*)isa::bwd_dq_kernel<D>, sm_dq, &cur_dq))) return rc;
   if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 0>, sm_dkv, &cur_e))) return rc;
   if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 1>, sm_dkv, &cur_c))) return rc;
   if (d.n_flat) {
@@ -791,7 +792,7 @@ int launch_bwd(const isa::BwdParams& bp, const Dims& d, cudaStream_t st) {
   }
   isa::bwd_dkv_kernel<D, 0><<<dim3(d.t_new, d.BH), 128, sm_dkv, st>>>(bp);
   ISA_LAUNCHED("bwd_dkv_kernel<exact>");
-  isa::bwd_dq_kernel<D><<<dim3(d.n_sharp + d.n_flat, d.BH), 128, tiles, st>>>(bp);
+  isa::bwd_dq_kernel<D><<<dim3(d.n_sharp + d.n_flat, d.BH), 128, sm_dq, st>>>(bp);
   ISA_LAUNCHED("bwd_dq_kernel");
   return ISA_OK;
 }
