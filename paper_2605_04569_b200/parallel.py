@@ -35,16 +35,17 @@ def gather_heads(out_local: torch.Tensor, out_full: torch.Tensor, world: int, gr
                  chunks: Optional[List[int]] = None) -> None:
     """All-gather head shards into out_full (B, H, S, D) (round-robin layout).
 
-    B == 1 on CUDA with H % P == 0: one all_gather_into_tensor per local head
-    chunk c straight into the contiguous slab out_full[0, c*P:(c+1)*P].
-    Otherwise a generic all_gather of shards padded to ceil(H/P) heads and a
-    strided scatter (uneven head counts; the CPU/gloo tests)."""
+    B == 1 with H % P == 0: one all_gather_into_tensor per local head chunk c
+    straight into the contiguous slab out_full[0, c*P:(c+1)*P] (viewed as the
+    concatenation (P*S, D), which NCCL and gloo both accept, so the CPU gloo
+    tests run this exact path). Otherwise a generic all_gather of shards
+    padded to ceil(H/P) heads and a strided scatter (uneven head counts, B > 1)."""
     B, Hl, S, D = out_local.shape
     H = out_full.shape[1]
-    if B == 1 and out_full.is_cuda and out_full.is_contiguous() and H % world == 0:
+    if B == 1 and out_full.is_contiguous() and H % world == 0:
         for c in (chunks if chunks is not None else range(Hl)):
-            dist.all_gather_into_tensor(out_full[0, c * world:(c + 1) * world], out_local[0, c].contiguous(),
-                                        group=group)
+            dist.all_gather_into_tensor(out_full[0, c * world:(c + 1) * world].view(world * S, D),
+                                        out_local[0, c].contiguous(), group=group)
         return
     h_max = -(-H // world)
     send = out_local
