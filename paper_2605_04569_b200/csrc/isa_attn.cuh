@@ -695,22 +695,29 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           }
           tmem_st16(t_p + 16 * ch, pk);
         };
+        auto zero = [&](const int ch) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk[c] = 0u;
+          tmem_st16(t_p + 16 * ch, pk);
+        };
         if (MODE != MODE_TAYLOR || dense || cmask) {  // every K6/K8 tile: one straight-line schedule
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) chunk(ch);
-        } else {      // Taylor union tiles: per-half (warp-uniform) choice
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            if (ch < 2 ? half0 : half1) {
-              chunk(ch);
-            } else {
-              uint32_t pk[16];
-#pragma unroll
-              for (int c = 0; c < 16; ++c) pk[c] = 0u;
-              tmem_st16(t_p + 16 * ch, pk);
-            }
-          }
+        } else if (half0) {  // Taylor union tile, only the first 64 keys listed (warp-uniform):
+          chunk(0);          // straight-line code per case so the two chunks interleave
+          chunk(1);
+          zero(2);
+          zero(3);
+        } else {
+          zero(0);
+          zero(1);
+          chunk(2);
+          chunk(3);
         }
+#ifdef ISA_TRACE_SPEC
+        if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 2);
+#endif
 #ifdef ISA_SPEC_SUMCHECK
         // every p <= sum: sum <= 2^8 bounds the tile max by m + 8
         const float2 s2c = fadd2(fadd2(sp2[0], sp2[1]), fadd2(sp2[2], sp2[3]));
@@ -720,6 +727,9 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         const bool redo = (m == -INFINITY) || (fmaf(mt, sl2, bias) > m + 8.f);
 #endif
         tmem_st_wait();
+#ifdef ISA_TRACE_SPEC
+        if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 3);
+#endif
         if (!__any_sync(0xffffffffu, redo)) {
           tc_fence_before();
           __syncwarp();

@@ -67,13 +67,13 @@ def run(args):
     buf = np.zeros((96, 2, 8), dtype=np.int64)
     N.check(lib.isa_debug_trace_copy(buf.ctypes.data, buf.nbytes))
     t = buf - buf[1, 0, 0]
-    print("step st |  S_rdy   ld  S->P(arrive) | mma_see issue | S_rdy(i+1)-issue | step_dt")
+    print("step st |  S_rdy   ld  exps st_wait  S->P(arrive) | mma_see issue | S_rdy(i+1)-issue | step_dt")
     for i in range(args.first, min(args.first + args.n, 95)):
         for s in range(2):
             a = t[i, s]
             nxt = t[i + 1, s, 0] - t[i + 1, s, 7] if i + 1 < 96 else 0
             dt = t[i + 1, s, 0] - a[0]
-            print(f"{i:4d} {s}  | {a[0]:7d} {a[1]-a[0]:4d} {a[4]-a[0]:6d} |"
+            print(f"{i:4d} {s}  | {a[0]:7d} {a[1]-a[0]:4d} {a[2]-a[1]:5d} {a[3]-a[2]:5d} {a[4]-a[0]:6d} |"
                   f" {t[i+1, s, 6]-a[4]:6d} {t[i+1, s, 7]-t[i+1, s, 6]:5d} | {nxt:6d} | {dt:6d}")
     steps = t[args.first + args.n, 0, 0] - t[args.first, 0, 0]
     print(f"avg clk/step over {args.n} steps: {steps / args.n:.0f} (ideal MMA 2048 at D=128)")
