@@ -1,0 +1,320 @@
+// tcgen05 key-major dK/dV kernel of the ISA backward (exact K_new blocks):
+// the sharp-branch (reference.py:173-225) and Taylor exact-slot
+// (taylor.py:262-273) contributions to dK_new / dV_new, plus the centroid
+// block-mean adjoint (taylor.py:290-292) and the K_new gather adjoint
+// (pipeline.py:423-433) fused into the epilogue.
+//
+// CTA = 128 keys = K_new blocks (2x, 2x+1); it streams 128-row query tiles
+// (pairs of query blocks: all sharp blocks, then the flat blocks whose exact
+// list holds either key block). Per query tile, with K/V resident in shared
+// memory and Q/dO double-buffered by TMA:
+//   S^T  = K Q^T     (SS, TMEM cols [0,128))
+//   dP^T = V dO^T    (SS, TMEM cols [128,256))
+//   softmax warps (thread = key row = TMEM lane): P^T = exp2(S^T*sl2 - lse),
+//     dS^T = P^T (dP^T - rho); bf16 P^T / dS^T over the upper halves of the
+//     S^T / dP^T regions (chunks in descending order: each write lands on
+//     columns already read)
+//   dV  += P^T dO    (TS, TMEM cols [256,384); dO tile read MN-major)
+//   dK  += dS^T Q    (TS, TMEM cols [384,512); Q tile read MN-major)
+// Warps: 0-3 softmax + epilogue, 4 TMEM alloc + MMA issue, 5 TMA producer
+// (+ per-query lse/rho rows into shared memory).
+#pragma once
+#include "isa_bwd.cuh"
+
+namespace isa {
+
+struct BwdTcParams {
+  BwdParams b;
+  int n_list_max;  // n_sharp + n_flat (query-list capacity)
+};
+
+template <int D>
+struct BwdTcSmem {
+  static constexpr int kTile = 128 * D * 2;  // one 128-row bf16 tile
+  static constexpr int kK = 0;
+  static constexpr int kV = kTile;
+  static constexpr int kQO = 2 * kTile;          // [2 slots][Q, dO]
+  static constexpr int kStats = kQO + 4 * kTile;  // [2 slots][lse 128, rho 128] floats
+  static constexpr int kBar = kStats + 2 * 256 * 4;
+  static constexpr int kList = kBar + 256;       // int list (query-block positions) + vis flags
+  static constexpr int bytes(int n_list) { return kList + 8 * n_list + 1024; }
+};
+
+template <int D>
+__global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
+                                                            const __grid_constant__ CUtensorMap tm_k,
+                                                            const __grid_constant__ CUtensorMap tm_v,
+                                                            const __grid_constant__ CUtensorMap tm_do,
+                                                            const BwdTcParams tp) {
+  using L = BwdTcSmem<D>;
+  const BwdParams& p = tp.b;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* qo_full = bars + 1;   // [2]
+  uint64_t* qo_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* d_full = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  int* s_count = reinterpret_cast<int*>(bars + 9);
+  int* sList = reinterpret_cast<int*>(smem + L::kList);     // query-block position (x < n_sharp: sharp)
+  int* sVis = sList + tp.n_list_max;                          // bit0: lists j0, bit1: lists j1
+  float* sStats = reinterpret_cast<float*>(smem + L::kStats);
+
+  const int bh = blockIdx.y;
+  const int hh = bh % p.H, bb = bh / p.H;
+  const int j0 = 2 * blockIdx.x, j1 = 2 * blockIdx.x + 1;
+  const bool has1 = j1 < p.t_new;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int* tab = p.kv_blk + (long long)bh * p.t_new;
+
+  // ---- query list (sharp blocks, then flat blocks listing j0 or j1)
+  if (threadIdx.x == 0) {
+    *s_count = 0;
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qo_full[s], 1);
+      mbar_init(&qo_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(d_full, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < p.n_sharp; x += blockDim.x) {
+    sList[x] = x;
+    sVis[x] = 3;
+  }
+  for (int f = threadIdx.x; f < p.n_flat; f += blockDim.x) {
+    const uint32_t* mb = p.bits + ((long long)bh * p.n_flat + f) * p.W;
+    const int v0 = (mb[j0 >> 5] >> (j0 & 31)) & 1u;
+    const int v1 = has1 ? (mb[j1 >> 5] >> (j1 & 31)) & 1u : 0;
+    if (v0 | v1) {
+      const int at = p.n_sharp + atomicAdd(s_count, 1);
+      sList[at] = p.n_sharp + f;
+      sVis[at] = v0 | (v1 << 1);
+    }
+  }
+  if (warp == 4) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_list = p.n_sharp + *s_count;
+  const int n_tiles = (n_list + 1) >> 1;
+
+  if (warp == 5) {
+    // ---------------------------------------------------------------- TMA producer
+    const bool leader = elect_one();
+    const uint64_t pol = policy_evict_last();
+    if (leader) {
+      mbar_arrive_expect_tx(kv_full, 2 * L::kTile);
+      for (int half = 0; half < 2; ++half) {
+        const int j = half ? (has1 ? j1 : j0) : j0;
+        const int u = tab[j];
+        const int tok = bw_tok0(p, u);
+        for (int pl = 0; pl < D / 64; ++pl) {
+          tma_load_4d(smem + L::kK + pl * 16384 + half * 8192, &tm_k, kv_full, pl * 64, tok, hh, bb, pol);
+          tma_load_4d(smem + L::kV + pl * 16384 + half * 8192, &tm_v, kv_full, pl * 64, tok, hh, bb, pol);
+        }
+      }
+    }
+    for (int t = 0; t < n_tiles; ++t) {
+      const int slot = t & 1;
+      if (t >= 2) mbar_wait(&qo_empty[slot], ((t >> 1) - 1) & 1);
+      __syncwarp();
+      float* st = sStats + slot * 256;
+      int u[2], vq[2];
+      for (int h = 0; h < 2; ++h) {
+        const int li = 2 * t + h;
+        if (li < n_list) {
+          const int x = sList[li];
+          u[h] = x < p.n_sharp ? p.sharp[bh * p.n_sharp + x] : p.flat[bh * p.n_flat + (x - p.n_sharp)];
+          vq[h] = bw_valid(p, u[h]);
+        } else {
+          u[h] = -1;
+          vq[h] = 0;
+        }
+      }
+      // per-query softmax statistics (lse = -inf masks missing / padded rows)
+      for (int r = lane; r < 128; r += 32) {
+        const int h = r >> 6, rr = r & 63;
+        float ls = -INFINITY, rh = 0.f;
+        if (u[h] >= 0 && rr < vq[h]) {
+          const long long row = (long long)bh * p.S + bw_tok0(p, u[h]) + rr;
+          ls = p.lse[row];
+          rh = p.rho[row];
+        }
+        st[r] = ls;
+        st[128 + r] = rh;
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (leader) {
+        mbar_arrive_expect_tx(&qo_full[slot], 2 * L::kTile);
+        uint8_t* dq_ = smem + L::kQO + slot * 2 * L::kTile;
+        for (int h = 0; h < 2; ++h) {
+          const int uu = u[h] >= 0 ? u[h] : u[0];
+          const int tok = bw_tok0(p, uu);
+          for (int pl = 0; pl < D / 64; ++pl) {
+            tma_load_4d(dq_ + pl * 16384 + h * 8192, &tm_q, &qo_full[slot], pl * 64, tok, hh, bb, pol);
+            tma_load_4d(dq_ + L::kTile + pl * 16384 + h * 8192, &tm_do, &qo_full[slot], pl * 64, tok, hh, bb,
+                        pol);
+          }
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128, 0, 0);
+    constexpr uint32_t idesc_g = idesc_bf16_f32(128, D, 0, 1);
+    const bool leader = elect_one();
+    const uint64_t dk_base = sdesc_sw128_base(smem_u32(smem + L::kK), 16, 1024);
+    const uint64_t dv_base = sdesc_sw128_base(smem_u32(smem + L::kV), 16, 1024);
+    auto qo_desc = [&](int slot, int which, bool mn) {
+      return sdesc_sw128_base(smem_u32(smem + L::kQO + (slot * 2 + which) * L::kTile), mn ? 16384 : 16, 1024);
+    };
+    auto issue_sd = [&](int slot) {  // S^T = K Q^T, dP^T = V dO^T
+      if (leader) {
+        const uint64_t dq = qo_desc(slot, 0, false), dd = qo_desc(slot, 1, false);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + 0, dk_base + off, dq + off, idesc_s, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + 128, dv_base + off, dd + off, idesc_s, kk > 0);
+        }
+        mma_commit(s_full);
+      }
+      __syncwarp();
+    };
+    auto issue_g = [&](int slot, bool acc) {  // dV += P^T dO, dK += dS^T Q
+      if (leader) {
+        const uint64_t dq = qo_desc(slot, 0, true), dd = qo_desc(slot, 1, true);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + 256, tmem + 64 + kk * 8, dd + (uint64_t)((kk * 2048) >> 4), idesc_g, acc || kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + 384, tmem + 128 + 64 + kk * 8, dq + (uint64_t)((kk * 2048) >> 4), idesc_g, acc || kk > 0);
+        mma_commit(&qo_empty[slot]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(kv_full, 0);
+    for (int t = 0; t < n_tiles; ++t) {
+      const int slot = t & 1;
+      mbar_wait(&qo_full[slot], (t >> 1) & 1);
+      __syncwarp();
+      tc_fence_after();
+      issue_sd(slot);
+      mbar_wait(p_full, t & 1);
+      __syncwarp();
+      tc_fence_after();
+      issue_g(slot, t > 0);
+    }
+    if (leader) mma_commit(d_full);
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- softmax (thread = key row)
+    const int row = warp * 32 + lane;
+    const int kh = row >> 6;          // key half: 0 -> j0, 1 -> j1
+    const int j = kh ? j1 : j0;
+    const bool key_exists = kh == 0 || has1;
+    const int uk = key_exists ? tab[j] : tab[j0];
+    const bool key_ok = key_exists && (row & 63) < bw_valid(p, uk);
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t t_s = tmem + lane_base, t_dp = tmem + lane_base + 128;
+    const float sl2 = p.sl2;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int slot = t & 1;
+      const float* st = sStats + slot * 256;
+      // visibility of this key row for the two query halves of the tile
+      bool vis[2];
+      for (int h = 0; h < 2; ++h) {
+        const int li = 2 * t + h;
+        vis[h] = key_ok && li < n_list && ((sVis[li] >> kh) & 1);
+      }
+      mbar_wait(&qo_full[slot], (t >> 1) & 1);  // the producer's lse/rho rows of this tile
+      mbar_wait(s_full, t & 1);
+      __syncwarp();
+      tc_fence_after();
+#pragma unroll 1
+      for (int ch = 3; ch >= 0; --ch) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(t_s + ch * 32, sr);
+        tmem_ld32(t_dp + ch * 32, dr);
+        tmem_ld_wait();
+        const bool v = vis[ch >> 1];
+        uint32_t pk[16], dk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int q0 = ch * 32 + 2 * c;
+          float pv[2], dv[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float ls = st[q0 + e];
+            const float pr = (v && ls > -INFINITY) ? ex2_approx(fmaf(__uint_as_float(sr[2 * c + e]), sl2, -ls)) : 0.f;
+            pv[e] = pr;
+            dv[e] = pr * (__uint_as_float(dr[2 * c + e]) - st[128 + q0 + e]);
+          }
+          pk[c] = pack_bf16x2(pv[0], pv[1]);
+          dk[c] = pack_bf16x2(dv[0], dv[1]);
+        }
+        tmem_st16(t_s + 64 + ch * 16, pk);
+        tmem_st16(t_dp + 64 + ch * 16, dk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // ---------------------------------------------------------------- epilogue
+    mbar_wait(d_full, 0);
+    __syncwarp();
+    tc_fence_after();
+    const long long orow = (long long)bh * p.S + bw_tok0(p, uk) + (row & 63);
+    const float invw = 1.f / (float)bw_valid(p, uk);
+    const long long cb = ((long long)bh * p.t_new + j) * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t vr[32], kr[32];
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + 256 + c * 32, vr);
+      tmem_ld32(tmem + lane_base + 384 + c * 32, kr);
+      tmem_ld_wait();
+      if (n_tiles == 0) {  // no query block sees these keys: only the centroid part
+#pragma unroll
+        for (int e = 0; e < 32; ++e) vr[e] = kr[e] = 0u;
+      }
+      if (key_ok) {
+        float* dkp = p.dk + orow * D + c * 32;
+        float* dvp = p.dv + orow * D + c * 32;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          float ck = 0.f, cv = 0.f;
+          if (p.n_flat) {
+            ck = p.dkc[cb + c * 32 + e] * invw;
+            cv = p.dvc[cb + c * 32 + e] * invw;
+          }
+          dkp[e] = p.scale * __uint_as_float(kr[e]) + ck;
+          dvp[e] = __uint_as_float(vr[e]) + cv;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace isa

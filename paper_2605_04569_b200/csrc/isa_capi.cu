@@ -26,6 +26,7 @@
 #include "isa_attn.cuh"
 #include "isa_attn_p2.cuh"
 #include "isa_bwd.cuh"
+#include "isa_bwd_tc.cuh"
 #include "isa_route.cuh"
 
 namespace {
@@ -776,8 +777,17 @@ BwdWs carve_bwd(const Dims& d, uint8_t* base) {
   return b;
 }
 
+// Backward dK/dV path: tcgen05 kernel by default, mma.sync (ISA_BWD_MMASYNC=1) for A/B.
+bool bwd_mmasync() {
+  static bool v = [] {
+    const char* e = getenv("ISA_BWD_MMASYNC");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 template <int D>
-int launch_bwd(const isa::BwdParams& bp, const Dims& d, cudaStream_t st) {
+int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps, cudaStream_t st) {
   const size_t tiles = 6ull * 64 * D * 2;  // 2 resident + 2 x 2 double-buffered tiles
   const size_t sm_dq = tiles + 2 * 64 * 4;
   const size_t sm_dkv = tiles + 4 * 64 * 4 + 16 + 4ull * (d.n_sharp + d.n_flat);
@@ -790,8 +800,19 @@ int launch_bwd(const isa::BwdParams& bp, const Dims& d, cudaStream_t st) {
     isa::bwd_dkv_kernel<D, 1><<<dim3(d.tn_pad / 64, d.BH), 128, sm_dkv, st>>>(bp);
     ISA_LAUNCHED("bwd_dkv_kernel<centroid>");
   }
-  isa::bwd_dkv_kernel<D, 0><<<dim3(d.t_new, d.BH), 128, sm_dkv, st>>>(bp);
-  ISA_LAUNCHED("bwd_dkv_kernel<exact>");
+  if (bwd_mmasync()) {
+    isa::bwd_dkv_kernel<D, 0><<<dim3(d.t_new, d.BH), 128, sm_dkv, st>>>(bp);
+    ISA_LAUNCHED("bwd_dkv_kernel<exact>");
+  } else {
+    using TL = isa::BwdTcSmem<D>;
+    const int n_list = d.n_sharp + d.n_flat;
+    const size_t sm_tc = TL::bytes(n_list);
+    static size_t cur_tc = 48 * 1024;
+    if ((rc = ensure_smem((const void*)isa::bwd_dkv_tc_kernel<D>, sm_tc, &cur_tc))) return rc;
+    isa::BwdTcParams tp{bp, n_list};
+    isa::bwd_dkv_tc_kernel<D><<<dim3((d.t_new + 1) / 2, d.BH), 192, sm_tc, st>>>(maps[0], maps[1], maps[2], maps[3], tp);
+    ISA_LAUNCHED("bwd_dkv_tc_kernel");
+  }
   isa::bwd_dq_kernel<D><<<dim3(d.n_sharp + d.n_flat, d.BH), 128, sm_dq, st>>>(bp);
   ISA_LAUNCHED("bwd_dq_kernel");
   return ISA_OK;
@@ -897,8 +918,14 @@ int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, co
   bp.dq = dq;
   bp.dk = dk;
   bp.dv = dv;
+  CUtensorMap maps[4];  // q, k, v, dO (bf16, the shape's strides)
+  const void* srcs[4] = {q, k, v, dout};
+  for (int i = 0; i < 4; ++i)
+    if ((rc = make_map(&maps[i], srcs[i], d.D, d.S, d.H, d.B, shape->stride_s * 2, shape->stride_h * 2,
+                       shape->stride_b * 2)))
+      return rc;
   g_launches = 0;
-  rc = d.D == 128 ? launch_bwd<128>(bp, d, st) : launch_bwd<64>(bp, d, st);
+  rc = d.D == 128 ? launch_bwd<128>(bp, d, maps, st) : launch_bwd<64>(bp, d, maps, st);
   g_launches += launches;
   return rc;
 }
