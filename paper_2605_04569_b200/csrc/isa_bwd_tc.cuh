@@ -317,4 +317,296 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------- dQ (query-major, tcgen05)
+// CTA = 128 query rows = a pair of query blocks: sharp pairs stream every
+// K_new block pair (reference.py:173-225); flat pairs (the Taylor plan's
+// (item, stage) streams) stream their exact-union tiles, then every centroid
+// tile (taylor.py:262-285). Q/dO resident, K/V double-buffered by TMA:
+//   S  = Q K^T   (SS, TMEM [0,128)),  dP = dO V^T (SS, TMEM [128,256))
+//   softmax (thread = query row): dS = P (dP - rho), bf16 over S's upper half
+//   dQ += dS K   (TS, TMEM [256,384); K tile read MN-major)
+template <int D>
+struct BwdDqSmem {
+  static constexpr int kTile = 128 * D * 2;
+  static constexpr int kQ = 0;
+  static constexpr int kO = kTile;
+  static constexpr int kKV = 2 * kTile;                  // [2 slots][K, V]
+  static constexpr int kCol = kKV + 4 * kTile;          // [2 slots][128] column bias (centroid) floats
+  static constexpr int kMeta = kCol + 2 * 128 * 4;      // [2 slots][4] ints: centroid flag, tile index, meta0, meta1
+  static constexpr int kBar = kMeta + 64;
+  static constexpr int kBytes = kBar + 128 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
+                                                           const __grid_constant__ CUtensorMap tm_k,
+                                                           const __grid_constant__ CUtensorMap tm_v,
+                                                           const __grid_constant__ CUtensorMap tm_do,
+                                                           const __grid_constant__ CUtensorMap tm_kc,
+                                                           const __grid_constant__ CUtensorMap tm_vc,
+                                                           const BwdParams p, const int4* __restrict__ tiles,
+                                                           const int* __restrict__ n_tiles_f, int n_items,
+                                                           int max_tiles) {
+  using L = BwdDqSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* qo_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* d_full = bars + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  float* sCol = reinterpret_cast<float*>(smem + L::kCol);
+  int* sMeta = reinterpret_cast<int*>(smem + L::kMeta);
+
+  const int bh = blockIdx.y;
+  const int hh = bh % p.H, bb = bh / p.H;
+  const int n_sp = (p.n_sharp + 1) >> 1;  // sharp pairs
+  const bool flat = (int)blockIdx.x >= n_sp;
+  const int pair = flat ? blockIdx.x - n_sp : blockIdx.x;
+  const int item = pair >> 1, stg = pair & 1;  // flat: Taylor plan (item, stage)
+  int u[2];
+  for (int h = 0; h < 2; ++h) {
+    if (!flat) {
+      const int x = 2 * pair + h;
+      u[h] = x < p.n_sharp ? p.sharp[bh * p.n_sharp + x] : -1;
+    } else {
+      const int f = 4 * item + 2 * stg + h;
+      u[h] = f < p.n_flat ? p.flat[bh * p.n_flat + f] : -1;
+    }
+  }
+  const int n_exact = flat ? n_tiles_f[bh * n_items + item] : (p.t_new + 1) >> 1;
+  const int n_kv = n_exact + (flat ? p.tn_pad / 128 : 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int* tab = p.kv_blk + (long long)bh * p.t_new;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qo_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(d_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 4) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 5) {
+    // ---------------------------------------------------------------- TMA producer
+    const bool leader = elect_one();
+    const uint64_t pol = policy_evict_last();
+    if (leader) {
+      mbar_arrive_expect_tx(qo_full, 2 * L::kTile);
+      for (int h = 0; h < 2; ++h) {
+        const int tok = bw_tok0(p, u[h] >= 0 ? u[h] : u[0]);
+        for (int pl = 0; pl < D / 64; ++pl) {
+          tma_load_4d(smem + L::kQ + pl * 16384 + h * 8192, &tm_q, qo_full, pl * 64, tok, hh, bb, pol);
+          tma_load_4d(smem + L::kO + pl * 16384 + h * 8192, &tm_do, qo_full, pl * 64, tok, hh, bb, pol);
+        }
+      }
+    }
+    const int4* tl = flat ? tiles + (((long long)bh * n_items + item) * 2 + stg) * max_tiles : nullptr;
+    for (int i = 0; i < n_kv; ++i) {
+      const int slot = i & 1;
+      if (i >= 2) mbar_wait(&kv_empty[slot], ((i >> 1) - 1) & 1);
+      __syncwarp();
+      int tok0, tok1, cent = 0, meta0 = 0xF | (64 << 8), meta1 = 0xF | (64 << 8);
+      if (i < n_exact) {
+        if (flat) {
+          const int4 e = tl[i];
+          tok0 = e.x >= 0 ? e.x : 0;
+          tok1 = e.y >= 0 ? e.y : tok0;
+          meta0 = e.z >> (2 * stg) & 3 | (e.z & ~0xFF);  // visibility bits of this pair's two blocks
+          meta1 = e.w >> (2 * stg) & 3 | (e.w & ~0xFF);
+        } else {
+          const int kn0 = 2 * i, kn1 = 2 * i + 1;
+          const int u0 = tab[kn0];
+          tok0 = bw_tok0(p, u0);
+          meta0 = 3 | (bw_valid(p, u0) << 8);
+          if (kn1 < p.t_new) {
+            const int u1 = tab[kn1];
+            tok1 = bw_tok0(p, u1);
+            meta1 = 3 | (bw_valid(p, u1) << 8);
+          } else {
+            tok1 = tok0;
+            meta1 = 0;
+          }
+        }
+      } else {
+        cent = 1;
+        tok0 = (i - n_exact) * 128;
+        tok1 = tok0 + 64;
+        // column weights log2(valid rows) of the 128 centroids (-inf past t_new), taylor.py:156
+        for (int c = lane; c < 128; c += 32) {
+          const int jj = tok0 + c;
+          sCol[slot * 128 + c] = jj < p.t_new ? __log2f((float)bw_valid(p, tab[jj])) : -INFINITY;
+        }
+      }
+      if (lane == 0) {
+        sMeta[slot * 4 + 0] = cent;
+        sMeta[slot * 4 + 1] = i - n_exact;
+        sMeta[slot * 4 + 2] = meta0;
+        sMeta[slot * 4 + 3] = meta1;
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (leader) {
+        mbar_arrive_expect_tx(&kv_full[slot], 2 * L::kTile);
+        uint8_t* dst = smem + L::kKV + slot * 2 * L::kTile;
+        for (int h = 0; h < 2; ++h) {
+          const int tok = h ? tok1 : tok0;
+          for (int pl = 0; pl < D / 64; ++pl) {
+            if (cent) {
+              tma_load_4d(dst + pl * 16384 + h * 8192, &tm_kc, &kv_full[slot], pl * 64, tok, bh, 0, pol);
+              tma_load_4d(dst + L::kTile + pl * 16384 + h * 8192, &tm_vc, &kv_full[slot], pl * 64, tok, bh, 0, pol);
+            } else {
+              tma_load_4d(dst + pl * 16384 + h * 8192, &tm_k, &kv_full[slot], pl * 64, tok, hh, bb, pol);
+              tma_load_4d(dst + L::kTile + pl * 16384 + h * 8192, &tm_v, &kv_full[slot], pl * 64, tok, hh, bb, pol);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128, 0, 0);
+    constexpr uint32_t idesc_g = idesc_bf16_f32(128, D, 0, 1);
+    const bool leader = elect_one();
+    const uint64_t dq_base = sdesc_sw128_base(smem_u32(smem + L::kQ), 16, 1024);
+    const uint64_t do_base = sdesc_sw128_base(smem_u32(smem + L::kO), 16, 1024);
+    mbar_wait(qo_full, 0);
+    for (int i = 0; i < n_kv; ++i) {
+      const int slot = i & 1;
+      mbar_wait(&kv_full[slot], (i >> 1) & 1);
+      __syncwarp();
+      tc_fence_after();
+      const uint32_t kb = smem_u32(smem + L::kKV + slot * 2 * L::kTile);
+      if (leader) {
+        const uint64_t dk = sdesc_sw128_base(kb, 16, 1024), dv = sdesc_sw128_base(kb + L::kTile, 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + 0, dq_base + off, dk + off, idesc_s, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + 128, do_base + off, dv + off, idesc_s, kk > 0);
+        }
+        mma_commit(s_full);
+      }
+      __syncwarp();
+      mbar_wait(p_full, i & 1);
+      __syncwarp();
+      tc_fence_after();
+      if (leader) {
+        const uint64_t dkm = sdesc_sw128_base(kb, 16384, 1024);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + 256, tmem + 64 + kk * 8, dkm + (uint64_t)((kk * 2048) >> 4), idesc_g, (i > 0) || kk > 0);
+        mma_commit(&kv_empty[slot]);
+      }
+      __syncwarp();
+    }
+    if (leader) mma_commit(d_full);
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- softmax (thread = query row)
+    const int row = warp * 32 + lane;
+    const int qh = row >> 6;
+    const int uq = u[qh];
+    const int vq = uq >= 0 ? bw_valid(p, uq) : 0;
+    const bool row_ok = (row & 63) < vq;
+    const long long grow = row_ok ? (long long)bh * p.S + bw_tok0(p, uq) + (row & 63) : 0;
+    const float lse = row_ok ? p.lse[grow] : -INFINITY;
+    const float rho = row_ok ? p.rho[grow] : 0.f;
+    const bool live = row_ok && lse > -INFINITY;
+    const uint32_t* mb = (flat && uq >= 0) ? p.bits + ((long long)bh * p.n_flat + 4 * item + 2 * stg + qh) * p.W
+                                           : nullptr;
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t t_s = tmem + lane_base, t_dp = tmem + lane_base + 128;
+    const float sl2 = p.sl2;
+    for (int i = 0; i < n_kv; ++i) {
+      const int slot = i & 1;
+      mbar_wait(&kv_full[slot], (i >> 1) & 1);  // the producer's per-tile metadata
+      const int cent = sMeta[slot * 4 + 0], cidx = sMeta[slot * 4 + 1];
+      const int m0 = sMeta[slot * 4 + 2], m1 = sMeta[slot * 4 + 3];
+      // exact tiles: per-half limit (valid rows if this row's block sees the half, else 0)
+      const int lim0 = ((m0 >> qh) & 1) ? (m0 >> 8) : 0;
+      const int lim1 = ((m1 >> qh) & 1) ? (m1 >> 8) : 0;
+      uint32_t mw[4] = {0u, 0u, 0u, 0u};
+      if (cent && mb) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) mw[w] = __ldg(mb + cidx * 4 + w);  // own exact members excluded
+      }
+      mbar_wait(s_full, i & 1);
+      __syncwarp();
+      tc_fence_after();
+#pragma unroll 1
+      for (int ch = 3; ch >= 0; --ch) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(t_s + ch * 32, sr);
+        tmem_ld32(t_dp + ch * 32, dr);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          float dv[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = ch * 32 + 2 * c + e;
+            float bias;
+            bool ok;
+            if (cent) {
+              bias = sCol[slot * 128 + col];
+              ok = !((mw[col >> 5] >> (col & 31)) & 1u);
+            } else {
+              bias = 0.f;
+              ok = (col & 63) < (col < 64 ? lim0 : lim1);
+            }
+            const float pr = (live && ok) ? ex2_approx(fmaf(__uint_as_float(sr[2 * c + e]), sl2, bias - lse)) : 0.f;
+            dv[e] = pr * (__uint_as_float(dr[2 * c + e]) - rho);
+          }
+          pk[c] = pack_bf16x2(dv[0], dv[1]);
+        }
+        tmem_st16(t_s + 64 + ch * 16, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // ---------------------------------------------------------------- epilogue
+    mbar_wait(d_full, 0);
+    __syncwarp();
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t qr[32];
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + 256 + c * 32, qr);
+      tmem_ld_wait();
+      if (row_ok) {
+        float* dst = p.dq + grow * D + c * 32;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) dst[e] = n_kv ? p.scale * __uint_as_float(qr[e]) : 0.f;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 }  // namespace isa

@@ -787,7 +787,8 @@ bool bwd_mmasync() {
 }
 
 template <int D>
-int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps, cudaStream_t st) {
+int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps, const Workspace& w,
+               cudaStream_t st) {
   const size_t tiles = 6ull * 64 * D * 2;  // 2 resident + 2 x 2 double-buffered tiles
   const size_t sm_dq = tiles + 2 * 64 * 4;
   const size_t sm_dkv = tiles + 4 * 64 * 4 + 16 + 4ull * (d.n_sharp + d.n_flat);
@@ -813,8 +814,27 @@ int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps,
     isa::bwd_dkv_tc_kernel<D><<<dim3((d.t_new + 1) / 2, d.BH), 192, sm_tc, st>>>(maps[0], maps[1], maps[2], maps[3], tp);
     ISA_LAUNCHED("bwd_dkv_tc_kernel");
   }
-  isa::bwd_dq_kernel<D><<<dim3(d.n_sharp + d.n_flat, d.BH), 128, sm_dq, st>>>(bp);
-  ISA_LAUNCHED("bwd_dq_kernel");
+  if (bwd_mmasync()) {
+    isa::bwd_dq_kernel<D><<<dim3(d.n_sharp + d.n_flat, d.BH), 128, sm_dq, st>>>(bp);
+    ISA_LAUNCHED("bwd_dq_kernel");
+  } else {
+    using QL = isa::BwdDqSmem<D>;
+    static size_t cur_q = 48 * 1024;
+    if ((rc = ensure_smem((const void*)isa::bwd_dq_tc_kernel<D>, QL::kBytes, &cur_q))) return rc;
+    CUtensorMap tkc = maps[0], tvc = maps[0];  // centroid maps (unused without flat blocks)
+    if (d.n_flat) {
+      if ((rc = make_map(&tkc, w.kc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
+                         (long long)d.BH * d.tn_pad * d.D * 2)))
+        return rc;
+      if ((rc = make_map(&tvc, w.vc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
+                         (long long)d.BH * d.tn_pad * d.D * 2)))
+        return rc;
+    }
+    const int grid_x = (d.n_sharp + 1) / 2 + 2 * d.items_f;
+    isa::bwd_dq_tc_kernel<D><<<dim3(grid_x, d.BH), 192, QL::kBytes, st>>>(
+        maps[0], maps[1], maps[2], maps[3], tkc, tvc, bp, w.tiles, w.n_tiles, d.items_f, d.max_tiles);
+    ISA_LAUNCHED("bwd_dq_tc_kernel");
+  }
   return ISA_OK;
 }
 
@@ -925,7 +945,7 @@ int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, co
                        shape->stride_b * 2)))
       return rc;
   g_launches = 0;
-  rc = d.D == 128 ? launch_bwd<128>(bp, d, maps, st) : launch_bwd<64>(bp, d, maps, st);
+  rc = d.D == 128 ? launch_bwd<128>(bp, d, maps, b.fw, st) : launch_bwd<64>(bp, d, maps, b.fw, st);
   g_launches += launches;
   return rc;
 }
