@@ -28,6 +28,8 @@
 // TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512);
 // P_s (bf16 pairs) overwrites the upper 64 columns of S_s.
 #pragma once
+#include <type_traits>
+
 #include "isa_ptx.cuh"
 
 namespace isa {
@@ -487,12 +489,18 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
     float m = -INFINITY;  // running max, log2 domain (already scaled)
     float l = 0.f;
     const uint32_t* mbits = nullptr;
+    uint32_t mreg[4] = {0u, 0u, 0u, 0u};  // member words (W <= 128, checked on the host)
     int jsrc = -1, jctx = -1;
     float lwsrc = 6.f, lwctx = 6.f;
     if (MODE == MODE_TAYLOR) {
       int pos = item * 4 + qb;
       if (pos >= p.n_qblk) pos = item * 4;
       mbits = p.member_bits + ((long long)bh * p.n_qblk + pos) * p.W;
+      // the row block's member words live in registers across the warp
+      // (lane w holds words w and w + 32): centroid tiles fetch theirs with
+      // shuffles instead of a dependent global load on the S -> P path
+#pragma unroll
+      for (int r = 0; r < 4; ++r) mreg[r] = lane + 32 * r < p.W ? __ldg(mbits + lane + 32 * r) : 0u;
       if (p.l_src & 63) {  // short last source block = K_new block t_src-1
         jsrc = p.t_src - 1;
         lwsrc = log2f(static_cast<float>(p.l_src & 63));
@@ -614,20 +622,35 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           mw[w] = lim >= 32 ? 0u : (lim <= 0 ? 0xffffffffu : ~((1u << lim) - 1u));
         }
       } else {
-        const uint32_t* wb = mbits + t.cidx * 4;
         const int j0 = t.cidx * 128;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
           const int live = p.t_new - (j0 + 32 * w);  // columns < t_new in this word
           const uint32_t oob = live >= 32 ? 0u : (live <= 0 ? 0xffffffffu : ~((1u << live) - 1u));
-          mw[w] = __ldg(wb + w) | oob;
+          mw[w] = oob;  // the row block's own members are ORed in where needed (add_members)
         }
         bias = 6.f;
         special = (jsrc >= j0 && jsrc < j0 + 128) || (jctx >= j0 && jctx < j0 + 128);
       }
-      const bool skip0 = (mw[0] & mw[1]) == 0xffffffffu;
-      const bool skip1 = (mw[2] & mw[3]) == 0xffffffffu;
-      const bool dense = (mw[0] | mw[1] | mw[2] | mw[3]) == 0u;
+      // centroid tiles: exclude the row block's own exact members
+      // (taylor.py:154); words fetched from the warp's registers by shuffles,
+      // only on the paths that process a centroid tile
+      auto add_members = [&]() {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int wi = t.cidx * 4 + w;
+          uint32_t word = 0u;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const uint32_t xw = __shfl_sync(0xffffffffu, mreg[r], wi & 31);
+            word = (wi >> 5) == r ? xw : word;
+          }
+          mw[w] |= word;
+        }
+      };
+      bool skip0 = (mw[0] & mw[1]) == 0xffffffffu;
+      bool skip1 = (mw[2] & mw[3]) == 0xffffffffu;
+      bool dense = (mw[0] | mw[1] | mw[2] | mw[3]) == 0u;
       float mx[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
@@ -660,29 +683,39 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[s]);
+        ISA_COUNT(MODE, 3);
         continue;
       }
       // Taylor centroid tiles (taylor.py:153-159) also take the speculative
       // path: excluded centroids (the row block's own exact members, columns
       // past t_new) are set to -inf first, so they contribute p = 0.
+#ifdef ISA_TAYLOR_FULLMASK
+      const bool cmask = MODE == MODE_TAYLOR && (t.centroid || (halfwise && !dense));
+#else
       const bool cmask = MODE == MODE_TAYLOR && t.centroid;
+#endif
       if (i > 0 && (halfwise || cmask) && !special) {
-        if (cmask) {
-#pragma unroll
-          for (int cc = 0; cc < 128; ++cc)
-            if ((mw[cc >> 5] >> (cc & 31)) & 1u) x[cc] = -INFINITY;
-        }
         const float2 sl2x2 = make_float2(sl2, sl2), nb2 = make_float2(bias - m, bias - m);
         float2 sp2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        auto chunk = [&](const int ch) {
+        // masked_tag: std::true_type only on the centroid path, so the per-column
+        // exclusion selects exist in that copy of the code alone (a runtime flag
+        // gets if-converted into 128 SELs on every tile)
+        auto chunk = [&](const int ch, auto masked_tag) {
+          constexpr bool kMasked = decltype(masked_tag)::value;
           uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
             const int cc = 32 * ch + 2 * c;
+            float xa = x[cc], xb = x[cc + 1];
+            if (kMasked) {  // excluded centroids (own exact members, past t_new) -> p = 0
+              const uint32_t w = mw[ch];
+              xa = ((w >> (2 * c)) & 1u) ? -INFINITY : xa;
+              xb = ((w >> (2 * c + 1)) & 1u) ? -INFINITY : xb;
+            }
 #ifndef ISA_SPEC_SUMCHECK
-            mx[c & 7] = fmax3(mx[c & 7], x[cc], x[cc + 1]);
+            mx[c & 7] = fmax3(mx[c & 7], xa, xb);
 #endif
-            const float2 tt = ffma2(make_float2(x[cc], x[cc + 1]), sl2x2, nb2);
+            const float2 tt = ffma2(make_float2(xa, xb), sl2x2, nb2);
             float2 pp;
             if (kEmuEvery > 0 && (c % kEmuEvery) == kEmuEvery - 1) {
               pp = ex2_emu2(tt);
@@ -701,19 +734,24 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           for (int c = 0; c < 16; ++c) pk[c] = 0u;
           tmem_st16(t_p + 16 * ch, pk);
         };
-        if (MODE != MODE_TAYLOR || dense || cmask) {  // every K6/K8 tile: one straight-line schedule
+        const std::false_type plain{};
+        if (MODE == MODE_TAYLOR && cmask) {  // Taylor centroid tile
+          add_members();
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) chunk(ch);
+          for (int ch = 0; ch < 4; ++ch) chunk(ch, std::true_type{});
+        } else if (MODE != MODE_TAYLOR || dense) {  // every K6/K8 tile: one straight-line schedule
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) chunk(ch, plain);
         } else if (half0) {  // Taylor union tile, only the first 64 keys listed (warp-uniform):
-          chunk(0);          // straight-line code per case so the two chunks interleave
-          chunk(1);
+          chunk(0, plain);   // straight-line code per case so the two chunks interleave
+          chunk(1, plain);
           zero(2);
           zero(3);
         } else {
           zero(0);
           zero(1);
-          chunk(2);
-          chunk(3);
+          chunk(2, plain);
+          chunk(3, plain);
         }
 #ifdef ISA_TRACE_SPEC
         if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 2);
@@ -731,6 +769,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 3);
 #endif
         if (!__any_sync(0xffffffffu, redo)) {
+          ISA_COUNT(MODE, 0);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[s]);
@@ -741,11 +780,18 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           continue;
         }
         // rare: the general path below recomputes the max and P from x[]
+        ISA_COUNT(MODE, 1);
         force_rescale = true;
 #pragma unroll
         for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
       }
 #endif
+      if (MODE == MODE_TAYLOR && t.centroid) {  // general path on a centroid tile (first tile / redo)
+        add_members();
+        skip0 = (mw[0] & mw[1]) == 0xffffffffu;
+        skip1 = (mw[2] & mw[3]) == 0xffffffffu;
+        dense = (mw[0] | mw[1] | mw[2] | mw[3]) == 0u;
+      }
       if (special) {  // rare: per-column weights, scaled in place
         const int j0 = t.cidx * 128;
 #pragma unroll
@@ -774,6 +820,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
       if (!special) mt = fmaf(mt, sl2, bias);  // max(x*sl2 + b) over the kept columns
       // running max with lazy rescale (threshold 8 in log2 units)
+      ISA_COUNT(MODE, 2);
       float m_new = fmaxf(m, mt);
       float o_scale = 1.f;
       bool need = false;

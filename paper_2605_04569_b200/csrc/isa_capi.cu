@@ -152,6 +152,8 @@ int derive(const IsaShape* sh, const IsaKnobs* kn, Dims* d) {
     return fail(ISA_ERR_CONFIG, "k_mask=%d out of [1, %d]", d->k, d->t_new);
   d->tn_pad = ((d->t_new + 127) / 128) * 128;
   d->W = d->tn_pad / 32;
+  if (d->n_flat && d->W > 128)  // the Taylor kernel keeps a row block's member words in 4 registers per lane
+    return fail(ISA_ERR_CONFIG, "t_new=%d K_new blocks exceed the Taylor kernel's limit (4096)", d->t_new);
   d->items_s = (d->n_sharp + 3) / 4;
   d->items_f = (d->n_flat + 3) / 4;
   int u = 2 * d->k < d->t_new ? 2 * d->k : d->t_new;  // union of a pair of exact lists
@@ -1164,6 +1166,14 @@ int isa_forward_host(const IsaShape* shape, const IsaKnobs* knobs, const void* q
 
 #ifdef ISA_TRACE
 // Debug build only (not in the header): copy the timeline stamps to host.
+int isa_debug_count_copy(void* host, int reset) {
+  ISA_CUDA(cudaMemcpyFromSymbol(host, isa::g_isa_count, sizeof(isa::g_isa_count)));
+  if (reset) {
+    static const unsigned long long z[3][4] = {};
+    ISA_CUDA(cudaMemcpyToSymbol(isa::g_isa_count, z, sizeof(z)));
+  }
+  return ISA_OK;
+}
 int isa_debug_trace_copy(void* host, size_t bytes) {
   ISA_CUDA(cudaMemcpyFromSymbol(host, isa::g_isa_trace, bytes < sizeof(isa::g_isa_trace) ? bytes : sizeof(isa::g_isa_trace)));
   return ISA_OK;

@@ -108,7 +108,16 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == ISA_TRACE && 
   do {                                                                              \
     if (trace_cta() && (step) < kTraceSteps) g_isa_trace[(step)][(stage)][(slot)] = clock64(); \
   } while (0)
+// softmax path counters (per warp-tile): [mode][0 spec, 1 redo, 2 general, 3 skip]
+__device__ unsigned long long g_isa_count[3][4];
+#define ISA_COUNT(mode, k)                                    \
+  do {                                                        \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_isa_count[(mode)][(k)], 1ull); \
+  } while (0)
 #else
+#define ISA_COUNT(mode, k) \
+  do {                     \
+  } while (0)
 #define ISA_TSTAMP(step, stage, slot) \
   do {                                \
   } while (0)

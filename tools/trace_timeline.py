@@ -77,6 +77,13 @@ def run(args):
                   f" {t[i+1, s, 6]-a[4]:6d} {t[i+1, s, 7]-t[i+1, s, 6]:5d} | {nxt:6d} | {dt:6d}")
     steps = t[args.first + args.n, 0, 0] - t[args.first, 0, 0]
     print(f"avg clk/step over {args.n} steps: {steps / args.n:.0f} (ideal MMA 2048 at D=128)")
+    cnt = np.zeros((3, 4), dtype=np.uint64)
+    lib.isa_debug_count_copy.restype = ctypes.c_int
+    lib.isa_debug_count_copy.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    N.check(lib.isa_debug_count_copy(cnt.ctypes.data, 0))
+    for mode, name in enumerate(("dense", "exact", "taylor")):
+        if cnt[mode].sum():
+            print(f"softmax warp-tiles {name}: spec {cnt[mode][0]}  redo {cnt[mode][1]}  general {cnt[mode][2]}  skip {cnt[mode][3]}")
     if args.isa:
         return
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
