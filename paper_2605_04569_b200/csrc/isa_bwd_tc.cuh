@@ -19,6 +19,8 @@
 // Warps: 0-3 softmax + epilogue, 4 TMEM alloc + MMA issue, 5 TMA producer
 // (+ per-query lse/rho rows into shared memory).
 #pragma once
+#include <type_traits>
+
 #include "isa_bwd.cuh"
 
 namespace isa {
@@ -550,34 +552,45 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
       mbar_wait(s_full, i & 1);
       __syncwarp();
       tc_fence_after();
-#pragma unroll 1
-      for (int ch = 3; ch >= 0; --ch) {
+      // one copy of the chunk code per tile kind (compile-time tag), so the
+      // exact tiles carry no centroid selects / shared-memory bias loads
+      auto chunk = [&](const int ch, auto cent_tag) {
+        constexpr bool kCent = decltype(cent_tag)::value;
         uint32_t sr[32], dr[32];
         tmem_ld32(t_s + ch * 32, sr);
         tmem_ld32(t_dp + ch * 32, dr);
         tmem_ld_wait();
+        // exact tiles: this chunk lies in one 64-key half with a row-uniform limit
+        const int lim = (ch < 2 ? lim0 : lim1) - 32 * (ch & 1);
+        const uint32_t cw = kCent ? mw[ch] : 0u;
         uint32_t pk[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
           float dv[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int col = ch * 32 + 2 * c + e;
-            float bias;
+            const int cc = 2 * c + e;  // column within the chunk
+            float bias = 0.f;
             bool ok;
-            if (cent) {
-              bias = sCol[slot * 128 + col];
-              ok = !((mw[col >> 5] >> (col & 31)) & 1u);
+            if (kCent) {
+              bias = sCol[slot * 128 + ch * 32 + cc];
+              ok = !((cw >> cc) & 1u);
             } else {
-              bias = 0.f;
-              ok = (col & 63) < (col < 64 ? lim0 : lim1);
+              ok = cc < lim;
             }
-            const float pr = (live && ok) ? ex2_approx(fmaf(__uint_as_float(sr[2 * c + e]), sl2, bias - lse)) : 0.f;
-            dv[e] = pr * (__uint_as_float(dr[2 * c + e]) - rho);
+            const float pr = (live && ok) ? ex2_approx(fmaf(__uint_as_float(sr[cc]), sl2, bias - lse)) : 0.f;
+            dv[e] = pr * (__uint_as_float(dr[cc]) - rho);
           }
           pk[c] = pack_bf16x2(dv[0], dv[1]);
         }
         tmem_st16(t_s + 64 + ch * 16, pk);
+      };
+      if (cent) {
+#pragma unroll 1
+        for (int ch = 3; ch >= 0; --ch) chunk(ch, std::true_type{});
+      } else {
+#pragma unroll 1
+        for (int ch = 3; ch >= 0; --ch) chunk(ch, std::false_type{});
       }
       tmem_st_wait();
       tc_fence_before();
