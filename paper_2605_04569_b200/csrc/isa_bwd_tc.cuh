@@ -16,8 +16,10 @@
 //     columns already read)
 //   dV  += P^T dO    (TS, TMEM cols [256,384); dO tile read MN-major)
 //   dK  += dS^T Q    (TS, TMEM cols [384,512); Q tile read MN-major)
-// Warps: 0-3 softmax + epilogue, 4 TMEM alloc + MMA issue, 5 TMA producer
-// (+ per-query lse/rho rows into shared memory).
+// Warps: 0-7 softmax + epilogue (two warps per TMEM lane quadrant: warps 0-3
+// take query columns 64-127, warps 4-7 columns 0-63, so every SM
+// sub-partition runs two independent softmax streams), 8 TMEM alloc + MMA
+// issue, 9 TMA producer (+ per-query lse/rho rows into shared memory).
 #pragma once
 #include <type_traits>
 
@@ -43,7 +45,7 @@ struct BwdTcSmem {
 };
 
 template <int D>
-__global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
+__global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                                                             const __grid_constant__ CUtensorMap tm_k,
                                                             const __grid_constant__ CUtensorMap tm_v,
                                                             const __grid_constant__ CUtensorMap tm_do,
@@ -81,7 +83,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
       mbar_init(&qo_empty[s], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
+    mbar_init(p_full, 8);
     mbar_init(d_full, 1);
     fence_barrier_init();
   }
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
       sVis[at] = v0 | (v1 << 1);
     }
   }
-  if (warp == 4) tmem_alloc<512>(tmem_slot);
+  if (warp == 8) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
   const int n_list = p.n_sharp + *s_count;
   const int n_tiles = (n_list + 1) >> 1;
 
-  if (warp == 5) {
+  if (warp == 9) {
     // ---------------------------------------------------------------- TMA producer
     const bool leader = elect_one();
     const uint64_t pol = policy_evict_last();
@@ -124,34 +126,51 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
         }
       }
     }
-    for (int t = 0; t < n_tiles; ++t) {
-      const int slot = t & 1;
-      if (t >= 2) mbar_wait(&qo_empty[slot], ((t >> 1) - 1) & 1);
-      __syncwarp();
-      float* st = sStats + slot * 256;
-      int u[2], vq[2];
+    // Per-tile query info (block ids, lse/rho rows: lane holds rows lane + 32k)
+    // is loaded one tile ahead into registers, so its dependent global loads
+    // overlap the wait for the slot instead of delaying the TMA issue.
+    struct Info {
+      int u[2];
+      float ls[4], rh[4];
+    };
+    auto fetch = [&](int t, Info& in) {
+      int vq[2];
       for (int h = 0; h < 2; ++h) {
         const int li = 2 * t + h;
-        if (li < n_list) {
+        if (t < n_tiles && li < n_list) {
           const int x = sList[li];
-          u[h] = x < p.n_sharp ? p.sharp[bh * p.n_sharp + x] : p.flat[bh * p.n_flat + (x - p.n_sharp)];
-          vq[h] = bw_valid(p, u[h]);
+          in.u[h] = x < p.n_sharp ? p.sharp[bh * p.n_sharp + x] : p.flat[bh * p.n_flat + (x - p.n_sharp)];
+          vq[h] = bw_valid(p, in.u[h]);
         } else {
-          u[h] = -1;
+          in.u[h] = -1;
           vq[h] = 0;
         }
       }
-      // per-query softmax statistics (lse = -inf masks missing / padded rows)
-      for (int r = lane; r < 128; r += 32) {
-        const int h = r >> 6, rr = r & 63;
-        float ls = -INFINITY, rh = 0.f;
-        if (u[h] >= 0 && rr < vq[h]) {
-          const long long row = (long long)bh * p.S + bw_tok0(p, u[h]) + rr;
-          ls = p.lse[row];
-          rh = p.rho[row];
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {  // lse = -inf masks missing / padded rows
+        const int r = lane + 32 * k4, h = r >> 6, rr = r & 63;
+        in.ls[k4] = -INFINITY;
+        in.rh[k4] = 0.f;
+        if (in.u[h] >= 0 && rr < vq[h]) {
+          const long long row = (long long)bh * p.S + bw_tok0(p, in.u[h]) + rr;
+          in.ls[k4] = p.lse[row];
+          in.rh[k4] = p.rho[row];
         }
-        st[r] = ls;
-        st[128 + r] = rh;
+      }
+    };
+    Info cur, nxt;
+    fetch(0, nxt);
+    for (int t = 0; t < n_tiles; ++t) {
+      const int slot = t & 1;
+      cur = nxt;
+      fetch(t + 1, nxt);  // loads in flight during the wait below
+      if (t >= 2) mbar_wait(&qo_empty[slot], ((t >> 1) - 1) & 1);
+      __syncwarp();
+      float* st = sStats + slot * 256;
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        st[lane + 32 * k4] = cur.ls[k4];
+        st[128 + lane + 32 * k4] = cur.rh[k4];
       }
       __syncwarp();
       __threadfence_block();
@@ -159,7 +178,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
         mbar_arrive_expect_tx(&qo_full[slot], 2 * L::kTile);
         uint8_t* dq_ = smem + L::kQO + slot * 2 * L::kTile;
         for (int h = 0; h < 2; ++h) {
-          const int uu = u[h] >= 0 ? u[h] : u[0];
+          const int uu = cur.u[h] >= 0 ? cur.u[h] : cur.u[0];
           const int tok = bw_tok0(p, uu);
           for (int pl = 0; pl < D / 64; ++pl) {
             tma_load_4d(dq_ + pl * 16384 + h * 8192, &tm_q, &qo_full[slot], pl * 64, tok, hh, bb, pol);
@@ -169,7 +188,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
         }
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == 8) {
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128, 0, 0);
     constexpr uint32_t idesc_g = idesc_bf16_f32(128, D, 0, 1);
@@ -225,15 +244,17 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
     __syncwarp();
   } else {
     // ---------------------------------------------------------------- softmax (thread = key row)
-    const int row = warp * 32 + lane;
+    const int grp = warp >> 2;        // 0: query columns 64-127, 1: columns 0-63
+    const int row = (warp & 3) * 32 + lane;
     const int kh = row >> 6;          // key half: 0 -> j0, 1 -> j1
     const int j = kh ? j1 : j0;
     const bool key_exists = kh == 0 || has1;
     const int uk = key_exists ? tab[j] : tab[j0];
     const bool key_ok = key_exists && (row & 63) < bw_valid(p, uk);
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t t_s = tmem + lane_base, t_dp = tmem + lane_base + 128;
     const float sl2 = p.sl2;
+    const int c_hi = grp == 0 ? 3 : 1;  // this group's chunks: c_hi, c_hi - 1
     for (int t = 0; t < n_tiles; ++t) {
       const int slot = t & 1;
       const float* st = sStats + slot * 256;
@@ -247,14 +268,21 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
       mbar_wait(s_full, t & 1);
       __syncwarp();
       tc_fence_after();
-#pragma unroll 1
-      for (int ch = 3; ch >= 0; --ch) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32(t_s + ch * 32, sr);
-        tmem_ld32(t_dp + ch * 32, dr);
-        tmem_ld_wait();
-        const bool v = vis[ch >> 1];
-        uint32_t pk[16], dk[16];
+      uint32_t sr[2][32], dr[2][32];
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        tmem_ld32(t_s + (c_hi - k2) * 32, sr[k2]);
+        tmem_ld32(t_dp + (c_hi - k2) * 32, dr[k2]);
+      }
+      tmem_ld_wait();
+      // group 0's columns 64-95 are where group 1's packed P^T / dS^T land:
+      // group 0 signals once they are in registers, group 1 waits before storing
+      if (grp == 0) named_bar_arrive(1, 256);
+      const bool v = vis[grp == 0 ? 1 : 0];
+      uint32_t pk[2][16], dk[2][16];
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const int ch = c_hi - k2;
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
           const int q0 = ch * 32 + 2 * c;
@@ -262,15 +290,21 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const float ls = st[q0 + e];
-            const float pr = (v && ls > -INFINITY) ? ex2_approx(fmaf(__uint_as_float(sr[2 * c + e]), sl2, -ls)) : 0.f;
+            const float pr =
+                (v && ls > -INFINITY) ? ex2_approx(fmaf(__uint_as_float(sr[k2][2 * c + e]), sl2, -ls)) : 0.f;
             pv[e] = pr;
-            dv[e] = pr * (__uint_as_float(dr[2 * c + e]) - st[128 + q0 + e]);
+            dv[e] = pr * (__uint_as_float(dr[k2][2 * c + e]) - st[128 + q0 + e]);
           }
-          pk[c] = pack_bf16x2(pv[0], pv[1]);
-          dk[c] = pack_bf16x2(dv[0], dv[1]);
+          pk[k2][c] = pack_bf16x2(pv[0], pv[1]);
+          dk[k2][c] = pack_bf16x2(dv[0], dv[1]);
         }
-        tmem_st16(t_s + 64 + ch * 16, pk);
-        tmem_st16(t_dp + 64 + ch * 16, dk);
+      }
+      if (grp == 1) named_bar_sync(1, 256);
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {
+        const int ch = c_hi - k2;
+        tmem_st16(t_s + 64 + ch * 16, pk[k2]);
+        tmem_st16(t_dp + 64 + ch * 16, dk[k2]);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -285,7 +319,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
     const float invw = 1.f / (float)bw_valid(p, uk);
     const long long cb = ((long long)bh * p.t_new + j) * D;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = grp * (D / 64); c < (grp + 1) * (D / 64); ++c) {  // each group stores half the columns
       uint32_t vr[32], kr[32];
       __syncwarp();
       tmem_ld32(tmem + lane_base + 256 + c * 32, vr);
@@ -313,7 +347,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dkv_tc_kernel(const __grid_constan
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }

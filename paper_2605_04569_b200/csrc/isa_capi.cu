@@ -813,7 +813,7 @@ int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps,
     static size_t cur_tc = 48 * 1024;
     if ((rc = ensure_smem((const void*)isa::bwd_dkv_tc_kernel<D>, sm_tc, &cur_tc))) return rc;
     isa::BwdTcParams tp{bp, n_list};
-    isa::bwd_dkv_tc_kernel<D><<<dim3((d.t_new + 1) / 2, d.BH), 192, sm_tc, st>>>(maps[0], maps[1], maps[2], maps[3], tp);
+    isa::bwd_dkv_tc_kernel<D><<<dim3((d.t_new + 1) / 2, d.BH), 320, sm_tc, st>>>(maps[0], maps[1], maps[2], maps[3], tp);
     ISA_LAUNCHED("bwd_dkv_tc_kernel");
   }
   if (bwd_mmasync()) {
