@@ -700,8 +700,9 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         // masked_tag: std::true_type only on the centroid path, so the per-column
         // exclusion selects exist in that copy of the code alone (a runtime flag
         // gets if-converted into 128 SELs on every tile)
-        auto chunk = [&](const int ch, auto masked_tag) {
+        auto chunk = [&](const int ch, auto masked_tag, auto emu_tag) {
           constexpr bool kMasked = decltype(masked_tag)::value;
+          constexpr int kEmu = decltype(emu_tag)::value;
           uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
@@ -717,7 +718,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
 #endif
             const float2 tt = ffma2(make_float2(xa, xb), sl2x2, nb2);
             float2 pp;
-            if (kEmuEvery > 0 && (c % kEmuEvery) == kEmuEvery - 1) {
+            if (kEmu > 0 && (c % kEmu) == kEmu - 1) {
               pp = ex2_emu2(tt);
             } else {
               pp.x = ex2_approx(tt.x);
@@ -728,6 +729,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           }
           tmem_st16(t_p + 16 * ch, pk);
         };
+        using EmuStd = std::integral_constant<int, kEmuEvery>;
         auto zero = [&](const int ch) {
           uint32_t pk[16];
 #pragma unroll
@@ -738,20 +740,20 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         if (MODE == MODE_TAYLOR && cmask) {  // Taylor centroid tile
           add_members();
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) chunk(ch, std::true_type{});
+          for (int ch = 0; ch < 4; ++ch) chunk(ch, std::true_type{}, EmuStd{});
         } else if (MODE != MODE_TAYLOR || dense) {  // every K6/K8 tile: one straight-line schedule
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) chunk(ch, plain);
+          for (int ch = 0; ch < 4; ++ch) chunk(ch, plain, EmuStd{});
         } else if (half0) {  // Taylor union tile, only the first 64 keys listed (warp-uniform):
-          chunk(0, plain);   // straight-line code per case so the two chunks interleave
-          chunk(1, plain);
+          chunk(0, plain, EmuStd{});  // straight-line code per case so the two chunks interleave
+          chunk(1, plain, EmuStd{});
           zero(2);
           zero(3);
         } else {
           zero(0);
           zero(1);
-          chunk(2, plain);
-          chunk(3, plain);
+          chunk(2, plain, EmuStd{});
+          chunk(3, plain, EmuStd{});
         }
 #ifdef ISA_TRACE_SPEC
         if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 2);
