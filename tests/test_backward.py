@@ -65,3 +65,26 @@ def test_backward_numpy_io_and_pinned_routing():
     g3 = P.isa_backward(*dev[:3], icl, cfg, dev[3])
     for n in ("dq", "dk", "dv"):
         assert torch.equal(getattr(g2, n), getattr(g3, n))
+
+
+@pytest.mark.gpu
+def test_backward_strided_inputs_and_fp32():
+    """(B,S,H,D)-strided bf16 inputs give the same gradients as contiguous ones;
+    fp32 inputs are computed in bf16 and returned as fp32."""
+    import torch
+
+    import paper_2605_04569_b200 as P
+
+    m, (q, k, v, do), ref = _case(BWD_CASES[0])
+    icl, cfg = P.IclLayout(m["l_src"], m["l_ctx"]), P.IsaConfig(**m["cfg"])
+    dev = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k, v, do)]
+    g = P.isa_backward(*dev[:3], icl, cfg, dev[3])
+    strided = [t.permute(0, 2, 1, 3).contiguous().permute(0, 2, 1, 3) for t in dev]
+    assert not strided[0].is_contiguous()
+    gs = P.isa_backward(*strided[:3], icl, cfg, strided[3])
+    for n in ("dq", "dk", "dv"):
+        assert torch.equal(getattr(g, n), getattr(gs, n))
+    g32 = P.isa_backward(*(t.float() for t in dev[:3]), icl, cfg, dev[3].float())
+    assert g32.dq.dtype == torch.float32
+    for n in ("dq", "dk", "dv"):  # same fp32 gradients; the bf16 call rounds them on return
+        assert torch.equal(getattr(g32, n).to(torch.bfloat16), getattr(g, n))
