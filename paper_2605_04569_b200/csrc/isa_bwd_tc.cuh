@@ -65,7 +65,10 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
   int* s_count = reinterpret_cast<int*>(bars + 9);
   int* sList = reinterpret_cast<int*>(smem + L::kList);     // query-block position (x < n_sharp: sharp)
   int* sVis = sList + tp.n_list_max;                          // bit0: lists j0, bit1: lists j1
-  float* sStats = reinterpret_cast<float*>(smem + L::kStats);
+  // per-query statistics [2 slots][lse 128 | rho 128]: a static __shared__
+  // array so the per-element reads compile to LDS (the aligned dynamic-smem
+  // pointer is generic to the compiler, which made them LD.E)
+  __shared__ float sStats[2 * 256];
 
   const int bh = blockIdx.y;
   const int hh = bh % p.H, bb = bh / p.H;
@@ -168,8 +171,8 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
       __syncwarp();
       float* st = sStats + slot * 256;
 #pragma unroll
-      for (int k4 = 0; k4 < 4; ++k4) {
-        st[lane + 32 * k4] = cur.ls[k4];
+      for (int k4 = 0; k4 < 4; ++k4) {  // -lse (-inf for missing rows: p = 0 with no predicate)
+        st[lane + 32 * k4] = cur.ls[k4] > -INFINITY ? -cur.ls[k4] : -INFINITY;
         st[128 + lane + 32 * k4] = cur.rh[k4];
       }
       __syncwarp();
@@ -232,13 +235,16 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
     for (int t = 0; t < n_tiles; ++t) {
       const int slot = t & 1;
       mbar_wait(&qo_full[slot], (t >> 1) & 1);
+      if (leader) ISA_TSTAMP(t, 0, 5);
       __syncwarp();
       tc_fence_after();
       issue_sd(slot);
       mbar_wait(p_full, t & 1);
+      if (leader) ISA_TSTAMP(t, 0, 6);
       __syncwarp();
       tc_fence_after();
       issue_g(slot, t > 0);
+      if (leader) ISA_TSTAMP(t, 0, 7);
     }
     if (leader) mma_commit(d_full);
     __syncwarp();
@@ -266,6 +272,7 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
       }
       mbar_wait(&qo_full[slot], (t >> 1) & 1);  // the producer's lse/rho rows of this tile
       mbar_wait(s_full, t & 1);
+      if (warp == 0 && lane == 0) ISA_TSTAMP(t, 0, 0);
       __syncwarp();
       tc_fence_after();
       uint32_t sr[2][32], dr[2][32];
@@ -276,40 +283,44 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
       }
       tmem_ld_wait();
       // group 0's columns 64-95 are where group 1's packed P^T / dS^T land:
-      // group 0 signals once they are in registers, group 1 waits before storing
-      if (grp == 0) named_bar_arrive(1, 256);
-      const bool v = vis[grp == 0 ? 1 : 0];
-      uint32_t pk[2][16], dk[2][16];
+      // group 0 signals once both its chunks are in registers, group 1 waits
+      // before its first store; each chunk is then computed and stored in turn
+      if (grp == 0)
+        named_bar_arrive(1, 256);
+      else
+        named_bar_sync(1, 256);
+      const bool v = vis[grp == 0 ? 1 : 0];  // uniform per warp (one key half, one query half)
 #pragma unroll
       for (int k2 = 0; k2 < 2; ++k2) {
         const int ch = c_hi - k2;
+        uint32_t pk[16], dk[16];
+        if (v) {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int q0 = ch * 32 + 2 * c;
-          float pv[2], dv[2];
+          for (int c = 0; c < 16; ++c) {
+            const int q0 = ch * 32 + 2 * c;
+            float pv[2], dv[2];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const float ls = st[q0 + e];
-            const float pr =
-                (v && ls > -INFINITY) ? ex2_approx(fmaf(__uint_as_float(sr[k2][2 * c + e]), sl2, -ls)) : 0.f;
-            pv[e] = pr;
-            dv[e] = pr * (__uint_as_float(dr[k2][2 * c + e]) - st[128 + q0 + e]);
+            for (int e = 0; e < 2; ++e) {
+              const float pr = ex2_approx(fmaf(__uint_as_float(sr[k2][2 * c + e]), sl2, st[q0 + e]));
+              pv[e] = pr;
+              dv[e] = pr * (__uint_as_float(dr[k2][2 * c + e]) - st[128 + q0 + e]);
+            }
+            pk[c] = pack_bf16x2(pv[0], pv[1]);
+            dk[c] = pack_bf16x2(dv[0], dv[1]);
           }
-          pk[k2][c] = pack_bf16x2(pv[0], pv[1]);
-          dk[k2][c] = pack_bf16x2(dv[0], dv[1]);
-        }
-      }
-      if (grp == 1) named_bar_sync(1, 256);
+        } else {
 #pragma unroll
-      for (int k2 = 0; k2 < 2; ++k2) {
-        const int ch = c_hi - k2;
-        tmem_st16(t_s + 64 + ch * 16, pk[k2]);
-        tmem_st16(t_dp + 64 + ch * 16, dk[k2]);
+          for (int c = 0; c < 16; ++c) pk[c] = dk[c] = 0u;
+        }
+        tmem_st16(t_s + 64 + ch * 16, pk);
+        tmem_st16(t_dp + 64 + ch * 16, dk);
       }
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if (warp == 0 && lane == 0) ISA_TSTAMP(t, 0, 4);
+      if (warp == 4 && lane == 0) ISA_TSTAMP(t, 1, 4);
     }
     // ---------------------------------------------------------------- epilogue
     mbar_wait(d_full, 0);
@@ -394,8 +405,8 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
   uint64_t* p_full = bars + 6;
   uint64_t* d_full = bars + 7;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
-  float* sCol = reinterpret_cast<float*>(smem + L::kCol);
-  int* sMeta = reinterpret_cast<int*>(smem + L::kMeta);
+  __shared__ float sCol[2 * 128];  // [2 slots][128] column bias (centroid tiles)
+  __shared__ int sMeta[2 * 4];     // [2 slots]: centroid flag, tile index, meta0, meta1
 
   const int bh = blockIdx.y;
   const int hh = bh % p.H, bb = bh / p.H;
@@ -565,6 +576,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
     const float lse = row_ok ? p.lse[grow] : -INFINITY;
     const float rho = row_ok ? p.rho[grow] : 0.f;
     const bool live = row_ok && lse > -INFINITY;
+    const float lse_eff = live ? lse : INFINITY;  // dead rows: exp2(-inf) = 0, no per-element predicate
     const uint32_t* mb = (flat && uq >= 0) ? p.bits + ((long long)bh * p.n_flat + 4 * item + 2 * stg + qh) * p.W
                                            : nullptr;
     const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
@@ -604,15 +616,12 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int cc = 2 * c + e;  // column within the chunk
-            float bias = 0.f;
-            bool ok;
-            if (kCent) {
-              bias = sCol[slot * 128 + ch * 32 + cc];
-              ok = !((cw >> cc) & 1u);
-            } else {
-              ok = cc < lim;
-            }
-            const float pr = (live && ok) ? ex2_approx(fmaf(__uint_as_float(sr[cc]), sl2, bias - lse)) : 0.f;
+            float bias;
+            if (kCent)
+              bias = ((cw >> cc) & 1u) ? -INFINITY : sCol[slot * 128 + ch * 32 + cc];
+            else
+              bias = cc < lim ? 0.f : -INFINITY;
+            const float pr = ex2_approx(fmaf(__uint_as_float(sr[cc]), sl2, bias - lse_eff));
             dv[e] = pr * (__uint_as_float(dr[cc]) - rho);
           }
           pk[c] = pack_bf16x2(dv[0], dv[1]);
