@@ -145,7 +145,8 @@ int isa_forward_host(const IsaShape* shape, const IsaKnobs* knobs, const void* q
                      void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
                      int32_t* err_word, void* const* streams);
 
-/* Backward with frozen routing (isa_backward, pipeline.py:373-466; gamma = 0):
+/* Backward with frozen routing (isa_backward, pipeline.py:373-466, incl. the
+ * gamma coarse residual through the block means, pipeline.py:435-452):
  * recomputes the forward (routing from q/k, or `pinned`) with its per-row
  * softmax statistics, then the sharp-branch (reference.py:173-225) and Taylor
  * (taylor.py:225-296) gradients, scattered back through the K_new gather

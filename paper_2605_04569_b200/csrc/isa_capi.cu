@@ -757,11 +757,14 @@ struct BwdWs {
   Workspace fw;
   __nv_bfloat16* o;
   float *lse, *rho, *dkc, *dvc;
+  float *g_doc, *g_stats, *g_dqc, *g_dkc, *g_dvc;  // gamma residual (gamma > 0 only)
   size_t bytes;
 };
 
-BwdWs carve_bwd(const Dims& d, uint8_t* base) {
+BwdWs carve_bwd(const Dims& d0, uint8_t* base) {
   BwdWs b{};
+  Dims d = d0;
+  d.gamma = 0.0;  // the forward recompute runs without the residual (rho uses the attention output)
   b.fw = carve(d, ISA_DTYPE_BF16, base);
   size_t off = b.fw.bytes;
   auto take = [&](size_t n) {
@@ -775,6 +778,13 @@ BwdWs carve_bwd(const Dims& d, uint8_t* base) {
   b.rho = reinterpret_cast<float*>(take(4ull * BH * d.S));
   b.dkc = reinterpret_cast<float*>(take(4ull * BH * d.t_new * d.D));
   b.dvc = reinterpret_cast<float*>(take(4ull * BH * d.t_new * d.D));
+  if (d0.gamma > 0.0) {
+    b.g_doc = reinterpret_cast<float*>(take(4ull * BH * d.T * d.D));
+    b.g_stats = reinterpret_cast<float*>(take(12ull * BH * d.T));
+    b.g_dqc = reinterpret_cast<float*>(take(4ull * BH * d.T * d.D));
+    b.g_dkc = reinterpret_cast<float*>(take(4ull * BH * d.T * d.D));
+    b.g_dvc = reinterpret_cast<float*>(take(4ull * BH * d.T * d.D));
+  }
   b.bytes = off;
   return b;
 }
@@ -877,7 +887,6 @@ int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, co
   int rc = derive(shape, knobs, &d);
   if (rc) return rc;
   if (shape->dtype != ISA_DTYPE_BF16) return fail(ISA_ERR_CONFIG, "isa_backward takes bf16 q/k/v/dO");
-  if (d.gamma > 0.0) return fail(ISA_ERR_CONFIG, "isa_backward: gamma > 0 is not implemented");
   if ((rc = check_io(shape, q, k, v))) return rc;
   if ((rc = check_io(shape, dout, dout, dout))) return rc;
   if (!dq || !dk || !dv) return fail(ISA_ERR_LAYOUT, "null gradient buffers");
@@ -885,10 +894,15 @@ int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, co
   if (!workspace || workspace_bytes < b.bytes)
     return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, b.bytes);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // forward recompute with the softmax statistics (routing frozen by determinism or `pinned`)
+  // forward recompute with the softmax statistics (routing frozen by determinism or `pinned`);
+  // without the gamma residual: rho must see the attention output alone (taylor.py:274)
   IsaShape os = *shape;
   os.out_stride_b = os.out_stride_h = os.out_stride_s = 0;  // O into the workspace, contiguous
-  if ((rc = forward_impl(&os, knobs, d, q, k, v, b.o, b.fw, pinned, nullptr, err_word, nullptr, b.lse, st)))
+  IsaKnobs kf = *knobs;
+  kf.gamma = 0.0;
+  Dims df = d;
+  df.gamma = 0.0;
+  if ((rc = forward_impl(&os, &kf, df, q, k, v, b.o, b.fw, pinned, nullptr, err_word, nullptr, b.lse, st)))
     return rc;
   int launches = g_launches;
   const size_t gbytes = 4ull * d.BH * d.S * d.D;
@@ -949,7 +963,45 @@ int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, co
   g_launches = 0;
   rc = d.D == 128 ? launch_bwd<128>(bp, d, maps, b.fw, st) : launch_bwd<64>(bp, d, maps, b.fw, st);
   g_launches += launches;
-  return rc;
+  if (rc || !(d.gamma > 0.0)) return rc;
+  // gamma coarse residual (pipeline.py:435-452) on the block means of the recompute
+  isa::GammaBwdParams gp{};
+  gp.H = d.H;
+  gp.S = d.S;
+  gp.D = d.D;
+  gp.T = d.T;
+  gp.t_src = d.t_src;
+  gp.l_src = d.l_src;
+  gp.l_ctx = d.l_ctx;
+  gp.gamma = static_cast<float>(d.gamma);
+  gp.scale = static_cast<float>(d.scale);
+  gp.softmax = d.resid_softmax;
+  gp.dout = static_cast<const __nv_bfloat16*>(dout);
+  gp.db = shape->stride_b;
+  gp.dh = shape->stride_h;
+  gp.ds = shape->stride_s;
+  gp.qc = b.fw.means;
+  gp.kc = b.fw.means + (long long)d.BH * d.T * d.D;
+  gp.vc = b.fw.means + 2ll * d.BH * d.T * d.D;
+  gp.doc = b.g_doc;
+  gp.m = b.g_stats;
+  gp.l = b.g_stats + (long long)d.BH * d.T;
+  gp.rho = b.g_stats + 2ll * d.BH * d.T;
+  gp.dqc = b.g_dqc;
+  gp.dkc = b.g_dkc;
+  gp.dvc = b.g_dvc;
+  gp.dq = dq;
+  gp.dk = dk;
+  gp.dv = dv;
+  isa::gamma_doc_kernel<<<dim3(d.T, d.BH), d.D, 0, st>>>(gp);
+  ISA_LAUNCHED("gamma_doc_kernel");
+  isa::gamma_row_kernel<<<dim3((d.T + 3) / 4, d.BH), 128, 0, st>>>(gp);
+  ISA_LAUNCHED("gamma_row_kernel");
+  isa::gamma_col_kernel<<<dim3((d.T + 3) / 4, d.BH), 128, 0, st>>>(gp);
+  ISA_LAUNCHED("gamma_col_kernel");
+  isa::gamma_spread_kernel<<<dim3(d.T, d.BH), d.D, 0, st>>>(gp);
+  ISA_LAUNCHED("gamma_spread_kernel");
+  return ISA_OK;
 }
 
 int isa_dense_attention(const IsaShape* shape, double scale, const void* q, const void* k, const void* v, void* out,

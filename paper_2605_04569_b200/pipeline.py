@@ -398,7 +398,7 @@ def isa_forward_with_routing(q, k, v, icl: IclLayout, cfg: IsaConfig, routing) -
 
 def isa_backward(q, k, v, icl: IclLayout, cfg: IsaConfig, do, *, routing=None) -> GradBundle:
     """Gradients of isa_forward with routing frozen at this forward's decisions
-    (pipeline.py:373-466, same signature; gamma = 0). `routing` optionally pins
+    (pipeline.py:373-466, same signature, incl. the gamma residual). `routing` optionally pins
     the decisions (ours or the reference's IsaRouting). Computes in bf16 tensor
     arithmetic with fp32 accumulation; returns tensors in q's dtype (numpy fp32
     for numpy inputs)."""

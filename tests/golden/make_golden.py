@@ -130,6 +130,9 @@ BWD_CASES = [
     ("bwd_clustered_d128_s21", "clustered", 1, 1, 2048, 128, 1024, 1024, 21, {}),
     ("bwd_ragged_s22", "iid-gaussian", 1, 2, 1500, 64, 900, 600, 22, {"strict": False, "alpha_s": 0.5}),
     ("bwd_knobs_s23", "lowrank", 2, 1, 2048, 64, 1024, 1024, 23, {"alpha_f": 0.75, "alpha_ns": 0.25}),
+    ("bwd_gamma_s24", "clustered", 1, 2, 2048, 64, 1024, 1024, 24, {"gamma": 0.5}),
+    ("bwd_gamma_raw_s25", "iid-gaussian", 1, 1, 1500, 128, 900, 600, 25,
+     {"gamma": 0.05, "residual_softmax": False, "strict": False}),
 ]
 
 
