@@ -64,10 +64,12 @@ __global__ void __launch_bounds__(128) pool_means_kernel(const Tin* __restrict__
   bool finite = true;
   const Tin* base = x + b * sb + h * sh + (long long)tok0 * ss + col;
   constexpr int WAVES = 64 / RPW;
-#pragma unroll 8
-  for (int w = 0; w < WAVES; ++w) {
+  // full blocks (every block in strict mode): no per-wave exit, so all loads
+  // of a 16-wave group are in flight together
+  const int nw = valid == 64 ? WAVES : (valid - r0 + RPW - 1) / RPW;
+#pragma unroll 16
+  for (int w = 0; w < nw; ++w) {
     const int r = r0 + w * RPW;
-    if (r >= valid) break;
     const Tin* rowp = base + (long long)r * ss;
     float f[VEC];
     if constexpr (sizeof(Tin) == 2) {
