@@ -131,7 +131,7 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
 
 /* Host-streamed pipeline: q/k/v/out are HOST pointers (contiguous (B,H,S,D);
  * page-locked for copy/compute overlap). The flattened (b,h) range is processed
- * in chunks of `heads_per_chunk` heads (<= 0: ceil(B*H/8)); the H2D copy of
+ * in chunks of `heads_per_chunk` heads (<= 0: about 150 MB of inputs); the H2D copy of
  * chunk c+1 (streams[1]) and the D2H copy of chunk c-1 (streams[2]) overlap the
  * device pipeline of chunk c (streams[0]). streams[0] completes after the last
  * D2H. `stage` (device, caller-owned) and `workspace` are sized by

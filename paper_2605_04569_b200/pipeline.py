@@ -364,7 +364,7 @@ def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = T
     computed with bf16 tensor cores and fp32 accumulation). Routing decisions
     are exact float64 restatements of the reference and match it bit-for-bit.
     Host inputs (numpy / CPU tensors) are streamed through the GPU in chunks of
-    `heads_per_chunk` heads (0 = B*H/8); the result is complete on return.
+    `heads_per_chunk` heads (0 = about 150 MB of inputs); the result is complete on return.
     """
     res, trace, _ = _run(_Inputs(q, k, v, icl, cfg), collect_trace, out=out, validate=validate,
                          heads_per_chunk=heads_per_chunk)
