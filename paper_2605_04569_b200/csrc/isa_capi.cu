@@ -230,6 +230,20 @@ unsigned grid1d(long long n, int threads) {
   return static_cast<unsigned>(g < 1 ? 1 : (g > 65535 * 16 ? 65535 * 16 : g));
 }
 
+template <int D>
+int launch_resid_tiled(dim3 g, const float* qc, const float* kc, const float* vc, const Dims& d, float* out,
+                       cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::coarse_residual_tiled_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)isa::ResidTile<D>::kBytes));
+    configured = true;
+  }
+  isa::coarse_residual_tiled_kernel<D><<<g, 256, isa::ResidTile<D>::kBytes, st>>>(qc, kc, vc, d.T, (float)d.scale,
+                                                                                 d.resid_softmax, out);
+  return ISA_OK;
+}
+
 template <int D, int MODE>
 int launch_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
                      const CUtensorMap& tvc, const isa::AttnParams& p, int items, int BH, cudaStream_t st) {
@@ -494,12 +508,20 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
     ISA_LAUNCHED("ctx_score_kernel");
   }
   if (d.gamma > 0.0) {  // coarse residual rows (pipeline.py:261-267), consumed by the attention epilogues
-    dim3 g((d.T + 15) / 16, d.BH);
-    if (d.D == 128)
-      isa::coarse_residual_kernel<128><<<g, 128, 0, st>>>(qc, kc, vc, d.T, (float)d.scale, d.resid_softmax, w.resid);
-    else
-      isa::coarse_residual_kernel<64><<<g, 128, 0, st>>>(qc, kc, vc, d.T, (float)d.scale, d.resid_softmax, w.resid);
-    ISA_LAUNCHED("coarse_residual_kernel");
+    if (getenv("ISA_RESID_WARP")) {  // A/B: the warp-per-row kernel
+      dim3 g((d.T + 15) / 16, d.BH);
+      if (d.D == 128)
+        isa::coarse_residual_kernel<128><<<g, 128, 0, st>>>(qc, kc, vc, d.T, (float)d.scale, d.resid_softmax, w.resid);
+      else
+        isa::coarse_residual_kernel<64><<<g, 128, 0, st>>>(qc, kc, vc, d.T, (float)d.scale, d.resid_softmax, w.resid);
+      ISA_LAUNCHED("coarse_residual_kernel");
+    } else {
+      dim3 g((d.T + 63) / 64, d.BH);
+      if ((rc = d.D == 128 ? launch_resid_tiled<128>(g, qc, kc, vc, d, w.resid, st)
+                           : launch_resid_tiled<64>(g, qc, kc, vc, d, w.resid, st)))
+        return rc;
+      ISA_LAUNCHED("coarse_residual_tiled_kernel");
+    }
   }
   record(ev, 1, st);
   // ---- stage 2: select (context top-k, K_new block table, fp64 scores vs K_new, centroids)

@@ -747,6 +747,162 @@ __global__ void __launch_bounds__(128) coarse_residual_kernel(const float* __res
 }
 
 // ----------------------------------------------------------------------------
+// Coarse residual, register-tiled (same math as coarse_residual_kernel above):
+// a small fp32 flash attention of the T block means per head. CTA = 64 query
+// blocks x all T key blocks in tiles of 64, 256 threads; thread (ty, tx) owns
+// query rows 4ty..4ty+3, keys tx + 16kk (kk < 4) of S and output columns
+// 4tx + 64cc (cc < D/64) of O. Q/K/V tiles are row-major in shared memory
+// (row stride D+4 floats: the float4 reads of 8 consecutive tx hit 8
+// distinct bank quads, the Q reads broadcast); P^T is written into the dead
+// K tile. 16 FMA per 2 LDS.128 in both products. Rows / keys past T are
+// zero-filled; softmax masks keys past T with -inf (raw: zero K and V rows
+// contribute 0). grid (ceil(T/64), BH), 101 KB smem at D=128 (2 CTAs / SM).
+// ----------------------------------------------------------------------------
+template <int D>
+struct ResidTile {
+  static constexpr int kRow = D + 4;            // padded row, floats
+  static constexpr int kQ = 0;                  // Q tile [64][kRow]
+  static constexpr int kK = 64 * kRow;          // K tile [64][kRow]; P^T [64][68] after S
+  static constexpr int kV = 2 * 64 * kRow;      // V tile [64][kRow]
+  static constexpr int kFloats = 3 * 64 * kRow;
+  static constexpr size_t kBytes = sizeof(float) * kFloats;
+};
+
+template <int D>
+__device__ __forceinline__ void resid_load_rows(float* dst, const float* __restrict__ src, int row0, int T) {
+  constexpr int kV4 = D / 4;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < 64 * kV4; e += 256) {
+    const int r = e / kV4, c = (e % kV4) * 4;
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row0 + r < T) x = *reinterpret_cast<const float4*>(src + (long long)(row0 + r) * D + c);
+    *reinterpret_cast<float4*>(dst + r * ResidTile<D>::kRow + c) = x;
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 2) coarse_residual_tiled_kernel(const float* __restrict__ qc,
+                                                                     const float* __restrict__ kc,
+                                                                     const float* __restrict__ vc, int T,
+                                                                     float scale, int use_softmax,
+                                                                     float* __restrict__ out) {
+  using L = ResidTile<D>;
+  constexpr int kCC = D / 64;  // float4 output column groups per thread
+  constexpr int kPRow = 68;    // P^T row stride
+  extern __shared__ __align__(16) float rsm[];
+  float* sq = rsm + L::kQ;
+  float* sk = rsm + L::kK;
+  float* sv = rsm + L::kV;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long long base = (long long)blockIdx.y * T * D;
+  const int u0 = blockIdx.x * 64;
+  resid_load_rows<D>(sq, qc + base, u0, T);
+  float o[4][kCC][4], m[4], l[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    m[r] = -INFINITY;
+    l[r] = 0.f;
+#pragma unroll
+    for (int cc = 0; cc < kCC; ++cc)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[r][cc][j] = 0.f;
+  }
+  for (int j0 = 0; j0 < T; j0 += 64) {
+    __syncthreads();  // previous tile's P^T / V reads done
+    resid_load_rows<D>(sk, kc + base, j0, T);
+    resid_load_rows<D>(sv, vc + base, j0, T);
+    __syncthreads();
+    float s[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) s[r][kk] = 0.f;
+#pragma unroll 4
+    for (int d = 0; d < D; d += 4) {
+      float4 qv[4], kv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) qv[r] = *reinterpret_cast<const float4*>(sq + (4 * ty + r) * L::kRow + d);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) kv[kk] = *reinterpret_cast<const float4*>(sk + (tx + 16 * kk) * L::kRow + d);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          s[r][kk] = fmaf(qv[r].x, kv[kk].x, s[r][kk]);
+          s[r][kk] = fmaf(qv[r].y, kv[kk].y, s[r][kk]);
+          s[r][kk] = fmaf(qv[r].z, kv[kk].z, s[r][kk]);
+          s[r][kk] = fmaf(qv[r].w, kv[kk].w, s[r][kk]);
+        }
+    }
+    if (use_softmax) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          s[r][kk] = j0 + tx + 16 * kk < T ? s[r][kk] * scale : -INFINITY;
+          mx = fmaxf(mx, s[r][kk]);
+        }
+#pragma unroll
+        for (int off = 1; off < 16; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        const float mn = fmaxf(m[r], mx);
+        const float corr = __expf(m[r] - mn);  // m = -inf -> 0
+        float ps = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          s[r][kk] = __expf(s[r][kk] - mn);
+          ps += s[r][kk];
+        }
+        l[r] = l[r] * corr + ps;  // this thread's partial row sum
+        m[r] = mn;
+#pragma unroll
+        for (int cc = 0; cc < kCC; ++cc)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[r][cc][j] *= corr;
+      }
+    }  // raw variant: p = unscaled dot; keys past T have zero K rows
+    __syncthreads();  // every thread is done reading the K tile
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      *reinterpret_cast<float4*>(sk + (tx + 16 * kk) * kPRow + 4 * ty) =
+          make_float4(s[0][kk], s[1][kk], s[2][kk], s[3][kk]);
+    __syncthreads();
+#pragma unroll 4
+    for (int j = 0; j < 64; ++j) {
+      const float4 p = *reinterpret_cast<const float4*>(sk + j * kPRow + 4 * ty);
+      const float pr[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+      for (int cc = 0; cc < kCC; ++cc) {
+        const float4 v = *reinterpret_cast<const float4*>(sv + j * L::kRow + 64 * cc + 4 * tx);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          o[r][cc][0] = fmaf(pr[r], v.x, o[r][cc][0]);
+          o[r][cc][1] = fmaf(pr[r], v.y, o[r][cc][1]);
+          o[r][cc][2] = fmaf(pr[r], v.z, o[r][cc][2]);
+          o[r][cc][3] = fmaf(pr[r], v.w, o[r][cc][3]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    float inv = 1.f;
+    if (use_softmax) {
+      float lt = l[r];
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) lt += __shfl_xor_sync(0xffffffffu, lt, off);
+      inv = 1.f / lt;
+    }
+    const int u = u0 + 4 * ty + r;
+    if (u >= T) continue;
+#pragma unroll
+    for (int cc = 0; cc < kCC; ++cc)
+      *reinterpret_cast<float4*>(out + base + (long long)u * D + 64 * cc + 4 * tx) =
+          make_float4(o[r][cc][0] * inv, o[r][cc][1] * inv, o[r][cc][2] * inv, o[r][cc][3] * inv);
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Decoupled RoPE (pipeline.py:469-490): position = token index within its
 // segment (source 0..L_src-1, context 0..L_ctx-1); pair i of D/2 rotates by
 // pos * base^(-2i/D). One thread per (token, 4 pairs): the angles are formed
