@@ -22,6 +22,7 @@ runs in libisa_b200.so; there is no CPU path.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import math
 from typing import Optional
 
@@ -356,6 +357,43 @@ def _run(inp: _Inputs, collect_trace: bool, pinned=None, out: Optional[torch.Ten
     return out, trace, bufs
 
 
+def _kernel_width(D: int) -> int:
+    return 64 if D <= 64 else 128
+
+
+def _pad_head_dim(cfg, *xs):
+    """Head dims the kernels are not instantiated for (D < 128, not 64): the D
+    axis is zero-padded to the next kernel width (64 or 128). Zero columns add
+    exact zeros to every dot product (the fp64 block-mean scores included, so
+    routing is unchanged) and V's zero columns only produce output columns that
+    are dropped; the scale stays 1/sqrt(D) of the real width. Returns None when
+    no padding applies, else (cfg with the scale fixed, padded arrays...)."""
+    shape = getattr(xs[0], "shape", None)
+    if shape is None or len(shape) != 4:
+        return None
+    D = int(shape[-1])
+    if D in SUPPORTED_HEAD_DIMS or D > max(SUPPORTED_HEAD_DIMS) or D < 1:
+        return None
+    cfg = cfg_from_any(cfg)
+    cfg = dataclasses.replace(cfg, scale=cfg.scale if cfg.scale is not None else 1.0 / math.sqrt(D))
+    w = _kernel_width(D) - D
+    padded = []
+    for x in xs:
+        if isinstance(x, np.ndarray):
+            padded.append(np.pad(np.asarray(x, dtype=np.float32), ((0, 0),) * 3 + ((0, w),)))
+        elif isinstance(x, torch.Tensor):
+            padded.append(torch.nn.functional.pad(x, (0, w)))
+        else:
+            raise LayoutError("expected torch tensors or numpy arrays")
+    return (cfg, *padded)
+
+
+def _unpad(x, D: int):
+    if isinstance(x, np.ndarray):
+        return np.ascontiguousarray(x[..., :D])
+    return x[..., :D].contiguous()
+
+
 def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = True, *, out=None, validate=True,
                 heads_per_chunk: int = 0):
     """Run the full pipeline; returns (output, IsaTrace or None) (pipeline.py:307-316).
@@ -365,7 +403,21 @@ def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = T
     are exact float64 restatements of the reference and match it bit-for-bit.
     Host inputs (numpy / CPU tensors) are streamed through the GPU in chunks of
     `heads_per_chunk` heads (0 = about 150 MB of inputs); the result is complete on return.
+    Head dims other than 64/128 (up to 128) run zero-padded (`_pad_head_dim`).
     """
+    padded = _pad_head_dim(cfg, q, k, v)
+    if padded is not None:
+        D = int(q.shape[-1])
+        pcfg, pq, pk, pv = padded
+        res, trace = isa_forward(pq, pk, pv, icl, pcfg, collect_trace, validate=validate,
+                                 heads_per_chunk=heads_per_chunk)
+        res = _unpad(res, D)
+        if trace is not None:  # FLOP tallies of the real head dim
+            trace.flops = IsaDims.derive(q.shape, icl_from_any(icl), pcfg).flops()
+        if out is not None:
+            out[...] = res
+            res = out
+        return res, trace
     res, trace, _ = _run(_Inputs(q, k, v, icl, cfg), collect_trace, out=out, validate=validate,
                          heads_per_chunk=heads_per_chunk)
     return res, trace
@@ -373,6 +425,9 @@ def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = T
 
 def isa_routing(q, k, v, icl: IclLayout, cfg: IsaConfig) -> IsaRouting:
     """Stages 1-3 only (pipeline.py:302-304); index tensors stay on the GPU."""
+    padded = _pad_head_dim(cfg, q, k, v)
+    if padded is not None:
+        return isa_routing(*padded[1:], icl, padded[0])
     inp = _Inputs(q, k, v, icl, cfg)
     if inp.host:  # routing reads all of Q/K/V once: one plain upload
         inp = _Inputs(*(t.cuda() for t in (inp.q, inp.k, inp.v)), icl, cfg)
@@ -392,6 +447,9 @@ def isa_routing(q, k, v, icl: IclLayout, cfg: IsaConfig) -> IsaRouting:
 def isa_forward_with_routing(q, k, v, icl: IclLayout, cfg: IsaConfig, routing) -> object:
     """Forward pass with pinned routing (pipeline.py:319-328). Accepts our
     IsaRouting or the reference's (numpy index arrays)."""
+    padded = _pad_head_dim(cfg, q, k, v)
+    if padded is not None:
+        return _unpad(isa_forward_with_routing(*padded[1:], icl, padded[0], routing), int(q.shape[-1]))
     res, _, _ = _run(_Inputs(q, k, v, icl, cfg), False, pinned=routing)
     return res
 
@@ -402,6 +460,11 @@ def isa_backward(q, k, v, icl: IclLayout, cfg: IsaConfig, do, *, routing=None) -
     the decisions (ours or the reference's IsaRouting). Computes in bf16 tensor
     arithmetic with fp32 accumulation; returns tensors in q's dtype (numpy fp32
     for numpy inputs)."""
+    padded = _pad_head_dim(cfg, q, k, v, do)
+    if padded is not None:
+        D = int(q.shape[-1])
+        g = isa_backward(*padded[1:4], icl, padded[0], padded[4], routing=routing)
+        return GradBundle(_unpad(g.dq, D), _unpad(g.dk, D), _unpad(g.dv, D))
     numpy_io = isinstance(q, np.ndarray)
     inp = _Inputs(q, k, v, icl, cfg)
     if inp.host:
@@ -444,6 +507,14 @@ def dense_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, scale: Op
     if q.dtype != torch.bfloat16:
         raise ConfigError("dense_attention takes bf16 tensors")
     B, H, S, D = q.shape
+    if D not in SUPPORTED_HEAD_DIMS and D < max(SUPPORTED_HEAD_DIMS):  # zero-padded head dim
+        scale = scale if scale is not None else 1.0 / math.sqrt(D)
+        w = _kernel_width(D) - D
+        res = dense_attention(*(torch.nn.functional.pad(x, (0, w)) for x in (q, k, v)), scale)[..., :D]
+        if out is None:
+            return res.contiguous()
+        out.copy_(res)
+        return out
     if D not in SUPPORTED_HEAD_DIMS:
         raise ConfigError(f"head dim {D} not supported")
     scale = scale if scale is not None else 1.0 / math.sqrt(D)

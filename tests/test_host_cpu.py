@@ -209,3 +209,25 @@ def test_host_stream_plan_on_cpu():
     sh.stride_s = 256
     rc = lib.isa_forward_host_bytes(ctypes.byref(sh), ctypes.byref(kn), 5, ctypes.byref(st), ctypes.byref(ws))
     assert E.STATUS_TO_ERROR[rc] is E.LayoutError
+
+
+def test_head_dim_padding_plan():
+    """Head dims other than 64/128 (up to 128) are zero-padded to the next
+    kernel width with the scale pinned to 1/sqrt(D) of the real width."""
+    import math
+
+    import torch
+
+    from paper_2605_04569_b200 import IsaConfig
+    from paper_2605_04569_b200.pipeline import _pad_head_dim, _unpad
+
+    for D, width in ((1, 64), (32, 64), (63, 64), (65, 128), (96, 128), (127, 128)):
+        x = torch.randn(1, 2, 3, D)
+        cfg, px, pn = _pad_head_dim(IsaConfig(), x, x.numpy())
+        assert px.shape[-1] == width and pn.shape[-1] == width
+        assert cfg.scale == 1.0 / math.sqrt(D)
+        assert torch.equal(px[..., :D], x) and not px[..., D:].any()
+        assert torch.equal(_unpad(px, D), x)
+    assert _pad_head_dim(IsaConfig(scale=0.5), torch.ones(1, 1, 1, 40))[0].scale == 0.5
+    for D in (64, 128, 129, 256):
+        assert _pad_head_dim(IsaConfig(), torch.ones(1, 1, 1, D)) is None
