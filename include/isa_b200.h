@@ -177,6 +177,19 @@ int isa_dense_attention(const IsaShape* shape, double scale, const void* q, cons
  * strides; dtype bf16 or fp32; angles in fp64, rotation in fp32. */
 int isa_decoupled_rope(const IsaShape* shape, double base, const void* x, void* out, void* stream);
 
+/* Standalone Taylor kernel (taylor_sparse_forward, taylor.py:163-194, with
+ * TaylorKernelInput, taylor.py:45-109): every 64-row query block of q is
+ * flat; mask[b][h][u][0..k_mask) (int64, ascending, in [0, k_len/64)) are its
+ * exact key blocks of k/v; kc/vc (fp32 contiguous (B,H,k_len/64,D)) are the
+ * key-block centroids. q_shape describes q and out (seq_len = S_q, bf16,
+ * l_src = seq_len, l_ctx = 0); k and v share k_strides {b, h, s} (elements).
+ * Full blocks only (S_q, k_len multiples of 64). */
+int isa_taylor_workspace_bytes(const IsaShape* q_shape, int32_t k_len, int32_t k_mask, size_t* bytes);
+int isa_taylor_forward(const IsaShape* q_shape, int32_t k_len, const int64_t* k_strides, int32_t k_mask,
+                       double scale, const void* q, const void* k, const void* v, const float* kc, const float* vc,
+                       const int64_t* mask, void* out, void* workspace, size_t workspace_bytes, int32_t* err_word,
+                       void* stream);
+
 /* ---- stage primitives (test hooks; same kernels as the pipeline) ---- */
 
 /* K1: block means (B,H,T,D) fp32 of q, k, v into means[3][B][H][T][D]. */

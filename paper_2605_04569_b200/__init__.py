@@ -35,6 +35,10 @@ from .types import (
     SharpnessSplit,
 )
 
+from .tensorio import dump, load, load_tensor4, save_tensor4
+from .workload import WorkloadSpec, generate
+from .taylor import TaylorKernelInput, flop_count, taylor_sparse_forward
+
 __version__ = "0.1.0"
 
 

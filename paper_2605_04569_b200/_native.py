@@ -37,6 +37,8 @@ EXPORTED_SYMBOLS = (
     "isa_decoupled_rope",
     "isa_backward_workspace_bytes",
     "isa_backward",
+    "isa_taylor_workspace_bytes",
+    "isa_taylor_forward",
 )
 
 
@@ -123,6 +125,11 @@ _SIGS = {
     "isa_backward": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _P, _P, _P, _P, _P, _P, _P,
                                     _P, ctypes.c_size_t, ctypes.POINTER(IsaRoutingIn), _P, _P]),
     "isa_decoupled_rope": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.c_double, _P, _P, _P]),
+    "isa_taylor_workspace_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), _I, _I,
+                                                  ctypes.POINTER(ctypes.c_size_t)]),
+    "isa_taylor_forward": (ctypes.c_int, [ctypes.POINTER(IsaShape), _I, ctypes.POINTER(ctypes.c_int64), _I,
+                                          ctypes.c_double, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P,
+                                          _P]),
     "isa_forward_host_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _I,
                                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
     "isa_forward_host": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _P, _P, _P, _P, _I, _P,

@@ -1058,6 +1058,151 @@ int isa_dense_attention(const IsaShape* shape, double scale, const void* q, cons
                                              static_cast<cudaStream_t>(stream));
 }
 
+// ---------------------------------------------------------------- standalone Taylor kernel
+// taylor_sparse_forward (taylor.py:163-194): every query block of q is flat,
+// its exact K_new blocks are the caller's mask rows, the centroids the
+// caller's kc/vc. Same K7 kernel as the pipeline: identity block table over
+// k (K_new = k), flat list 0..t_q-1, member words from the mask, the Taylor
+// work plan, kc/vc rounded to the bf16 centroid rows. The query geometry goes
+// in the attention params (l_src = S_q), the key geometry in the plan
+// (l_src = S_k); full 64-row blocks on both sides.
+struct TaylorWs {
+  int *kv_blk, *flat, *mask, *ctx_short, *n_tiles;
+  uint32_t* bits;
+  __nv_bfloat16 *kc_bf, *vc_bf;
+  int4* tiles;
+  size_t bytes;
+};
+
+int taylor_dims(const IsaShape* sh, int k_len, int k_mask, Dims* d) {
+  if (!sh) return fail(ISA_ERR_CONFIG, "null shape");
+  if (sh->block != 64) return fail(ISA_ERR_CONFIG, "block_size=%d not supported (only 64)", sh->block);
+  if (sh->head_dim != 64 && sh->head_dim != 128)
+    return fail(ISA_ERR_CONFIG, "head_dim=%d not supported (64 or 128)", sh->head_dim);
+  if (sh->dtype != ISA_DTYPE_BF16) return fail(ISA_ERR_CONFIG, "the standalone Taylor kernel takes bf16 q/k/v");
+  if (sh->batch < 1 || sh->heads < 1 || sh->seq_len < 1 || k_len < 1)
+    return fail(ISA_ERR_LAYOUT, "all dims must be >= 1");
+  if (sh->seq_len % 64) return fail(ISA_ERR_LAYOUT, "query length %d not divisible by block size 64", sh->seq_len);
+  if (k_len % 64) return fail(ISA_ERR_LAYOUT, "key length %d not divisible by block size 64", k_len);
+  *d = Dims{};
+  d->B = sh->batch;
+  d->H = sh->heads;
+  d->S = sh->seq_len;
+  d->D = sh->head_dim;
+  d->BH = d->B * d->H;
+  d->l_src = sh->seq_len;
+  d->t_src = d->T = d->n_flat = sh->seq_len / 64;
+  d->t_new = k_len / 64;
+  d->k = k_mask;
+  if (k_mask < 1 || k_mask > d->t_new)
+    return fail(ISA_ERR_CONTRACT, "mask width %d out of [1, %d]", k_mask, d->t_new);
+  d->tn_pad = ((d->t_new + 127) / 128) * 128;
+  d->W = d->tn_pad / 32;
+  if (d->W > 128) return fail(ISA_ERR_CONFIG, "%d key blocks exceed the Taylor kernel's limit (4096)", d->t_new);
+  d->items_f = (d->n_flat + 3) / 4;
+  const int u = 2 * d->k < d->t_new ? 2 * d->k : d->t_new;
+  d->max_tiles = (u + 1) / 2;
+  return ISA_OK;
+}
+
+TaylorWs carve_taylor(const Dims& d, uint8_t* base) {
+  TaylorWs w{};
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    uint8_t* p = base ? base + off : nullptr;
+    off += align256(n ? n : 1);
+    return p;
+  };
+  const long long BH = d.BH;
+  w.kv_blk = reinterpret_cast<int*>(take(4ull * BH * d.t_new));
+  w.flat = reinterpret_cast<int*>(take(4ull * BH * d.n_flat));
+  w.mask = reinterpret_cast<int*>(take(4ull * BH * d.n_flat * d.k));
+  w.bits = reinterpret_cast<uint32_t*>(take(4ull * BH * d.n_flat * d.W));
+  w.kc_bf = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.tn_pad * d.D));
+  w.vc_bf = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.tn_pad * d.D));
+  w.ctx_short = reinterpret_cast<int*>(take(4ull * BH));
+  w.tiles = reinterpret_cast<int4*>(take(16ull * BH * d.items_f * 2 * d.max_tiles));
+  w.n_tiles = reinterpret_cast<int*>(take(4ull * BH * d.items_f));
+  w.bytes = off;
+  return w;
+}
+
+int isa_taylor_workspace_bytes(const IsaShape* q_shape, int32_t k_len, int32_t k_mask, size_t* bytes) {
+  Dims d;
+  int rc = taylor_dims(q_shape, k_len, k_mask, &d);
+  if (rc) return rc;
+  if (!bytes) return fail(ISA_ERR_CONFIG, "null bytes");
+  *bytes = carve_taylor(d, nullptr).bytes;
+  return ISA_OK;
+}
+
+int isa_taylor_forward(const IsaShape* q_shape, int32_t k_len, const int64_t* k_strides, int32_t k_mask,
+                       double scale, const void* q, const void* k, const void* v, const float* kc, const float* vc,
+                       const int64_t* mask, void* out, void* workspace, size_t workspace_bytes, int32_t* err_word,
+                       void* stream) {
+  g_launches = 0;
+  Dims d;
+  int rc = taylor_dims(q_shape, k_len, k_mask, &d);
+  if (rc) return rc;
+  if (!(scale > 0.0)) return fail(ISA_ERR_CONFIG, "scale must be > 0");
+  if (!q || !k || !v || !kc || !vc || !mask || !k_strides) return fail(ISA_ERR_CONFIG, "null operand");
+  if ((rc = check_out(q_shape, out))) return rc;
+  TaylorWs w = carve_taylor(d, static_cast<uint8_t*>(workspace));
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, w.bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long BH = d.BH;
+  // identity K_new table (ctx_short = -1), flat list 0..t_q-1, member words
+  isa::kvblk_from_sel_kernel<<<d.BH, 256, 0, st>>>(nullptr, d.t_new, 0, 0, 0, w.kv_blk, w.ctx_short);
+  ISA_LAUNCHED("kvblk_from_sel_kernel");
+  isa::iota_rows_kernel<<<grid1d(BH * d.n_flat, 256), 256, 0, st>>>(w.flat, d.n_flat, BH * d.n_flat);
+  ISA_LAUNCHED("iota_rows_kernel");
+  isa::narrow_kernel<<<grid1d(BH * d.n_flat * d.k, 256), 256, 0, st>>>(mask, w.mask, BH * d.n_flat * d.k);
+  ISA_LAUNCHED("narrow_kernel");
+  isa::bits_from_mask_kernel<<<BH * d.n_flat, 128, 0, st>>>(w.mask, d.k, d.W, w.bits);
+  ISA_LAUNCHED("bits_from_mask_kernel");
+  isa::SegInfo seg{k_len, 0, d.t_new, 0};
+  isa::centroid_kernel<<<dim3(d.tn_pad, d.BH), d.D, 0, st>>>(kc, vc, w.kv_blk, d.t_new, d.t_new, d.tn_pad, d.D, seg,
+                                                              w.kc_bf, w.vc_bf, w.ctx_short);
+  ISA_LAUNCHED("centroid_kernel");
+  isa::taylor_plan_kernel<<<dim3(d.items_f, d.BH), 64, 0, st>>>(w.bits, d.n_flat, d.W, d.items_f, d.max_tiles,
+                                                                 w.kv_blk, d.t_new, d.t_new, k_len, 0, w.tiles,
+                                                                 w.n_tiles);
+  ISA_LAUNCHED("taylor_plan_kernel");
+  CUtensorMap tq, tk, tv, tkc, tvc;
+  const IsaShape* sh = q_shape;
+  if ((rc = make_map(&tq, q, d.D, d.S, d.H, d.B, sh->stride_s * 2, sh->stride_h * 2, sh->stride_b * 2))) return rc;
+  if ((rc = make_map(&tk, k, d.D, k_len, d.H, d.B, k_strides[2] * 2, k_strides[1] * 2, k_strides[0] * 2))) return rc;
+  if ((rc = make_map(&tv, v, d.D, k_len, d.H, d.B, k_strides[2] * 2, k_strides[1] * 2, k_strides[0] * 2))) return rc;
+  const long long cr = (long long)d.D * 2, ch = (long long)d.tn_pad * d.D * 2;
+  if ((rc = make_map(&tkc, w.kc_bf, d.D, d.tn_pad, d.BH, 1, cr, ch, BH * ch))) return rc;
+  if ((rc = make_map(&tvc, w.vc_bf, d.D, d.tn_pad, d.BH, 1, cr, ch, BH * ch))) return rc;
+  isa::AttnParams p{};
+  p.H = d.H;
+  p.l_src = d.S;  // query geometry: one segment of t_q full blocks
+  p.t_src = d.t_src;
+  p.t_new = d.t_new;
+  p.scale_log2 = static_cast<float>(scale * 1.4426950408889634);
+  p.kv_blk = w.kv_blk;
+  p.out = out;
+  p.out_fp32 = 0;
+  out_strides(sh, d, &p);
+  p.err_flag = err_word;
+  p.T = d.T;
+  p.S = d.S;
+  p.n_qblk = d.n_flat;
+  p.qlist = w.flat;
+  p.tiles = w.tiles;
+  p.n_tiles = w.n_tiles;
+  p.n_items = d.items_f;
+  p.max_tiles = d.max_tiles;
+  p.member_bits = w.bits;
+  p.W = d.W;
+  p.ctx_short_j = w.ctx_short;
+  p.tn_pad = d.tn_pad;
+  return launch_attention_d<isa::MODE_TAYLOR>(d.D, tq, tk, tv, tkc, tvc, p, d.items_f, d.BH, st);
+}
+
 int isa_decoupled_rope(const IsaShape* shape, double base, const void* x, void* out, void* stream) {
   g_launches = 0;
   if (!shape) return fail(ISA_ERR_CONFIG, "null shape");

@@ -980,6 +980,12 @@ __global__ void narrow_kernel(const int64_t* __restrict__ src, int* __restrict__
     dst[i] = static_cast<int>(src[i]);
 }
 
+// out[i] = i mod n: per-(b, h) lists 0..n-1 (the standalone Taylor kernel's flat list).
+__global__ void iota_rows_kernel(int* __restrict__ out, int n, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x)
+    out[i] = static_cast<int>(i % n);
+}
+
 // Pinned selection -> K_new block table.
 // Also records the K_new index of the short last context block when it was
 // selected (-1 otherwise): the only K_new block besides t_src-1 whose valid
