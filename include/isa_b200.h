@@ -170,6 +170,14 @@ int isa_routing(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
 int isa_dense_attention(const IsaShape* shape, double scale, const void* q, const void* k, const void* v,
                         void* out, void* stream);
 
+/* Dense attention with a query length S_q different from the key length
+ * k_len (full_attention / online_softmax_attention without a key mask,
+ * reference.py:79-170). q_shape describes q and out (bf16, seq_len = S_q a
+ * multiple of 64); k and v share k_strides {b, h, s} (elements). A ragged
+ * k_len (not a multiple of 64) needs ceil(k_len/64) > S_q/64. */
+int isa_cross_attention(const IsaShape* q_shape, int32_t k_len, const int64_t* k_strides, double scale,
+                        const void* q, const void* k, const void* v, void* out, void* stream);
+
 /* Decoupled rotary embedding (pipeline.py:469-490, apply_decoupled_rope):
  * pairs (2i, 2i+1) of each token rotate by pos * base^(-2i/D) with positions
  * 0..L_src-1 for the source segment and 0..L_ctx-1 for the context segment.

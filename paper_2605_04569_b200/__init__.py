@@ -50,6 +50,10 @@ def __getattr__(name):
         from . import pipeline
 
         return getattr(pipeline, name)
+    if name in ("full_attention", "online_softmax_attention"):
+        from . import exact
+
+        return getattr(exact, name)
     if name in ("isa_forward_sharded", "head_shard"):
         from . import parallel
 

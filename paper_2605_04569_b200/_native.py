@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "isa_backward",
     "isa_taylor_workspace_bytes",
     "isa_taylor_forward",
+    "isa_cross_attention",
 )
 
 
@@ -125,6 +126,8 @@ _SIGS = {
     "isa_backward": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _P, _P, _P, _P, _P, _P, _P,
                                     _P, ctypes.c_size_t, ctypes.POINTER(IsaRoutingIn), _P, _P]),
     "isa_decoupled_rope": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.c_double, _P, _P, _P]),
+    "isa_cross_attention": (ctypes.c_int, [ctypes.POINTER(IsaShape), _I, ctypes.POINTER(ctypes.c_int64),
+                                           ctypes.c_double, _P, _P, _P, _P, _P]),
     "isa_taylor_workspace_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), _I, _I,
                                                   ctypes.POINTER(ctypes.c_size_t)]),
     "isa_taylor_forward": (ctypes.c_int, [ctypes.POINTER(IsaShape), _I, ctypes.POINTER(ctypes.c_int64), _I,

@@ -1058,6 +1058,58 @@ int isa_dense_attention(const IsaShape* shape, double scale, const void* q, cons
                                              static_cast<cudaStream_t>(stream));
 }
 
+// ---------------------------------------------------------------- dense attention, S_q != S_k
+// full_attention / online_softmax_attention (reference.py:79-170) for a
+// query length different from the key length, on the K8 (DENSE) kernel. The
+// kernel's two-segment geometry carries both sides: segment 1 = the t_q query
+// blocks (l_src = S_q, a multiple of 64, so key block j sits at row 64j in
+// either segment), segment 2 length S_k - S_q, so key block j's valid rows
+// are min(64, S_k - 64j) for j >= t_q. Hence either S_k is a multiple of 64
+// or t_k > t_q (the ragged block must lie in segment 2).
+int isa_cross_attention(const IsaShape* q_shape, int32_t k_len, const int64_t* k_strides, double scale,
+                        const void* q, const void* k, const void* v, void* out, void* stream) {
+  g_launches = 0;
+  const IsaShape* sh = q_shape;
+  if (!sh || !k_strides) return fail(ISA_ERR_CONFIG, "null shape/strides");
+  if (sh->head_dim != 64 && sh->head_dim != 128)
+    return fail(ISA_ERR_CONFIG, "head_dim=%d not supported (64 or 128)", sh->head_dim);
+  if (sh->dtype != ISA_DTYPE_BF16) return fail(ISA_ERR_CONFIG, "dense attention takes bf16 inputs");
+  if (sh->batch < 1 || sh->heads < 1 || sh->seq_len < 1 || k_len < 1)
+    return fail(ISA_ERR_LAYOUT, "all dims must be >= 1");
+  if (sh->seq_len % 64) return fail(ISA_ERR_LAYOUT, "query length %d must be a multiple of 64", sh->seq_len);
+  const int t_q = sh->seq_len / 64, t_k = (k_len + 63) / 64;
+  if ((k_len % 64) && t_k <= t_q)
+    return fail(ISA_ERR_LAYOUT, "a ragged key length needs more key blocks (%d) than query blocks (%d)", t_k, t_q);
+  if (!(scale > 0.0)) return fail(ISA_ERR_CONFIG, "scale must be > 0");
+  if (!q || !k || !v) return fail(ISA_ERR_CONFIG, "null operand");
+  int rc;
+  if ((rc = check_out(sh, out))) return rc;
+  Dims d{};
+  d.B = sh->batch;
+  d.H = sh->heads;
+  d.S = sh->seq_len;
+  d.D = sh->head_dim;
+  d.BH = d.B * d.H;
+  CUtensorMap tq, tk, tv;
+  if ((rc = make_map(&tq, q, d.D, d.S, d.H, d.B, sh->stride_s * 2, sh->stride_h * 2, sh->stride_b * 2))) return rc;
+  if ((rc = make_map(&tk, k, d.D, k_len, d.H, d.B, k_strides[2] * 2, k_strides[1] * 2, k_strides[0] * 2))) return rc;
+  if ((rc = make_map(&tv, v, d.D, k_len, d.H, d.B, k_strides[2] * 2, k_strides[1] * 2, k_strides[0] * 2))) return rc;
+  isa::AttnParams p{};
+  p.H = d.H;
+  p.l_src = d.S;
+  p.t_src = t_q;
+  p.l_ctx = k_len - d.S;  // only read for key blocks j >= t_q, i.e. when k_len > S_q
+  p.t_ctx = t_k > t_q ? t_k - t_q : 0;
+  p.t_new = t_k;
+  p.n_qblk = t_q;
+  p.scale_log2 = static_cast<float>(scale * 1.4426950408889634);
+  p.out = out;
+  p.out_fp32 = 0;
+  out_strides(sh, d, &p);
+  return launch_attention_d<isa::MODE_DENSE>(d.D, tq, tk, tv, tq, tq, p, (t_q + 3) / 4, d.BH,
+                                             static_cast<cudaStream_t>(stream));
+}
+
 // ---------------------------------------------------------------- standalone Taylor kernel
 // taylor_sparse_forward (taylor.py:163-194): every query block of q is flat,
 // its exact K_new blocks are the caller's mask rows, the centroids the

@@ -1,0 +1,156 @@
+"""Exact softmax attention drop-ins: the reference's `full_attention` and
+`online_softmax_attention` (pkg/src/isattn/reference.py:79-170, the sharp
+branch's kernel and the dense oracle), with the same signatures and errors,
+computed by the sm_100a K8 kernel (bf16 operands, fp32 accumulation).
+
+S_q == S_k runs `isa_dense_attention`; S_q != S_k runs `isa_cross_attention`
+on query rows zero-padded to a multiple of 64, except a ragged key length with
+no more key blocks than query blocks, which runs `isa_dense_attention` on
+query slabs of S_k rows.
+Key masks: an all-valid mask is accepted; a mask that drops keys is not
+implemented on the GPU path and raises ConfigError (a row with every key
+masked raises DegenerateRowError first, like reference.py:116-117).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError, DegenerateRowError, InputError, LayoutError
+from .types import SUPPORTED_HEAD_DIMS
+
+
+def _shape4(x, name):
+    shape = tuple(int(s) for s in getattr(x, "shape", ()))
+    if len(shape) != 4:
+        raise LayoutError(f"{name}: expected 4 axes (B,H,S,D), got shape {shape}")
+    if min(shape) < 1:
+        raise LayoutError(f"{name}: all dims must be >= 1, got shape {shape}")
+    return shape
+
+
+def _key_mask(mask, B: int, H: int, S_k: int) -> Optional[np.ndarray]:
+    """(B,H,S_k) bool, True = valid key; a 1-D mask broadcasts (reference.py:67-76)."""
+    if mask is None:
+        return None
+    if hasattr(mask, "detach"):
+        mask = mask.detach().cpu().numpy()
+    mask = np.asarray(mask, dtype=bool)
+    if mask.ndim == 1:
+        mask = np.broadcast_to(mask, (B, H, S_k))
+    if mask.shape != (B, H, S_k):
+        raise LayoutError(f"key mask shape {mask.shape} != (B,H,S_k)=({B},{H},{S_k})")
+    return mask
+
+
+def _device_bf16(x, dev):
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+    if not isinstance(x, torch.Tensor):
+        raise LayoutError("expected torch tensors or numpy arrays")
+    x = x.to(device=dev, dtype=torch.bfloat16)
+    if x.stride(3) != 1 or any(s % 8 for s in x.stride()[:3]) or x.data_ptr() % 16:
+        x = x.contiguous()
+    return x
+
+
+def _exact(q, k, v, scale, mask):
+    (B, H, S_q, D), (Bk, Hk, S_k, Dk), (Bv, Hv, S_v, Dv) = (_shape4(x, n) for x, n in ((q, "Q"), (k, "K"), (v, "V")))
+    if (Bk, Hk) != (B, H) or (Bv, Hv) != (B, H) or Dk != D:
+        raise LayoutError(f"Q/K/V batch/head/dim mismatch: {(B, H, S_q, D)}, {(Bk, Hk, S_k, Dk)}, "
+                          f"{(Bv, Hv, S_v, Dv)}")
+    if S_v != S_k:
+        raise LayoutError(f"K and V sequence lengths differ: {S_k} vs {S_v}")
+    if Dv != D:
+        raise ConfigError(f"value width {Dv} != key width {D} is not supported by the sm_100a kernel")
+    scale = 1.0 / math.sqrt(D) if scale is None else float(scale)
+    if scale <= 0:
+        raise ConfigError(f"scale must be > 0, got {scale}")
+    km = _key_mask(mask, B, H, S_k)
+    if km is not None and not km.all():
+        if not km.any(axis=2).all():
+            raise DegenerateRowError("query row with all keys masked")
+        raise ConfigError("key masks that drop keys are not supported by the sm_100a kernel")
+    if D > max(SUPPORTED_HEAD_DIMS):
+        raise ConfigError(f"head dim {D} not supported by the sm_100a kernels (<= {max(SUPPORTED_HEAD_DIMS)})")
+    numpy_io = isinstance(q, np.ndarray)
+    out_dtype = q.dtype
+    dev = next((x.device for x in (q, k, v) if isinstance(x, torch.Tensor) and x.is_cuda), None)
+    if dev is None:
+        if not torch.cuda.is_available():
+            raise LayoutError("exact attention runs on a CUDA device and none is available (there is no CPU path)")
+        dev = torch.device("cuda", torch.cuda.current_device())
+    qd, kd, vd = (_device_bf16(x, dev) for x in (q, k, v))
+    if not all(bool(torch.isfinite(x).all()) for x in (qd, kd, vd)):
+        raise InputError("Q/K/V: non-finite elements")
+    width = 64 if D <= 64 else 128
+    if width != D:  # zero columns: exact zeros in every score, dropped output columns
+        qd, kd, vd = (torch.nn.functional.pad(x, (0, width - D)) for x in (qd, kd, vd))
+    if S_q == S_k:
+        from .pipeline import dense_attention
+
+        res = dense_attention(qd, kd, vd, scale)
+    else:
+        res = _cross(qd, kd, vd, scale)
+    res = res[..., :D]
+    if numpy_io:
+        return res.float().cpu().numpy().astype(out_dtype)
+    return res.to(out_dtype).contiguous()
+
+
+def _cross(q, k, v, scale):
+    B, H, S_q, D = q.shape
+    S_k = k.shape[2]
+    rows = -(-S_q // 64) * 64
+    t_q, t_k = rows // 64, -(-S_k // 64)
+    if S_k % 64 and t_k <= t_q:
+        # ragged keys and at least as many query blocks: query slabs of S_k rows
+        # on the equal-length kernel (the last slab zero-padded)
+        from .pipeline import dense_attention
+
+        k, v = k.contiguous(), v.contiguous()
+        n = -(-S_q // S_k)
+        qp = torch.nn.functional.pad(q, (0, 0, 0, n * S_k - S_q))
+        out = torch.empty((B, H, n * S_k, D), dtype=torch.bfloat16, device=q.device)
+        for i in range(n):
+            out[:, :, i * S_k:(i + 1) * S_k] = dense_attention(qp[:, :, i * S_k:(i + 1) * S_k].contiguous(), k, v,
+                                                               scale)
+        return out[:, :, :S_q]
+    if rows != S_q:
+        q = torch.nn.functional.pad(q, (0, 0, 0, rows - S_q))
+    if k.stride() != v.stride():
+        k, v = k.contiguous(), v.contiguous()
+    out = torch.empty((B, H, rows, D), dtype=torch.bfloat16, device=q.device)
+    shape = N.IsaShape(B, H, rows, D, rows, 0, 64, N.ISA_DTYPE_BF16, *q.stride()[:3])
+    shape.out_stride_b, shape.out_stride_h, shape.out_stride_s = out.stride()[:3]
+    kst = (ctypes.c_int64 * 3)(*k.stride()[:3])
+    N.check(N.load().isa_cross_attention(ctypes.byref(shape), S_k, kst, scale, q.data_ptr(), k.data_ptr(),
+                                         v.data_ptr(), out.data_ptr(), torch.cuda.current_stream(q.device).cuda_stream))
+    return out[:, :, :S_q]
+
+
+def full_attention(q, k, v, scale: Optional[float] = None, mask=None, row_chunk: int = 2048):
+    """Direct softmax attention O = softmax(scale * Q K^T) V (reference.py:79-123).
+    `row_chunk` (the reference's memory knob) is accepted and unused: the
+    kernel streams keys through shared memory and never forms the score matrix."""
+    del row_chunk
+    return _exact(q, k, v, scale, mask)
+
+
+def online_softmax_attention(q, k, v, scale: Optional[float] = None, layout=None, mask=None, block_order=None):
+    """Blockwise online-softmax attention (reference.py:126-170), same contract
+    as full_attention. `layout` must cover the key axis (LayoutError otherwise);
+    the kernel's own 128-key tiling replaces it, and `block_order` (the
+    reference's visiting-order test hook) is accepted and ignored: the result
+    is order-independent up to rounding."""
+    del block_order
+    S_k = _shape4(k, "K")[2]
+    if layout is not None and layout.seq_len != S_k:
+        raise LayoutError(f"layout.seq_len {layout.seq_len} != key length {S_k}")
+    return _exact(q, k, v, scale, mask)

@@ -1,0 +1,89 @@
+"""Exact attention drop-ins (`full_attention`, `online_softmax_attention`,
+reference.py:79-170) on the sm_100a kernel, against the reference's own
+`full_attention` outputs (`tests/golden/exact`, made by
+`tests/golden/make_exact_golden.py`): S_q == S_k and S_q != S_k, ragged
+lengths, head dims 64 / 128 / padded 96, the reference's errors."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import isa_oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "exact")
+CASES = sorted(f[:-4] for f in os.listdir(GOLD) if f.endswith(".npz"))
+
+
+def make_inputs(B, H, S_q, S_k, D, seed):
+    """Same draws as make_exact_golden.make_inputs."""
+    rng = np.random.default_rng(seed)
+    q = O.round_bf16(rng.standard_normal((B, H, S_q, D)).astype(np.float32))
+    k = O.round_bf16(rng.standard_normal((B, H, S_k, D)).astype(np.float32))
+    v = O.round_bf16(rng.standard_normal((B, H, S_k, D)).astype(np.float32))
+    return q, k, v
+
+
+def _case(name):
+    g = np.load(os.path.join(GOLD, f"{name}.npz"))
+    B, H, S_q, S_k, D, seed = (int(x) for x in g["geom"])
+    q, k, v = make_inputs(B, H, S_q, S_k, D, seed)
+    assert np.isclose(q.sum() + k.sum() + v.sum(), g["checksum"])
+    return (q, k, v), g
+
+
+def test_errors_before_device():
+    from paper_2605_04569_b200.errors import ConfigError, DegenerateRowError, LayoutError
+    from paper_2605_04569_b200.exact import full_attention, online_softmax_attention
+    from paper_2605_04569_b200.types import BlockLayout
+
+    q, k, v = make_inputs(1, 2, 64, 128, 64, 0)
+    with pytest.raises(LayoutError, match="batch/head/dim"):
+        full_attention(q, k[:, :1], v)
+    with pytest.raises(LayoutError, match="differ"):
+        full_attention(q, k, v[:, :, :64])
+    with pytest.raises(ConfigError, match="scale"):
+        full_attention(q, k, v, scale=-1.0)
+    with pytest.raises(LayoutError, match="key mask shape"):
+        full_attention(q, k, v, mask=np.ones((1, 2, 5), bool))
+    with pytest.raises(DegenerateRowError):
+        full_attention(q, k, v, mask=np.zeros(128, bool))
+    with pytest.raises(ConfigError, match="key masks"):
+        full_attention(q, k, v, mask=np.arange(128) < 100)
+    with pytest.raises(LayoutError, match="layout.seq_len"):
+        online_softmax_attention(q, k, v, layout=BlockLayout(64, 100))
+    with pytest.raises(LayoutError, match="4 axes"):
+        full_attention(q[0], k, v)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_matches_reference_golden(name):
+    import paper_2605_04569_b200 as P
+
+    (q, k, v), g = _case(name)
+    for fn in (P.full_attention, P.online_softmax_attention):
+        out = fn(q, k, v, mask=np.ones(k.shape[2], bool))
+        assert out.shape == g["out"].shape and out.dtype == np.float32
+        a, r = out.astype(np.float64).ravel(), g["out"].astype(np.float64).ravel()
+        err = float(np.abs(a - r).max())
+        cos = float(a @ r / (np.linalg.norm(a) * np.linalg.norm(r)))
+        assert err <= 2e-2 and cos >= 0.999, (name, err, cos)
+
+
+@pytest.mark.gpu
+def test_torch_strided_cross():
+    import torch
+
+    import paper_2605_04569_b200 as P
+
+    q, k, v = make_inputs(2, 3, 700, 1500, 128, 5)
+    dev = torch.device("cuda")
+    tq, tk, tv = (torch.from_numpy(x).to(dev, torch.bfloat16).permute(0, 2, 1, 3).contiguous().permute(0, 2, 1, 3)
+                  for x in (q, k, v))
+    out = P.full_attention(tq, tk, tv)
+    assert out.dtype == torch.bfloat16 and tuple(out.shape) == (2, 3, 700, 128)
+    ref = torch.softmax((tq.float() @ tk.float().transpose(-1, -2)) / np.sqrt(128), -1) @ tv.float()
+    assert (out.float() - ref).abs().max().item() < 2e-2
