@@ -38,8 +38,10 @@ struct BwdParams {
   const int* kv_blk;                       // [BH][t_new]
   const uint32_t* bits;                    // [BH][n_flat][W] member bits
   const __nv_bfloat16 *kc, *vc;            // [BH][tn_pad][D] K_new centroids
-  float *dkc, *dvc;                        // [BH][t_new][D]
+  float *dkc, *dvc;                        // [BH][t_new][D] (x c_splits partials before the reduce)
   float *dq, *dk, *dv;                     // [BH][S][D]
+  int c_splits;                            // centroid kernel: flat query list split across gridDim.z
+  long long c_part;                        // elements per partial dkc/dvc slab (BH * t_new * D)
 };
 
 __device__ __forceinline__ int bw_tok0(const BwdParams& p, int u) {
@@ -340,7 +342,12 @@ __global__ void __launch_bounds__(128, 2) bwd_dkv_kernel(const BwdParams p) {
     if (take) sList[base + atomicAdd(&s_count, 1)] = p.n_sharp + f;
   }
   __syncthreads();
-  const int n_list = base + s_count;
+  int li0 = 0, n_list = base + s_count;
+  if (CENTROID && p.c_splits > 1) {  // this CTA's share of the flat list (gridDim.z-way split)
+    const int per = (n_list + p.c_splits - 1) / p.c_splits;
+    li0 = blockIdx.z * per;
+    n_list = min(n_list, li0 + per);
+  }
   auto prefetch = [&](int li, int buf) {
     const int x = sList[li];
     const bool is_flat = x >= p.n_sharp;
@@ -374,10 +381,10 @@ __global__ void __launch_bounds__(128, 2) bwd_dkv_kernel(const BwdParams p) {
   for (int n = 0; n < D / 8; ++n)
 #pragma unroll
     for (int e = 0; e < 4; ++e) dk[n][e] = dv[n][e] = 0.f;
-  if (n_list > 0) prefetch(0, 0);
+  if (n_list > li0) prefetch(li0, 0);
   const uint32_t bk = smem_u32(sK), bvv = smem_u32(sV);
-  for (int li = 0; li < n_list; ++li) {
-    const int buf = li & 1;
+  for (int li = li0; li < n_list; ++li) {
+    const int buf = (li - li0) & 1;
     if (li + 1 < n_list) {
       prefetch(li + 1, buf ^ 1);
       cp_wait<1>();
@@ -453,18 +460,19 @@ __global__ void __launch_bounds__(128, 2) bwd_dkv_kernel(const BwdParams p) {
   const bool kv1 = CENTROID ? c0 + kr1 < p.t_new : kr1 < vk;
   // stores
   if (CENTROID) {
+    const long long part = blockIdx.z * p.c_part;  // partial slab (reduced by bwd_centroid_reduce_kernel)
 #pragma unroll
     for (int n = 0; n < D / 8; ++n) {
       const int col = n * 8 + tig * 2;
       if (kv0) {
-        const long long o = ((long long)bh * p.t_new + c0 + kr0) * D + col;
+        const long long o = part + ((long long)bh * p.t_new + c0 + kr0) * D + col;
         p.dkc[o] = p.scale * dk[n][0];
         p.dkc[o + 1] = p.scale * dk[n][1];
         p.dvc[o] = dv[n][0];
         p.dvc[o + 1] = dv[n][1];
       }
       if (kv1) {
-        const long long o = ((long long)bh * p.t_new + c0 + kr1) * D + col;
+        const long long o = part + ((long long)bh * p.t_new + c0 + kr1) * D + col;
         p.dkc[o] = p.scale * dk[n][2];
         p.dkc[o + 1] = p.scale * dk[n][3];
         p.dvc[o] = dv[n][2];
@@ -648,6 +656,21 @@ __global__ void gamma_spread_kernel(const GammaBwdParams p) {
     p.dq[o] += a;
     p.dk[o] += b;
     p.dv[o] += e;
+  }
+}
+
+// Sum of the c_splits partial centroid-gradient slabs into slab 0, in slab
+// order (deterministic: no atomics).
+__global__ void bwd_centroid_reduce_kernel(float* __restrict__ dkc, float* __restrict__ dvc, long long n,
+                                           int splits) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float a = dkc[i], b = dvc[i];
+    for (int z = 1; z < splits; ++z) {
+      a += dkc[z * n + i];
+      b += dvc[z * n + i];
+    }
+    dkc[i] = a;
+    dvc[i] = b;
   }
 }
 

@@ -787,6 +787,22 @@ struct BwdWs {
   size_t bytes;
 };
 
+// Centroid dK/dV kernel: split the flat query list over gridDim.z so the grid
+// covers ~4 CTAs per SM (tn_pad/64 centroid tiles x BH is only 360 CTAs at
+// cfg3), keeping >= 16 query blocks per split. ISA_BWD_CSPLIT=n overrides.
+int centroid_splits(const Dims& d) {
+  if (!d.n_flat) return 1;
+  static int forced = [] {
+    const char* e = getenv("ISA_BWD_CSPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  int s = forced > 0 ? forced : (4 * 148 + (d.tn_pad / 64) * d.BH - 1) / ((d.tn_pad / 64) * d.BH);
+  const int cap = d.n_flat / 16 > 1 ? d.n_flat / 16 : 1;
+  if (s > cap) s = cap;
+  if (s > 16) s = 16;
+  return s < 1 ? 1 : s;
+}
+
 BwdWs carve_bwd(const Dims& d0, uint8_t* base) {
   BwdWs b{};
   Dims d = d0;
@@ -802,8 +818,9 @@ BwdWs carve_bwd(const Dims& d0, uint8_t* base) {
   b.o = reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.S * d.D));
   b.lse = reinterpret_cast<float*>(take(4ull * BH * d.S));
   b.rho = reinterpret_cast<float*>(take(4ull * BH * d.S));
-  b.dkc = reinterpret_cast<float*>(take(4ull * BH * d.t_new * d.D));
-  b.dvc = reinterpret_cast<float*>(take(4ull * BH * d.t_new * d.D));
+  const int cs = centroid_splits(d);
+  b.dkc = reinterpret_cast<float*>(take(4ull * cs * BH * d.t_new * d.D));
+  b.dvc = reinterpret_cast<float*>(take(4ull * cs * BH * d.t_new * d.D));
   if (d0.gamma > 0.0) {
     b.g_doc = reinterpret_cast<float*>(take(4ull * BH * d.T * d.D));
     b.g_stats = reinterpret_cast<float*>(take(12ull * BH * d.T));
@@ -836,8 +853,13 @@ int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps,
   if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 0>, sm_dkv, &cur_e))) return rc;
   if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 1>, sm_dkv, &cur_c))) return rc;
   if (d.n_flat) {
-    isa::bwd_dkv_kernel<D, 1><<<dim3(d.tn_pad / 64, d.BH), 128, sm_dkv, st>>>(bp);
+    const int cs = bp.c_splits;
+    isa::bwd_dkv_kernel<D, 1><<<dim3(d.tn_pad / 64, d.BH, cs), 128, sm_dkv, st>>>(bp);
     ISA_LAUNCHED("bwd_dkv_kernel<centroid>");
+    if (cs > 1) {
+      isa::bwd_centroid_reduce_kernel<<<grid1d(bp.c_part, 256), 256, 0, st>>>(bp.dkc, bp.dvc, bp.c_part, cs);
+      ISA_LAUNCHED("bwd_centroid_reduce_kernel");
+    }
   }
   if (bwd_mmasync()) {
     isa::bwd_dkv_kernel<D, 0><<<dim3(d.t_new, d.BH), 128, sm_dkv, st>>>(bp);
@@ -977,6 +999,8 @@ int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, co
   bp.vc = b.fw.vc_bf;
   bp.dkc = b.dkc;
   bp.dvc = b.dvc;
+  bp.c_splits = centroid_splits(d);
+  bp.c_part = (long long)d.BH * d.t_new * d.D;
   bp.dq = dq;
   bp.dk = dk;
   bp.dv = dv;
