@@ -67,6 +67,9 @@ struct AttnParams {
   // (surrogate) softmax, [BH][S] by original token row, or null
   float* lse;
   int S;
+  // transposed Taylor kernel (isa_taylor_t.cuh): exact K_new lists [BH][n_qblk][kmask]
+  const int* mask;
+  int kmask;
 };
 
 #ifndef ISA_TRACE_Q

@@ -28,6 +28,7 @@
 #include "isa_bwd.cuh"
 #include "isa_bwd_tc.cuh"
 #include "isa_route.cuh"
+#include "isa_taylor_t.cuh"
 
 namespace {
 
@@ -307,6 +308,32 @@ int launch_isa_fused_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUten
   dim3 grid(items_e + items_t, BH);
   isa::gba_isa_kernel<D><<<grid, isa::kThreads, L::kAlloc, st>>>(tq, tk, tv, tkc, tvc, pe, pt, items_e);
   ISA_LAUNCHED("gba_isa_kernel");
+  return ISA_OK;
+}
+
+// Transposed Taylor kernel (isa_taylor_t.cuh, D = 128): on by default,
+// ISA_TAYLOR_T=0 selects the row-major K7 (fused with K6 in one launch).
+bool taylor_t_mode() {
+  static bool v = [] {
+    const char* e = getenv("ISA_TAYLOR_T");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+int launch_taylor_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
+                    const CUtensorMap& tvc, const isa::AttnParams& p, int BH, cudaStream_t st) {
+  using L = isa::TaylorTSmem<128>;
+  static bool configured = false;
+  if (!configured) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::gba_taylor_t_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  L::kAlloc));
+    configured = true;
+  }
+  const int items = (p.n_qblk + 1) / 2;
+  if (items < 1) return ISA_OK;
+  isa::gba_taylor_t_kernel<128><<<dim3(items, BH), isa::kTThreads, L::kAlloc, st>>>(tq, tk, tv, tkc, tvc, p);
+  ISA_LAUNCHED("gba_taylor_t_kernel");
   return ISA_OK;
 }
 
@@ -760,9 +787,18 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
     pf.W = d.W;
     pf.ctx_short_j = w.ctx_short;
     pf.tn_pad = d.tn_pad;
+    pf.mask = w.mask;
+    pf.kmask = d.k;
   }
-  const bool fuse = d.n_sharp && d.n_flat && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES);
-  if (fuse) {
+  const bool taylor_t = d.n_flat && d.D == 128 && taylor_t_mode();
+  const bool fuse = d.n_sharp && d.n_flat && !taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES);
+  if (taylor_t) {
+    // K6 over the sharp blocks, then K7T over the flat ones
+    if (d.n_sharp)
+      if ((rc = launch_attention_d<isa::MODE_EXACT>(d.D, tq, tk, tv, tq, tq, ps, d.items_s, d.BH, st))) return rc;
+    record(events, 4, st);
+    if ((rc = launch_taylor_t(tq, tk, tv, tkc, tvc, pf, d.BH, st))) return rc;
+  } else if (fuse) {
     // K6 + K7 in one grid: exact items first, Taylor items fill the tail.
     if ((rc = launch_isa_fused(d.D, tq, tk, tv, tkc, tvc, ps, pf, d.items_s, d.items_f, d.BH, st))) return rc;
     record(events, 4, st);
@@ -1276,6 +1312,9 @@ int isa_taylor_forward(const IsaShape* q_shape, int32_t k_len, const int64_t* k_
   p.W = d.W;
   p.ctx_short_j = w.ctx_short;
   p.tn_pad = d.tn_pad;
+  p.mask = w.mask;
+  p.kmask = d.k;
+  if (d.D == 128 && taylor_t_mode()) return launch_taylor_t(tq, tk, tv, tkc, tvc, p, d.BH, st);
   return launch_attention_d<isa::MODE_TAYLOR>(d.D, tq, tk, tv, tkc, tvc, p, d.items_f, d.BH, st);
 }
 
