@@ -28,14 +28,19 @@
 // CTA: two query blocks (stages 0/1, ping-pong like the row-major kernel),
 // warps 0-7 softmax (4 per stage, 208 registers), warp 8 MMA issuer, warp 9
 // TMA producer, warps 10-11 idle (88 registers each for warps 8-11).
-// TMEM: S^T stage s at columns 64s, O^T at 128 + 64s (256 columns).
+// TMEM: S^T stage s, buffer b at columns 128s + 64b; O^T at 256 + 64s.
+// S^T is double-buffered per stage, so QK(i+2) overlaps the softmax of tile
+// i; P^T has one buffer per stage (the softmax of tile i waits PV(i-1)).
 #pragma once
 #include "isa_attn.cuh"
 
 namespace isa {
 
 constexpr int kTThreads = 384;  // warps 10-11 only complete the register-donating warpgroup
-constexpr int kTKvStages = 4;
+#ifndef ISA_TT_KV_STAGES
+#define ISA_TT_KV_STAGES 5
+#endif
+constexpr int kTKvStages = ISA_TT_KV_STAGES;  // K/V ring slots of 32 KB
 
 template <int D>
 struct TaylorTSmem {
@@ -45,7 +50,7 @@ struct TaylorTSmem {
   static constexpr int kPT = 128 * 64 * 2;     // P^T: 128 key rows x 64 queries (bf16, SW128)
   static constexpr int kQOff = 0;
   static constexpr int kKvOff = 2 * kQStage;
-  static constexpr int kPOff = kKvOff + kTKvStages * kTile;
+  static constexpr int kPOff = kKvOff + kTKvStages * kTile;  // P^T [stage][buffer]
   static constexpr int kBarOff = kPOff + 2 * kPT;
   static constexpr int kBytes = kBarOff + 256;
   static constexpr int kAlloc = kBytes + 1024;
@@ -106,16 +111,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
   // dynamic-smem pointers above go through an integer alignment round trip)
   __shared__ __align__(16) float sM_all[2][64];   // running max per query (log2 domain)
   __shared__ __align__(16) float sA_all[2][64];   // rescale factors of the last slow path
-  __shared__ __align__(16) float sR_all[2][256];  // [4 warps][64] partial reductions
   __shared__ __align__(16) float sI_all[2][64];   // 1 / row sum
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* q_full = bars + 0;                      // [2]
   uint64_t* kv_full = bars + 2;                     // [kTKvStages]
   uint64_t* kv_empty = bars + 2 + kTKvStages;       // [kTKvStages]
-  uint64_t* s_full = bars + 2 + 2 * kTKvStages;     // [2]
-  uint64_t* p_full = bars + 4 + 2 * kTKvStages;     // [2]
-  uint64_t* o_full = bars + 6 + 2 * kTKvStages;     // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kTKvStages);
+  uint64_t* s_full = bars + 2 + 2 * kTKvStages;     // [stage][buffer]: S^T(i) in buffer i&1
+  uint64_t* p_full = bars + 6 + 2 * kTKvStages;     // [stage][buffer]: P^T(i) written (S^T buffer read)
+  uint64_t* pv_done = bars + 10 + 2 * kTKvStages;   // [stage][buffer]: PV(i) complete (P^T buffer free)
+  uint64_t* o_full = bars + 14 + 2 * kTKvStages;    // [stage]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * kTKvStages);
 
   const int item = blockIdx.x, bh = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -129,14 +134,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 4; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], 4);
-      mbar_init(&o_full[s], 1);
+      mbar_init(&pv_done[s], 1);
     }
+    mbar_init(&o_full[0], 1);
+    mbar_init(&o_full[1], 1);
     fence_barrier_init();
   }
-  if (warp == 8) tmem_alloc<256>(tmem_slot);
+  if (warp == 8) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -191,19 +198,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
         }
         ++c;
       };
-      // ring order per stage: K_0 | V_{i-1} K_i | ... | V_{n-1} (ring_entry<MODE_TAYLOR>)
-      TTileSrc cur[2] = {{0, 0, 0}, {0, 0, 0}}, prv[2] = {{0, 0, 0}, {0, 0, 0}};
-      for (int i = 0; i <= n_kv; ++i) {
+      // ring order = MMA consumption order: K_0, K_1 of both stages, then per
+      // step i and stage: V_i, K_{i+2}
+      for (int i = 0; i < 2 && i < n_kv; ++i)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) push(tt_tile(p, bh, pos[s], i, n_ex), 0);
+      for (int i = 0; i < n_kv; ++i) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-          if (i == n_kv) {
-            push(cur[s], 1);
-          } else {
-            prv[s] = cur[s];
-            cur[s] = tt_tile(p, bh, pos[s], i, n_ex);
-            if (i > 0) push(prv[s], 1);
-            push(cur[s], 0);
-          }
+          push(tt_tile(p, bh, pos[s], i, n_ex), 1);
+          if (i + 2 < n_kv) push(tt_tile(p, bh, pos[s], i + 2, n_ex), 0);
         }
       }
     } else if (warp == 8) {
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       const uint64_t dk_base = sdesc_sw128_base(smem_u32(sKV), 16, 1024);
       const uint64_t dv_base = sdesc_sw128_base(smem_u32(sKV), 16384, 1024);
       const uint64_t dp_base = sdesc_sw128_base(smem_u32(sP), 16, 1024);
-      auto issue_s = [&](int s, int slot) {
+      auto issue_s = [&](int s, int b, int slot) {
         if (leader) {
           const uint64_t da = dk_base + static_cast<uint64_t>((slot * L::kTile) >> 4);
           const uint64_t db = dq_base + static_cast<uint64_t>((s * L::kQStage) >> 4);
@@ -223,19 +227,19 @@ __global__ void __launch_bounds__(kTThreads, 1)
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint64_t oa = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
             const uint64_t ob = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
-            mma_ss(tmem + s * 64, da + oa, db + ob, idesc_s, kk > 0);
+            mma_ss(tmem + s * 128 + b * 64, da + oa, db + ob, idesc_s, kk > 0);
           }
         }
         __syncwarp();
       };
-      auto issue_o = [&](int s, int slot, uint32_t acc) {
+      auto issue_o = [&](int s, int b, int slot, uint32_t acc) {
         if (leader) {
           const uint64_t da = dv_base + static_cast<uint64_t>((slot * L::kTile) >> 4);
           const uint64_t db = dp_base + static_cast<uint64_t>((s * L::kPT) >> 4);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t o = (kk * 2048) >> 4;
-            mma_ss(tmem + 128 + s * 64, da + o, db + o, idesc_o, (acc | kk) != 0);
+            mma_ss(tmem + 256 + s * 64, da + o, db + o, idesc_o, (acc | kk) != 0);
           }
         }
         __syncwarp();
@@ -244,45 +248,41 @@ __global__ void __launch_bounds__(kTThreads, 1)
         if (leader) mma_commit(bar);
         __syncwarp();
       };
-      auto wait_entry = [&](int e) { mbar_wait(&kv_full[e % kTKvStages], (e / kTKvStages) & 1); };
-      auto release = [&](int e) { commit(&kv_empty[e % kTKvStages]); };
+      int e = 0;  // ring entry
+      auto take = [&]() {
+        mbar_wait(&kv_full[e % kTKvStages], (e / kTKvStages) & 1);
+        __syncwarp();
+        tc_fence_after();
+        return e % kTKvStages;
+      };
+      auto release = [&]() {
+        commit(&kv_empty[e % kTKvStages]);
+        ++e;
+      };
       mbar_wait(&q_full[0], 0);
       mbar_wait(&q_full[1], 0);
-      for (int s = 0; s < 2; ++s) {
-        wait_entry(s);
-        __syncwarp();
-        tc_fence_after();
-        issue_s(s, s % kTKvStages);
-        commit(&s_full[s]);
-        release(s);
-      }
-      for (int i = 1; i < n_kv; ++i) {
-        const int base = 2 + 4 * (i - 1);
+      for (int i = 0; i < 2 && i < n_kv; ++i)
         for (int s = 0; s < 2; ++s) {
-          const int ev = base + 2 * s, ek = ev + 1;
-          mbar_wait(&p_full[s], (i - 1) & 1);
-          wait_entry(ev);
-          __syncwarp();
-          tc_fence_after();
-          issue_o(s, ev % kTKvStages, i > 1);
-          release(ev);
-          wait_entry(ek);
-          __syncwarp();
-          tc_fence_after();
-          issue_s(s, ek % kTKvStages);
-          commit(&s_full[s]);
-          release(ek);
+          issue_s(s, i, take());
+          commit(&s_full[2 * s + i]);
+          release();
         }
-      }
-      for (int s = 0; s < 2; ++s) {
-        const int ev = 4 * n_kv - 2 + s;
-        mbar_wait(&p_full[s], (n_kv - 1) & 1);
-        wait_entry(ev);
-        __syncwarp();
-        tc_fence_after();
-        issue_o(s, ev % kTKvStages, n_kv > 1);
-        commit(&o_full[s]);
-        release(ev);
+      for (int i = 0; i < n_kv; ++i) {
+        const int b = i & 1;
+        for (int s = 0; s < 2; ++s) {
+          mbar_wait(&p_full[2 * s + b], (i >> 1) & 1);  // P^T(i) written, S^T buffer b read
+          __syncwarp();
+          tc_fence_after();
+          issue_o(s, b, take(), i > 0);
+          commit(&pv_done[2 * s + b]);
+          if (i + 1 == n_kv) commit(&o_full[s]);
+          release();
+          if (i + 2 < n_kv) {
+            issue_s(s, b, take());
+            commit(&s_full[2 * s + b]);
+            release();
+          }
+        }
       }
     }
     __syncwarp();
@@ -292,12 +292,11 @@ __global__ void __launch_bounds__(kTThreads, 1)
     const int s = warp >> 2, wq = warp & 3;
     const int r = wq * 32 + lane;  // TMEM lane: key row of S^T, head-dim row of O^T
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const uint32_t t_s = tmem + lane_base + s * 64;
-    const uint32_t t_o = tmem + lane_base + 128 + s * 64;
+    const uint32_t t_s0 = tmem + lane_base + s * 128;  // S^T buffers at +0 / +64
+    const uint32_t t_o = tmem + lane_base + 256 + s * 64;
     const uint32_t bar_id = 1 + s;
     float* sM = sM_all[s];
     float* sA = sA_all[s];
-    float* sRed = sR_all[s];
     float* sI = sI_all[s];
     uint8_t* sPs = sP + s * L::kPT;
     const float sl2 = p.scale_log2;
@@ -333,8 +332,13 @@ __global__ void __launch_bounds__(kTThreads, 1)
         const int w = excl ? 0 : kn_valid(j);
         bias = w == 64 ? 6.f : (w > 0 ? __log2f(static_cast<float>(w)) : -INFINITY);
       }
-      mbar_wait(&s_full[s], i & 1);
+      const int b = i & 1;
+      const uint32_t t_s = t_s0 + b * 64;
+      float* sRed = reinterpret_cast<float*>(sPs);  // slow-path scratch, before this tile's P^T
+      mbar_wait(&s_full[2 * s + b], (i >> 1) & 1);
       tc_fence_after();
+      // the P^T buffer is free once PV(i-1) completed
+      if (i >= 1) mbar_wait(&pv_done[2 * s + (b ^ 1)], ((i - 1) >> 1) & 1);
       float t[64];
       // t <- scaled score + key bias (- running max per query when kSub)
       auto load_t = [&](auto sub_tag) {
@@ -392,7 +396,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
           lp[(q >> 1) + 1].y *= a4.w;
           any |= (a4.x != 1.f) | (a4.y != 1.f) | (a4.z != 1.f) | (a4.w != 1.f);
         }
-        if (i > 0 && any) {  // O^T columns (queries) * alpha; PV of tile i-1 completed (s_full order)
+        if (i > 0 && any) {  // O^T columns (queries) * alpha (PV(i-1) completed above)
+          tc_fence_after();
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
             uint32_t o[32];
@@ -432,9 +437,13 @@ __global__ void __launch_bounds__(kTThreads, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[s]);
+      if (lane == 0) mbar_arrive(&p_full[2 * s + b]);
     }
     // -------------------------------------------------------------- epilogue
+    mbar_wait(&o_full[s], 0);  // every PV of this stage complete: both P^T buffers are free
+    __syncwarp();
+    tc_fence_after();
+    float* sRed = reinterpret_cast<float*>(sPs);
     {
       float v[64];
 #pragma unroll
@@ -458,9 +467,6 @@ __global__ void __launch_bounds__(kTThreads, 1)
       }
     }
     named_bar_sync(bar_id, 128);
-    mbar_wait(&o_full[s], 0);
-    __syncwarp();
-    tc_fence_after();
     // O^T (lane = d, column = query) -> out: transposed through the stage's
     // (now idle) P^T buffer so the global stores are 16-byte row chunks
     const float res = (p.resid && present) ? p.gamma * __ldg(p.resid + ((long long)bh * p.T + u) * D + r) : 0.f;
@@ -511,7 +517,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   __syncthreads();
   if (warp == 8) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<512>(tmem);
   }
 }
 
