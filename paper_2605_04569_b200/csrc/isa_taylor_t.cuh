@@ -199,15 +199,18 @@ __global__ void __launch_bounds__(kTThreads, 1)
         ++c;
       };
       // ring order = MMA consumption order: K_0, K_1 of both stages, then per
-      // step i and stage: V_i, K_{i+2}
+      // step i and stage: V_i, K_{i+2}. Centroid tiles (i >= n_ex) are the
+      // same for both stages: loaded once (stage 0's entry) and used by both.
+      auto own = [&](int i, int s) { return s == 0 || i < n_ex; };
       for (int i = 0; i < 2 && i < n_kv; ++i)
 #pragma unroll
-        for (int s = 0; s < 2; ++s) push(tt_tile(p, bh, pos[s], i, n_ex), 0);
+        for (int s = 0; s < 2; ++s)
+          if (own(i, s)) push(tt_tile(p, bh, pos[s], i, n_ex), 0);
       for (int i = 0; i < n_kv; ++i) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-          push(tt_tile(p, bh, pos[s], i, n_ex), 1);
-          if (i + 2 < n_kv) push(tt_tile(p, bh, pos[s], i + 2, n_ex), 0);
+          if (own(i, s)) push(tt_tile(p, bh, pos[s], i, n_ex), 1);
+          if (i + 2 < n_kv && own(i + 2, s)) push(tt_tile(p, bh, pos[s], i + 2, n_ex), 0);
         }
       }
     } else if (warp == 8) {
@@ -248,24 +251,33 @@ __global__ void __launch_bounds__(kTThreads, 1)
         if (leader) mma_commit(bar);
         __syncwarp();
       };
-      int e = 0;  // ring entry
+      int e = 0;  // next ring entry
       auto take = [&]() {
-        mbar_wait(&kv_full[e % kTKvStages], (e / kTKvStages) & 1);
+        const int slot = e % kTKvStages;
+        mbar_wait(&kv_full[slot], (e / kTKvStages) & 1);
         __syncwarp();
         tc_fence_after();
-        return e % kTKvStages;
-      };
-      auto release = [&]() {
-        commit(&kv_empty[e % kTKvStages]);
         ++e;
+        return slot;
+      };
+      auto release = [&](int slot) { commit(&kv_empty[slot]); };
+      // a centroid tile's slot is taken by stage 0, reused by stage 1, then released
+      int held_k = 0, held_v = 0;
+      auto get = [&](int i, int s, int& held) { return (s == 1 && i >= n_ex) ? held : take(); };
+      auto put = [&](int i, int s, int slot, int& held) {
+        if (s == 0 && i >= n_ex)
+          held = slot;
+        else
+          release(slot);
       };
       mbar_wait(&q_full[0], 0);
       mbar_wait(&q_full[1], 0);
       for (int i = 0; i < 2 && i < n_kv; ++i)
         for (int s = 0; s < 2; ++s) {
-          issue_s(s, i, take());
+          const int slot = get(i, s, held_k);
+          issue_s(s, i, slot);
           commit(&s_full[2 * s + i]);
-          release();
+          put(i, s, slot, held_k);
         }
       for (int i = 0; i < n_kv; ++i) {
         const int b = i & 1;
@@ -273,14 +285,16 @@ __global__ void __launch_bounds__(kTThreads, 1)
           mbar_wait(&p_full[2 * s + b], (i >> 1) & 1);  // P^T(i) written, S^T buffer b read
           __syncwarp();
           tc_fence_after();
-          issue_o(s, b, take(), i > 0);
+          const int vs = get(i, s, held_v);
+          issue_o(s, b, vs, i > 0);
           commit(&pv_done[2 * s + b]);
           if (i + 1 == n_kv) commit(&o_full[s]);
-          release();
+          put(i, s, vs, held_v);
           if (i + 2 < n_kv) {
-            issue_s(s, b, take());
+            const int ks = get(i + 2, s, held_k);
+            issue_s(s, b, ks);
             commit(&s_full[2 * s + b]);
-            release();
+            put(i + 2, s, ks, held_k);
           }
         }
       }
