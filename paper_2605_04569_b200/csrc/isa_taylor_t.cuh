@@ -41,6 +41,10 @@ constexpr int kTThreads = 384;  // warps 10-11 only complete the register-donati
 #define ISA_TT_KV_STAGES 5
 #endif
 constexpr int kTKvStages = ISA_TT_KV_STAGES;  // K/V ring slots of 32 KB
+#ifndef ISA_TT_EMU
+#define ISA_TT_EMU ISA_EMU_EVERY
+#endif
+constexpr int kTTEmu = ISA_TT_EMU;  // 1 in kTTEmu exp2 pairs on the FMA pipe (0 = none)
 
 template <int D>
 struct TaylorTSmem {
@@ -431,7 +435,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       for (int q = 0; q < 64; q += 2) {
         const float2 tt = make_float2(t[q], t[q + 1]);
         float2 pp;
-        if (kEmuEvery > 0 && ((q >> 1) % kEmuEvery) == kEmuEvery - 1) {
+        if (kTTEmu > 0 && ((q >> 1) % kTTEmu) == kTTEmu - 1) {
           pp = ex2_emu2(tt);
           if (bias == -INFINITY) pp = make_float2(0.f, 0.f);
         } else {
