@@ -16,4 +16,5 @@ for _ in range(5):
     P.isa_forward(q, k, v, icl, cfg, collect_trace=False, out=out)
 b.record(); torch.cuda.synchronize()
 print(os.environ.get("ISA_LIB", ""), os.environ.get("ISA_TAYLOR_T", "default"), "ms", a.elapsed_time(b) / 5)
-torch.save(out[0, :4].cpu(), f"/tmp/out_{os.environ.get('ISA_TAYLOR_T','d')}.pt")
+tag = os.path.basename(os.environ.get("ISA_LIB", "")) or os.environ.get("ISA_TAYLOR_T", "d")
+torch.save(out[0, :4].cpu(), f"/tmp/out_{tag}.pt")
