@@ -287,9 +287,11 @@ __global__ void __launch_bounds__(kTThreads, 1)
         const int b = i & 1;
         for (int s = 0; s < 2; ++s) {
           mbar_wait(&p_full[2 * s + b], (i >> 1) & 1);  // P^T(i) written, S^T buffer b read
+          if (leader) ISA_TSTAMP(i + 1, s, 6);
           __syncwarp();
           tc_fence_after();
           const int vs = get(i, s, held_v);
+          if (leader) ISA_TSTAMP(i + 1, s, 5);
           issue_o(s, b, vs, i > 0);
           commit(&pv_done[2 * s + b]);
           if (i + 1 == n_kv) commit(&o_full[s]);
@@ -299,6 +301,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
             issue_s(s, b, ks);
             commit(&s_full[2 * s + b]);
             put(i + 2, s, ks, held_k);
+            if (leader) ISA_TSTAMP(i + 1, s, 7);
           }
         }
       }
@@ -355,6 +358,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
       float* sRed = reinterpret_cast<float*>(sPs);  // slow-path scratch, before this tile's P^T
       mbar_wait(&s_full[2 * s + b], (i >> 1) & 1);
       tc_fence_after();
+      if (wq == 0 && lane == 0) ISA_TSTAMP(i, s, 0);
       // the P^T buffer is free once PV(i-1) completed
       if (i >= 1) mbar_wait(&pv_done[2 * s + (b ^ 1)], ((i - 1) >> 1) & 1);
       float t[64];
@@ -384,6 +388,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
         }
       };
       load_t(std::true_type{});
+      if (wq == 0 && lane == 0) ISA_TSTAMP(i, s, 1);
       // speculative check: any live key above m + 8 (m = -inf on the first
       // tile gives +inf and forces the slow path; masked keys carry -inf)
       float tmax = -INFINITY;
@@ -429,6 +434,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
         }
         load_t(std::true_type{});
       }
+      if (wq == 0 && lane == 0) ISA_TSTAMP(i, s, 2);
       // P = exp2(t) (1 in kEmuEvery pairs on the FMA pipe), row-sum partials, P^T row -> smem
       uint32_t pk[32];
 #pragma unroll
@@ -452,10 +458,12 @@ __global__ void __launch_bounds__(kTThreads, 1)
           *reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) << 4)) =
               make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
       }
+      if (wq == 0 && lane == 0) ISA_TSTAMP(i, s, 3);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[2 * s + b]);
+      if (wq == 0 && lane == 0) ISA_TSTAMP(i, s, 4);
     }
     // -------------------------------------------------------------- epilogue
     mbar_wait(&o_full[s], 0);  // every PV of this stage complete: both P^T buffers are free
