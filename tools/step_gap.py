@@ -37,5 +37,15 @@ for i in range(n):
     prep()
 b.record()
 torch.cuda.synchronize()
+names = ("coarse", "select", "split", "exact", "taylor")
+in_loop = {nm: sum(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(1, n)) / (n - 1) for j, nm in enumerate(names)}
+iso = {nm: 0.0 for nm in names}
+for r in range(3):  # isolated calls (synchronize before each)
+    torch.cuda.synchronize()
+    _call_with_events(prep, structs[0], 0)
+    torch.cuda.synchronize()
+    for j, nm in enumerate(names):
+        iso[nm] += evs[0][j].elapsed_time(evs[0][j + 1]) / 3
 print(json.dumps({"loop_ms_per_step_with_events": tot, "ev0_to_ev5_ms": inner, "gap_between_steps_ms": gaps,
-                  "loop_ms_per_step_plain": a.elapsed_time(b) / n}))
+                  "loop_ms_per_step_plain": a.elapsed_time(b) / n, "stages_in_loop": in_loop,
+                  "stages_isolated": iso}))
