@@ -270,11 +270,17 @@ def run_ours(args, rank, world, local_rank):
             acc["taylor"] += evs[4].elapsed_time(evs[5])
         return {k_: v_ / reps for k_, v_ in acc.items()}
 
-    # the shipped configuration (D = 128): K6 over the sharp blocks, then the
-    # transposed Taylor kernel K7T over the flat ones, one launch each; the C
-    # ABI records an event between the two. N = 1: averaged over the timed
-    # steps themselves; N > 1: separate calls after the timed region.
+    # the shipped configuration (D = 128): one launch, K6 items over the sharp
+    # blocks and transposed-Taylor (K7T) items over the flat ones. N = 1:
+    # stage times averaged over the timed steps themselves; N > 1: separate
+    # calls after the timed region. Per-branch attribution: a separate-launch
+    # call (ISA_FLAG_SEPARATE_BRANCHES) after the timed region.
+    step_stats = None
     if world == 1:
+        per = sorted(evl[0].elapsed_time(evl[5]) for evl in step_evs)
+        q_ = lambda f: per[min(len(per) - 1, int(round(f * (len(per) - 1))))]  # noqa: E731
+        step_stats = {"median": statistics.median(per), "p10": q_(0.1), "p90": q_(0.9), "n": len(per),
+                      "note": "per-step device time (first to last kernel event of the step)"}
         shipped = {k_: 0.0 for k_ in ("coarse", "select", "split", "attn", "exact", "taylor")}
         for evl in step_evs:
             shipped["coarse"] += evl[0].elapsed_time(evl[1]) / args.steps
@@ -285,13 +291,15 @@ def run_ours(args, rank, world, local_rank):
             shipped["taylor"] += evl[4].elapsed_time(evl[5]) / args.steps
     else:
         shipped = stage_times(0)
+    separate = stage_times(1)
     stage = {"coarse": shipped["coarse"], "select": shipped["select"], "split": shipped["split"],
-             "attention": shipped["attn"], "exact_k6": shipped["exact"], "taylor_k7t": shipped["taylor"]}
+             "attention_fused": shipped["attn"], "exact_k6_separate": separate["exact"],
+             "taylor_k7t_separate": separate["taylor"]}
     peaks = _peaks()
     peak_tc = peaks.get("bf16_tflops_sustained") or 1354.8
     attn_tflops = (f_sharp + f_taylor_alg) / (shipped["attn"] * 1e-3) / 1e12
-    exact_tflops = f_sharp / (shipped["exact"] * 1e-3) / 1e12
-    taylor_tflops = f_taylor_alg / (shipped["taylor"] * 1e-3) / 1e12 if shipped["taylor"] > 0 else None
+    exact_tflops = f_sharp / (separate["exact"] * 1e-3) / 1e12
+    taylor_tflops = f_taylor_alg / (separate["taylor"] * 1e-3) / 1e12 if separate["taylor"] > 0 else None
     prof = _profile_summary()
 
     result = {
@@ -305,23 +313,24 @@ def run_ours(args, rank, world, local_rank):
         "tflops_dense_equiv": f_dense / (ms * 1e-3) / 1e12,
         "flops": {"isa": f_isa, "dense": f_dense, "sharp": f_sharp * world, "taylor_alg": f_taylor_alg * world},
         "stage_ms": stage,
+        "step_ms_stats": step_stats,
         "gpu_launches": launches * args.steps,
         "roofline": {
-            "kernel": "gba_attention_kernel<128, MODE_EXACT> (K6, sharp branch)",
-            "bound": "tensor", "achieved": exact_tflops, "peak": peak_tc, "unit": "TFLOP/s",
-            "frac": exact_tflops / peak_tc, "traffic": prof.get("k6_dram_bytes"),
+            "kernel": "gba_isa_t_kernel<128> (K6 sharp + K7T transposed-Taylor items, one launch)",
+            "bound": "tensor", "achieved": attn_tflops, "peak": peak_tc, "unit": "TFLOP/s",
+            "frac": attn_tflops / peak_tc, "traffic": prof.get("attn_dram_bytes"),
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a ~23 ms step)",
-            "algorithmic": "F_sharp = 4*b^2*D*n_sharp*t_new (pipeline.py:278) per launch / average CUDA-event "
-                           "duration of the launch over the timed steps, on its stream",
+            "algorithmic": "F_sharp + F_taylor (pipeline.py:269-289, taylor.py:299-316) per launch / average "
+                           "CUDA-event duration of the launch over the timed steps, on its stream",
         },
-        "attention_kernels": {"achieved": attn_tflops, "frac": attn_tflops / peak_tc, "unit": "TFLOP/s",
-                              "algorithmic": "F_sharp + F_taylor (pipeline.py:269-289, taylor.py:299-316) / "
-                                             "K6 + K7T time"},
         "exact_kernel": {"achieved": exact_tflops, "frac": exact_tflops / peak_tc, "unit": "TFLOP/s",
-                         "algorithmic": "F_sharp = 4*b^2*D*n_sharp*t_new (pipeline.py:278)"},
+                         "kernel": "gba_attention_kernel<128, MODE_EXACT> (K6)",
+                         "algorithmic": "F_sharp = 4*b^2*D*n_sharp*t_new (pipeline.py:278)",
+                         "timed": "separate launch (ISA_FLAG_SEPARATE_BRANCHES)", "traffic": prof.get("k6_dram_bytes")},
         "taylor_kernel": {"achieved": taylor_tflops, "frac": (taylor_tflops / peak_tc) if taylor_tflops else None,
                           "unit": "TFLOP/s", "kernel": "gba_taylor_t_kernel<128> (K7T)",
                           "algorithmic": "reference flop_count (taylor.py:299-316)",
+                          "timed": "separate launch (ISA_FLAG_SEPARATE_BRANCHES)",
                           "traffic": prof.get("k7t_dram_bytes"), "l2_bytes": prof.get("k7t_l2_bytes")},
         "clocks": clocks,
     }

@@ -337,6 +337,24 @@ int launch_taylor_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensor
   return ISA_OK;
 }
 
+// K6 + K7T in one grid (D = 128)
+int launch_isa_t_fused(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
+                       const CUtensorMap& tvc, const isa::AttnParams& pe, const isa::AttnParams& pt, int items_e,
+                       int BH, cudaStream_t st) {
+  constexpr int kA = isa::TaylorTSmem<128>::kAlloc > isa::AttnSmem<128>::kAlloc ? isa::TaylorTSmem<128>::kAlloc
+                                                                                : isa::AttnSmem<128>::kAlloc;
+  static bool configured = false;
+  if (!configured) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::gba_isa_t_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kA));
+    configured = true;
+  }
+  const int items_t = (pt.n_qblk + 1) / 2;
+  isa::gba_isa_t_kernel<128><<<dim3(items_e + items_t, BH), isa::kTThreads, kA, st>>>(tq, tk, tv, tkc, tvc, pe, pt,
+                                                                                     items_e);
+  ISA_LAUNCHED("gba_isa_t_kernel");
+  return ISA_OK;
+}
+
 int launch_isa_fused(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& pe,
                      const isa::AttnParams& pt, int items_e, int items_t, int BH, cudaStream_t st) {
@@ -792,8 +810,12 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
   }
   const bool taylor_t = d.n_flat && d.D == 128 && taylor_t_mode();
   const bool fuse = d.n_sharp && d.n_flat && !taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES);
-  if (taylor_t) {
-    // K6 over the sharp blocks, then K7T over the flat ones
+  if (taylor_t && d.n_sharp && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES)) {
+    // K6 + K7T in one grid (Taylor CTAs fill the tail of the last K6 wave)
+    if ((rc = launch_isa_t_fused(tq, tk, tv, tkc, tvc, ps, pf, d.items_s, d.BH, st))) return rc;
+    record(events, 4, st);
+  } else if (taylor_t) {
+    // K6 over the sharp blocks, then K7T over the flat ones (per-branch attribution)
     if (d.n_sharp)
       if ((rc = launch_attention_d<isa::MODE_EXACT>(d.D, tq, tk, tv, tq, tq, ps, d.items_s, d.BH, st))) return rc;
     record(events, 4, st);

@@ -101,10 +101,10 @@ __device__ __forceinline__ TTileSrc tt_tile(const AttnParams& p, int bh, int pos
 }
 
 template <int D>
-__global__ void __launch_bounds__(kTThreads, 1)
-    gba_taylor_t_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
-                        const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
+__device__ __forceinline__ void taylor_t_body(const CUtensorMap& tm_q, const CUtensorMap& tm_k,
+                                              const CUtensorMap& tm_v, const CUtensorMap& tm_kc,
+                                              const CUtensorMap& tm_vc, const AttnParams& p, const int item,
+                                              const int bh) {
   using L = TaylorTSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -126,7 +126,6 @@ __global__ void __launch_bounds__(kTThreads, 1)
   uint64_t* o_full = bars + 14 + 2 * kTKvStages;    // [stage]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * kTKvStages);
 
-  const int item = blockIdx.x, bh = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_ex = (p.kmask + 1) >> 1;
   const int n_kv = n_ex + p.tn_pad / 128;
@@ -545,6 +544,29 @@ __global__ void __launch_bounds__(kTThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTThreads, 1)
+    gba_taylor_t_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
+                        const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
+  taylor_t_body<D>(tm_q, tm_k, tm_v, tm_kc, tm_vc, p, blockIdx.x, blockIdx.y);
+}
+
+// K6 and K7T in one grid: CTAs [0, n_exact) run the sharp items (long), the
+// rest the transposed Taylor items (short), which fill the tail of the last
+// K6 wave instead of starting after it.
+template <int D>
+__global__ void __launch_bounds__(kTThreads, 1)
+    gba_isa_t_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
+                     const __grid_constant__ CUtensorMap tm_vc, const AttnParams pe, const AttnParams pt,
+                     const int n_exact) {
+  if ((int)blockIdx.x < n_exact)
+    gba_body<D, MODE_EXACT>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pe, blockIdx.x, blockIdx.y);
+  else
+    taylor_t_body<D>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pt, blockIdx.x - n_exact, blockIdx.y);
 }
 
 }  // namespace isa
