@@ -219,3 +219,16 @@ def test_padded_head_dim_backward_and_trace():
     dense = P.dense_attention(q, k, v)
     ref = torch.softmax((q.float() @ k.float().transpose(-1, -2)) / math.sqrt(D), -1) @ v.float()
     assert (dense.float() - ref).abs().max().item() < 2e-2
+
+
+# ------------------------------------------------------------------ K7T corner cases (D = 128)
+@pytest.mark.parametrize("l_src,l_ctx,kw", [
+    (64 * 11, 64 * 10, dict(alpha_f=0.5, alpha_ns=0.01)),                  # k = 1: a centroid tile in the prologue
+    (64 * 12 + 7, 64 * 9 - 20, dict(strict=False, alpha_f=0.45)),          # ragged: short exact blocks, weights
+    (64 * 9, 64 * 12, dict(alpha_f=0.55, alpha_s=0.5, alpha_ns=0.3)),      # n_flat = 11: an absent second stage
+    (64 * 20, 64 * 20, dict(alpha_f=1.0, alpha_ns=1.0)),                   # every block flat and fully exact
+])
+def test_transposed_taylor_corners_vs_oracle(l_src, l_ctx, kw):
+    q, k, v = _inputs(1, 2, l_src + l_ctx, 128, seed=l_src + 7 * l_ctx, kind="clustered")
+    out = _run_and_compare(q, k, v, l_src, l_ctx, kw)
+    assert torch.isfinite(out).all()
