@@ -37,7 +37,7 @@ from .types import (
 
 from .tensorio import dump, load, load_tensor4, save_tensor4
 from .workload import WorkloadSpec, generate
-from .taylor import TaylorKernelInput, flop_count, taylor_sparse_forward
+from .taylor import TaylorKernelInput, flop_count, taylor_sparse_backward, taylor_sparse_forward
 
 __version__ = "0.1.0"
 
@@ -50,7 +50,7 @@ def __getattr__(name):
         from . import pipeline
 
         return getattr(pipeline, name)
-    if name in ("full_attention", "online_softmax_attention"):
+    if name in ("full_attention", "online_softmax_attention", "full_attention_backward"):
         from . import exact
 
         return getattr(exact, name)

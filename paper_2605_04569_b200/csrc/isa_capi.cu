@@ -602,7 +602,8 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   record(ev, 2, st);
   // ---- stage 3: split + block mask
   if (pinned) {
-    if (!pinned->sharp || (d.n_flat && !pinned->flat)) return fail(ISA_ERR_CONTRACT, "pinned routing lacks split");
+    if ((d.n_sharp && !pinned->sharp) || (d.n_flat && !pinned->flat))
+      return fail(ISA_ERR_CONTRACT, "pinned routing lacks split");
     if (d.n_sharp) {
       isa::narrow_kernel<<<grid1d(BH * d.n_sharp, 256), 256, 0, st>>>(pinned->sharp, w.sharp, BH * d.n_sharp);
       ISA_LAUNCHED("narrow_kernel");

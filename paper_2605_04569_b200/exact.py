@@ -154,3 +154,32 @@ def online_softmax_attention(q, k, v, scale: Optional[float] = None, layout=None
     if layout is not None and layout.seq_len != S_k:
         raise LayoutError(f"layout.seq_len {layout.seq_len} != key length {S_k}")
     return _exact(q, k, v, scale, mask)
+
+
+def full_attention_backward(q, k, v, scale: Optional[float] = None, do=None, mask=None, row_chunk: int = 2048):
+    """Analytic gradients of full_attention (reference.py:173-225, same argument
+    order). Self-attention (S_q == S_k) runs the tcgen05 backward kernels of
+    `isa_backward` on the all-exact configuration (one segment, alpha_f = 0:
+    every query block attends to every key block — ISA's dense identity);
+    S_q != S_k and key masks that drop keys raise ConfigError. Returns a
+    GradBundle in q's dtype (numpy fp32 for numpy inputs)."""
+    del row_chunk
+    from .pipeline import isa_backward
+    from .types import IclLayout, IsaConfig
+
+    (B, H, S_q, D), (_, _, S_k, _), _ = (_shape4(x, n) for x, n in ((q, "Q"), (k, "K"), (v, "V")))
+    if do is None:
+        raise LayoutError("dO is required")
+    if tuple(int(x) for x in do.shape) != (B, H, S_q, int(v.shape[3])):
+        raise LayoutError(f"dO shape {tuple(do.shape)} != output shape {(B, H, S_q, int(v.shape[3]))}")
+    if scale is not None and scale <= 0:
+        raise ConfigError(f"scale must be > 0, got {scale}")
+    km = _key_mask(mask, B, H, S_k)
+    if km is not None and not km.all():
+        if not km.any(axis=2).all():
+            raise DegenerateRowError("query row with all keys masked")
+        raise ConfigError("key masks that drop keys are not supported by the sm_100a kernels")
+    if S_q != S_k:
+        raise ConfigError("full_attention_backward on the sm_100a kernels needs S_q == S_k")
+    cfg = IsaConfig(alpha_s=1.0, alpha_f=0.0, scale=scale, strict=False)
+    return isa_backward(q, k, v, IclLayout(S_q, 0), cfg, do)

@@ -188,3 +188,38 @@ def flop_count(inp: TaylorKernelInput) -> FlopCount:
     exact_pair, taylor_pair = 4 * b * b * D, 4 * b * D
     return FlopCount(exact_mas=B * H * t_q * k * exact_pair, taylor_mas=B * H * t_q * (t_k - k) * taylor_pair,
                      overhead_mas=0, dense_equivalent_mas=B * H * t_q * t_k * exact_pair)
+
+
+def taylor_sparse_backward(inp: TaylorKernelInput, do):
+    """Gradients of taylor_sparse_forward (taylor.py:225-296): the Taylor
+    branch's gradients to Q, and to K_new / V_new directly and through the
+    block means. Self-attention geometry (S_q == S_k, full blocks) runs the
+    tcgen05 backward of `isa_backward` with the caller's mask pinned as the
+    routing (one segment, every query block flat); otherwise ConfigError."""
+    import torch
+
+    from .pipeline import isa_backward
+    from .types import BlockMask, IclLayout, IsaConfig, IsaRouting, SelectionIndex, SharpnessSplit
+
+    inp = inp.validated()
+    B, H, S_q, D = _shape4(inp.q, "Q")
+    S_k = int(inp.k_new.shape[2])
+    b = inp.block_size
+    if tuple(int(x) for x in do.shape) != (B, H, S_q, int(inp.v_new.shape[3])):
+        raise LayoutError(f"dO shape {tuple(do.shape)} != output shape")
+    if S_q != S_k:
+        raise ConfigError("taylor_sparse_backward on the sm_100a kernels needs S_q == S_k")
+    if inp.key_valid_rows is not None and np.any(np.asarray(inp.key_valid_rows) != b):
+        raise ConfigError("partial key blocks (key_valid_rows < block_size) are not supported by the sm_100a "
+                          "Taylor kernel")
+    t = S_q // b
+    idx = _np(inp.mask.indices).astype(np.int64)
+    k = int(idx.shape[3])
+    alpha_ns = min(1.0, (k + 0.5) / t)  # floor(alpha_ns * t) == k (coarse.py:169)
+    cfg = IsaConfig(alpha_s=1.0, alpha_f=1.0, alpha_ns=alpha_ns, scale=inp.scale, block_size=b)
+    flat = np.broadcast_to(np.arange(t, dtype=np.int64), (B, H, t)).copy()
+    routing = IsaRouting(selection=SelectionIndex(np.zeros((B, H, 0), np.int64), 0),
+                         split=SharpnessSplit(sharp=np.zeros((B, H, 0), np.int64), flat=flat,
+                                              sharpness=np.zeros((B, H, t))),
+                         mask=BlockMask(idx, t))
+    return isa_backward(inp.q, inp.k_new, inp.v_new, IclLayout(S_q, 0), cfg, do, routing=routing)

@@ -87,3 +87,31 @@ def test_torch_strided_cross():
     assert out.dtype == torch.bfloat16 and tuple(out.shape) == (2, 3, 700, 128)
     ref = torch.softmax((tq.float() @ tk.float().transpose(-1, -2)) / np.sqrt(128), -1) @ tv.float()
     assert (out.float() - ref).abs().max().item() < 2e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [c for c in CASES if c.endswith("_bwd")])
+def test_backward_matches_reference_golden(name):
+    """full_attention_backward (reference.py:173-225) vs the reference's gradients."""
+    import paper_2605_04569_b200 as P
+
+    (q, k, v), g = _case(name)
+    seed = int(g["geom"][5])
+    do = O.round_bf16(np.random.default_rng(seed + 1000).standard_normal(g["out"].shape).astype(np.float32))
+    grads = P.full_attention_backward(q, k, v, None, do)
+    for key, got in (("dq", grads.dq), ("dk", grads.dk), ("dv", grads.dv)):
+        a = np.asarray(got, dtype=np.float64).ravel()
+        r = np.asarray(g[key], dtype=np.float64).ravel()
+        cos = float(a @ r / (np.linalg.norm(a) * np.linalg.norm(r)))
+        assert cos >= 0.999 and float(np.abs(a - r).max()) <= 3e-2 * float(np.abs(r).max()), (key, cos)
+
+
+def test_backward_errors_before_device():
+    from paper_2605_04569_b200.errors import ConfigError, LayoutError
+    from paper_2605_04569_b200.exact import full_attention_backward
+
+    q, k, v = make_inputs(1, 1, 64, 128, 64, 0)
+    with pytest.raises(LayoutError, match="dO"):
+        full_attention_backward(q, k, v, None, None)
+    with pytest.raises(ConfigError, match="S_q == S_k"):
+        full_attention_backward(q, k, v, None, np.zeros_like(q))

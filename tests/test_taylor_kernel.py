@@ -144,3 +144,25 @@ def _partial_means(x, valid):
     for t, n in enumerate(valid):
         out[0, 0, t] = x[0, 0, t * 64:t * 64 + n].astype(np.float64).mean(axis=0)
     return out
+
+
+def _grad_close(got, ref, name):
+    a = np.asarray(got, dtype=np.float64).ravel()
+    r = np.asarray(ref, dtype=np.float64).ravel()
+    cos = float(a @ r / (np.linalg.norm(a) * np.linalg.norm(r) + 1e-300))
+    err = float(np.abs(a - r).max())
+    assert cos >= 0.999 and err <= 3e-2 * float(np.abs(r).max()), (name, cos, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [c for c in CASES if "dq" in np.load(os.path.join(GOLD, f"{c}.npz")).files])
+def test_backward_matches_reference_golden(name):
+    """taylor_sparse_backward (taylor.py:225-296) vs the reference's gradients."""
+    from paper_2605_04569_b200.taylor import taylor_sparse_backward
+
+    inp, g = _case(name)
+    B, H, t_q, t_k, D, k, seed = (int(x) for x in g["geom"])
+    do = O.round_bf16(np.random.default_rng(seed + 1000).standard_normal(g["out"].shape).astype(np.float32))
+    grads = taylor_sparse_backward(inp, do)
+    for key, got in (("dq", grads.dq), ("dk", grads.dk), ("dv", grads.dv)):
+        _grad_close(got, g[key], key)
