@@ -50,6 +50,10 @@ def __getattr__(name):
         from . import pipeline
 
         return getattr(pipeline, name)
+    if name in ("CoarseSet", "build_coarse", "rank_context", "build_block_mask", "sharpness_split"):
+        from . import coarse
+
+        return getattr(coarse, name)
     if name in ("full_attention", "online_softmax_attention", "full_attention_backward"):
         from . import exact
 
