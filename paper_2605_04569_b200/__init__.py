@@ -50,7 +50,7 @@ def __getattr__(name):
         from . import pipeline
 
         return getattr(pipeline, name)
-    if name in ("CoarseSet", "build_coarse", "rank_context", "build_block_mask", "sharpness_split"):
+    if name in ("CoarseSet", "build_coarse", "rank_context", "build_block_mask", "sharpness_split", "block_mean"):
         from . import coarse
 
         return getattr(coarse, name)

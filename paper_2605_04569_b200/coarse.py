@@ -78,6 +78,22 @@ def _block_means(x: torch.Tensor, layout: BlockLayout) -> torch.Tensor:
     return means[0]
 
 
+def block_mean(x, layout: BlockLayout):
+    """Per-block mean over each block's valid rows with fp64 accumulation
+    (tensor.py:96-119) on the pooling kernel. `x` may hold layout.seq_len or
+    layout.padded_len rows (padded rows never contribute). numpy in -> numpy
+    float32 out; torch in -> fp32 device tensor."""
+    numpy_io = isinstance(x, np.ndarray)
+    t = _device_tensor(x, "block_mean input")
+    if t.shape[2] not in (layout.seq_len, layout.padded_len):
+        raise LayoutError(f"block_mean: seq length {t.shape[2]} matches neither layout.seq_len "
+                          f"{layout.seq_len} nor padded_len {layout.padded_len}")
+    if t.shape[2] != layout.seq_len:
+        t = t[:, :, :layout.seq_len].contiguous()
+    out = _block_means(t, layout)
+    return out.cpu().numpy() if numpy_io else out
+
+
 def build_coarse(q, k, v, q_layout: BlockLayout, k_layout: BlockLayout, scale: Optional[float] = None) -> CoarseSet:
     """Block means of Q (over q_layout) and K, V (over k_layout) and
     s_coarse = scale * qc . kc^T in float64 (coarse.py:110-127)."""

@@ -63,3 +63,23 @@ def test_matches_reference_golden(name):
     np.testing.assert_array_equal(split.sharp.cpu().numpy(), g["sharp"])
     np.testing.assert_array_equal(split.flat.cpu().numpy(), g["flat"])
     np.testing.assert_allclose(split.sharpness.cpu().numpy(), g["sharpness"], rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.gpu
+def test_block_mean_seq_and_padded_inputs():
+    """block_mean (tensor.py:96-119) on unpadded and pre-padded inputs (ragged last block)."""
+    import torch
+
+    import paper_2605_04569_b200 as P
+    from paper_2605_04569_b200.coarse import block_mean
+
+    g = np.load(os.path.join(GOLD, f"{CASES[0]}.npz"))
+    B, H, ls, lc, D, seed = (int(x) for x in g["params"][:6])
+    q, _, _ = make_inputs(B, H, ls + lc, D, seed)
+    np.testing.assert_array_equal(block_mean(q, P.BlockLayout(64, ls + lc)), g["qc"])
+    S = ls + lc - 37  # ragged: last block has 27 valid rows
+    lay = P.BlockLayout(64, S)
+    ref = O.block_mean(q[:, :, :S], 64)
+    np.testing.assert_array_equal(block_mean(q[:, :, :S], lay), ref)
+    padded = np.concatenate([q[:, :, :S], np.full((B, H, lay.padded_len - S, D), 7.0, np.float32)], axis=2)
+    np.testing.assert_array_equal(block_mean(torch.from_numpy(padded).cuda(), lay).cpu().numpy(), ref)
