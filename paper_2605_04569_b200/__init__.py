@@ -36,6 +36,7 @@ from .types import (
 )
 
 from .tensorio import dump, load, load_tensor4, save_tensor4
+from .util import elementwise_relative_error, max_relative_error, mean_relative_error
 from .workload import WorkloadSpec, generate
 from .taylor import TaylorKernelInput, flop_count, taylor_sparse_backward, taylor_sparse_forward
 

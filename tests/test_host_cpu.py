@@ -231,3 +231,20 @@ def test_head_dim_padding_plan():
     assert _pad_head_dim(IsaConfig(scale=0.5), torch.ones(1, 1, 1, 40))[0].scale == 0.5
     for D in (64, 128, 129, 256):
         assert _pad_head_dim(IsaConfig(), torch.ones(1, 1, 1, D)) is None
+
+
+def test_error_metrics_match_reference_definitions():
+    """util.py:8-29 restated: numpy and (CPU) torch inputs give the same numbers."""
+    import numpy as np
+    import torch
+
+    from paper_2605_04569_b200 import elementwise_relative_error, max_relative_error, mean_relative_error
+
+    rng = np.random.default_rng(3)
+    a, r = rng.standard_normal((2, 3, 5, 4)), rng.standard_normal((2, 3, 5, 4))
+    assert max_relative_error(a, r) == float(np.max(np.abs(a - r))) / float(np.max(np.abs(r)))
+    assert abs(mean_relative_error(a, r) - float(np.mean(np.abs(a - r))) / float(np.mean(np.abs(r)))) < 1e-15
+    want = float(np.max(np.abs(a - r) / (np.maximum(np.abs(a), np.abs(r)) + 1e-12)))
+    assert abs(elementwise_relative_error(a, r) - want) < 1e-15
+    assert abs(max_relative_error(torch.from_numpy(a), torch.from_numpy(r)) - max_relative_error(a, r)) < 1e-15
+    assert max_relative_error(np.zeros(0), np.zeros(0)) == 0.0
