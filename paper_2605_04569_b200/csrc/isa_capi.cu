@@ -585,9 +585,16 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
                                                    w.ctx_short);
   ISA_LAUNCHED("kvblk_from_sel_kernel");
   if (need_scores) {
-    dim3 g((d.t_new + 127) / 128, (d.T + 127) / 128, d.BH);
-    isa::coarse_kernel<<<g, 256, 0, st>>>(qc, kc, w.kv_blk, d.T, d.t_new, d.D, d.scale, w.s_new);
-    ISA_LAUNCHED("coarse_kernel");
+    const char* c128 = getenv("ISA_COARSE_N64");
+    if (!(c128 && c128[0] == '0')) {  // default: 128x64 tiles, 2 CTAs/SM (ISA_COARSE_N64=0: 128x128 tiles)
+      dim3 g((d.t_new + 63) / 64, (d.T + 127) / 128, d.BH);
+      isa::coarse_kernel_n64<<<g, 256, 0, st>>>(qc, kc, w.kv_blk, d.T, d.t_new, d.D, d.scale, w.s_new);
+      ISA_LAUNCHED("coarse_kernel_n64");
+    } else {
+      dim3 g((d.t_new + 127) / 128, (d.T + 127) / 128, d.BH);
+      isa::coarse_kernel<<<g, 256, 0, st>>>(qc, kc, w.kv_blk, d.T, d.t_new, d.D, d.scale, w.s_new);
+      ISA_LAUNCHED("coarse_kernel");
+    }
   }
   if (d.n_flat) {
     isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};

@@ -668,6 +668,76 @@ __global__ void __launch_bounds__(64) taylor_plan_kernel(const uint32_t* __restr
   if (threadIdx.x == 0) n_tiles[bh * n_items + item] = nt;
 }
 
+// Same scores, 128 x 64 output tiles: 8 x 4 outputs per thread (half the
+// accumulators), so two CTAs (16 warps) fit per SM and hide the DFMA / LDS
+// latencies better; same sequential fp64 FMA order over d, so the values are
+// bit-identical to coarse_kernel. grid (ceil(n/64), ceil(T/128), BH).
+__global__ void __launch_bounds__(256, 2) coarse_kernel_n64(const float* __restrict__ qc, const float* __restrict__ kc,
+                                                            const int* __restrict__ kv_blk, int T, int n, int D,
+                                                            double scale, double* __restrict__ s_out) {
+  __shared__ double As[8][128];
+  __shared__ double Bs[8][64];
+  __shared__ int colrow[64];
+  const int bh = blockIdx.z;
+  const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 64;
+  const float* qb = qc + (long long)bh * T * D;
+  const float* kb = kc + (long long)bh * T * D;
+  if (threadIdx.x < 64) {
+    const int j = j0 + threadIdx.x;
+    colrow[threadIdx.x] = j < n ? (kv_blk ? kv_blk[(long long)bh * n + j] : j) : -1;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[8][4];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  // loaders: A = 128 rows x 8 d (thread -> row tid/2, 4 d); B = 64 rows x 8 d (threads < 128)
+  const int lr = threadIdx.x >> 1, ld = (threadIdx.x & 1) * 4;
+  const int gi = i0 + lr;
+  const float* arow = gi < T ? qb + (long long)gi * D + ld : nullptr;
+  const int gj = threadIdx.x < 128 ? colrow[lr] : -1;
+  const float* brow = gj >= 0 ? kb + (long long)gj * D + ld : nullptr;
+  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow)) : zero4;
+  float4 b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow)) : zero4;
+  for (int d0 = 0; d0 < D; d0 += 8) {
+    As[ld + 0][lr] = a4.x; As[ld + 1][lr] = a4.y; As[ld + 2][lr] = a4.z; As[ld + 3][lr] = a4.w;
+    if (threadIdx.x < 128) {
+      Bs[ld + 0][lr] = b4.x; Bs[ld + 1][lr] = b4.y; Bs[ld + 2][lr] = b4.z; Bs[ld + 3][lr] = b4.w;
+    }
+    __syncthreads();
+    if (d0 + 8 < D) {
+      a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow + d0 + 8)) : zero4;
+      b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow + d0 + 8)) : zero4;
+    }
+#pragma unroll
+    for (int dd = 0; dd < 8; ++dd) {
+      double a[8], bv[4];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] = As[dd][ty + 16 * t];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) bv[t] = Bs[dd][tx + 16 * t];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], bv[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + ty + 16 * r;
+    if (i >= T) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + tx + 16 * c;
+      if (j < n) s_out[((long long)bh * T + i) * n + j] = scale * acc[r][c];
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------
 // Coarse residual O_coarse (pipeline.py:261-267): per query block u,
 //   softmax variant  O_u = sum_j softmax_j(scale * qc_u . kc_j) vc_j
