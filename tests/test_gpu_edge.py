@@ -232,3 +232,24 @@ def test_transposed_taylor_corners_vs_oracle(l_src, l_ctx, kw):
     q, k, v = _inputs(1, 2, l_src + l_ctx, 128, seed=l_src + 7 * l_ctx, kind="clustered")
     out = _run_and_compare(q, k, v, l_src, l_ctx, kw)
     assert torch.isfinite(out).all()
+
+
+def test_prepared_call_replays_as_cuda_graph():
+    """The prepared forward (one C-ABI call: routing + fused attention, no host
+    sync) captures into a CUDA graph; replays match the eager result bit for bit."""
+    P = _P()
+    q, k, v = (_bf16(x) for x in _inputs(1, 4, 4096, 128, seed=11))
+    prep = P.prepare(q, k, v, P.IclLayout(2048, 2048), P.IsaConfig())
+    eager = prep().clone()  # warm-up: one-time kernel attribute setup happens outside the capture
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            prep(stream=side.cuda_stream)
+    torch.cuda.current_stream().wait_stream(side)
+    prep.out.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(prep.out, eager)
