@@ -35,6 +35,7 @@ from .types import (
     SharpnessSplit,
 )
 
+from .blocks import concat_seq, ensure_tensor4, gather_blocks, pad_to_blocks, scatter_blocks
 from .tensorio import dump, load, load_tensor4, save_tensor4
 from .util import elementwise_relative_error, max_relative_error, mean_relative_error
 from .workload import WorkloadSpec, generate
