@@ -187,6 +187,7 @@ struct Workspace {
   int* ctx_short;     // [BH]
   int4* tiles;        // [BH][items_f][max_tiles]
   int* n_tiles;       // [BH][items_f]
+  int* taylor_pick;   // [BH]: 0 = row-major K7 (union tiles), 1 = transposed K7T
   float* resid;       // [BH][T][D] coarse residual rows (gamma > 0 only)
   size_t bytes;
 };
@@ -222,6 +223,7 @@ Workspace carve(const Dims& d, int dtype, uint8_t* base) {
   w.tiles = reinterpret_cast<int4*>(take(16ull * BH * d.items_f * 2 * d.max_tiles));
   w.n_tiles = reinterpret_cast<int*>(take(4ull * BH * d.items_f));
   w.resid = d.gamma > 0.0 ? reinterpret_cast<float*>(take(4ull * BH * d.T * d.D)) : nullptr;
+  w.taylor_pick = reinterpret_cast<int*>(take(4ull * BH));
   w.bytes = off;
   return w;
 }
@@ -319,6 +321,36 @@ bool taylor_t_mode() {
     return !(e && e[0] == '0');
   }();
   return v;
+}
+
+// Taylor-branch kernel choice per head (ISA_TAYLOR_PICK): -1 = auto (plan
+// statistics), 0 = always the row-major K7, 1 = always K7T.
+int taylor_pick_mode() {
+  static int v = [] {
+    const char* e = getenv("ISA_TAYLOR_PICK");
+    if (e && e[0] == '7' && e[1] == 't') return 1;
+    if (e && e[0] == '7') return 0;
+    return -1;
+  }();
+  return v;
+}
+
+// K6 + (per head) K7 or K7T items in one grid (D = 128).
+int launch_isa_hybrid(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
+                      const CUtensorMap& tvc, const isa::AttnParams& pe, const isa::AttnParams& pt, int items_e,
+                      int items_k7, const int* pick, int BH, cudaStream_t st) {
+  constexpr int kA = isa::TaylorTSmem<128>::kAlloc > isa::AttnSmem<128>::kAlloc ? isa::TaylorTSmem<128>::kAlloc
+                                                                                : isa::AttnSmem<128>::kAlloc;
+  static bool configured = false;
+  if (!configured) {
+    ISA_CUDA(cudaFuncSetAttribute(isa::gba_isa_hybrid_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kA));
+    configured = true;
+  }
+  const int items_t = (pt.n_qblk + 1) / 2;
+  isa::gba_isa_hybrid_kernel<128><<<dim3(items_e + items_k7 + items_t, BH), isa::kTThreads, kA, st>>>(
+      tq, tk, tv, tkc, tvc, pe, pt, items_e, items_k7, pick);
+  ISA_LAUNCHED("gba_isa_hybrid_kernel");
+  return ISA_OK;
 }
 
 int launch_taylor_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
@@ -652,6 +684,9 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
                                                                    w.kv_blk, d.t_new, d.t_src, d.l_src, d.l_ctx,
                                                                    w.tiles, w.n_tiles);
     ISA_LAUNCHED("taylor_plan_kernel");
+    isa::taylor_pick_kernel<<<d.BH, 128, 0, st>>>(w.n_tiles, d.items_f, d.n_flat, d.k, taylor_pick_mode(),
+                                                  w.taylor_pick);
+    ISA_LAUNCHED("taylor_pick_kernel");
   }
   record(ev, 3, st);
   return ISA_OK;
@@ -819,8 +854,11 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
   const bool taylor_t = d.n_flat && d.D == 128 && taylor_t_mode();
   const bool fuse = d.n_sharp && d.n_flat && !taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES);
   if (taylor_t && d.n_sharp && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES)) {
-    // K6 + K7T in one grid (Taylor CTAs fill the tail of the last K6 wave)
-    if ((rc = launch_isa_t_fused(tq, tk, tv, tkc, tvc, ps, pf, d.items_s, d.BH, st))) return rc;
+    // K6 + Taylor items in one grid (the short Taylor CTAs fill the tail of
+    // the last K6 wave); per head the Taylor branch runs as K7T or, when the
+    // paired exact lists overlap enough that the union tiles cost less, K7
+    if ((rc = launch_isa_hybrid(tq, tk, tv, tkc, tvc, ps, pf, d.items_s, d.items_f, w.taylor_pick, d.BH, st)))
+      return rc;
     record(events, 4, st);
   } else if (taylor_t) {
     // K6 over the sharp blocks, then K7T over the flat ones (per-branch attribution)

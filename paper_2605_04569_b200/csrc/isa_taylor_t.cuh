@@ -569,4 +569,44 @@ __global__ void __launch_bounds__(kTThreads, 1)
     taylor_t_body<D>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pt, blockIdx.x - n_exact, blockIdx.y);
 }
 
+// Per head: row-major K7 (pair-of-blocks union tiles, one K/V load serves
+// both blocks of a pair, but every union tile costs a full 128x128 MMA pair)
+// or K7T (each block's own tiles, no MMA waste, no load sharing). Operand
+// traffic decides (both kernels are bound by it): K7 streams 2 * n_tiles
+// tiles per 4-block item, K7T ceil(k/2) per block. K7 is taken when its tile
+// count is below 0.8 x K7T's (measured break-even: K7T 3.3 ms vs K7 4.1 ms
+// at equal counts on cfg3). mode >= 0 forces the choice.
+__global__ void taylor_pick_kernel(const int* __restrict__ n_tiles, int n_items, int n_flat, int k, int mode,
+                                   int* __restrict__ pick) {
+  const int bh = blockIdx.x;
+  long long sum = 0;
+  for (int i = threadIdx.x; i < n_items; i += blockDim.x) sum += n_tiles[(long long)bh * n_items + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  __shared__ long long part[4];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long k7 = 2 * (part[0] + part[1] + part[2] + part[3]);
+    const long long k7t = (long long)n_flat * ((k + 1) / 2);
+    pick[bh] = mode >= 0 ? mode : (5 * k7 < 4 * k7t ? 0 : 1);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTThreads, 1)
+    gba_isa_hybrid_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
+                          const __grid_constant__ CUtensorMap tm_vc, const AttnParams pe, const AttnParams pt,
+                          const int n_exact, const int n_k7, const int* __restrict__ pick) {
+  const int x = blockIdx.x, bh = blockIdx.y;
+  if (x < n_exact) {
+    gba_body<D, MODE_EXACT>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pe, x, bh);
+  } else if (x < n_exact + n_k7) {
+    if (__ldg(pick + bh) == 0) gba_body<D, MODE_TAYLOR>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pt, x - n_exact, bh);
+  } else {
+    if (__ldg(pick + bh) == 1) taylor_t_body<D>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pt, x - n_exact - n_k7, bh);
+  }
+}
+
 }  // namespace isa
