@@ -316,7 +316,7 @@ def run_ours(args, rank, world, local_rank):
         "step_ms_stats": step_stats,
         "gpu_launches": launches * args.steps,
         "roofline": {
-            "kernel": "gba_isa_t_kernel<128> (K6 sharp + K7T transposed-Taylor items, one launch)",
+            "kernel": "gba_isa_hybrid_kernel<128> (K6 sharp items + per-head K7T / K7 Taylor items, one launch)",
             "bound": "tensor", "achieved": attn_tflops, "peak": peak_tc, "unit": "TFLOP/s",
             "frac": attn_tflops / peak_tc, "traffic": prof.get("attn_dram_bytes"),
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a ~23 ms step)",

@@ -369,24 +369,6 @@ int launch_taylor_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensor
   return ISA_OK;
 }
 
-// K6 + K7T in one grid (D = 128)
-int launch_isa_t_fused(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
-                       const CUtensorMap& tvc, const isa::AttnParams& pe, const isa::AttnParams& pt, int items_e,
-                       int BH, cudaStream_t st) {
-  constexpr int kA = isa::TaylorTSmem<128>::kAlloc > isa::AttnSmem<128>::kAlloc ? isa::TaylorTSmem<128>::kAlloc
-                                                                                : isa::AttnSmem<128>::kAlloc;
-  static bool configured = false;
-  if (!configured) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::gba_isa_t_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kA));
-    configured = true;
-  }
-  const int items_t = (pt.n_qblk + 1) / 2;
-  isa::gba_isa_t_kernel<128><<<dim3(items_e + items_t, BH), isa::kTThreads, kA, st>>>(tq, tk, tv, tkc, tvc, pe, pt,
-                                                                                     items_e);
-  ISA_LAUNCHED("gba_isa_t_kernel");
-  return ISA_OK;
-}
-
 int launch_isa_fused(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& pe,
                      const isa::AttnParams& pt, int items_e, int items_t, int BH, cudaStream_t st) {

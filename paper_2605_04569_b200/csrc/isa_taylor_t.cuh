@@ -554,21 +554,6 @@ __global__ void __launch_bounds__(kTThreads, 1)
   taylor_t_body<D>(tm_q, tm_k, tm_v, tm_kc, tm_vc, p, blockIdx.x, blockIdx.y);
 }
 
-// K6 and K7T in one grid: CTAs [0, n_exact) run the sharp items (long), the
-// rest the transposed Taylor items (short), which fill the tail of the last
-// K6 wave instead of starting after it.
-template <int D>
-__global__ void __launch_bounds__(kTThreads, 1)
-    gba_isa_t_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
-                     const __grid_constant__ CUtensorMap tm_vc, const AttnParams pe, const AttnParams pt,
-                     const int n_exact) {
-  if ((int)blockIdx.x < n_exact)
-    gba_body<D, MODE_EXACT>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pe, blockIdx.x, blockIdx.y);
-  else
-    taylor_t_body<D>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pt, blockIdx.x - n_exact, blockIdx.y);
-}
-
 // Per head: row-major K7 (pair-of-blocks union tiles, one K/V load serves
 // both blocks of a pair, but every union tile costs a full 128x128 MMA pair)
 // or K7T (each block's own tiles, no MMA waste, no load sharing). Operand
