@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
 // or K7T (each block's own tiles, no MMA waste, no load sharing). Operand
 // traffic decides (both kernels are bound by it): K7 streams 2 * n_tiles
 // tiles per 4-block item, K7T ceil(k/2) per block. K7 is taken when its tile
-// count is below 0.8 x K7T's (measured break-even: K7T 3.3 ms vs K7 4.1 ms
+// count is below 0.9 x K7T's (tuned on cfg3: iid inputs keep K7T, clustered inputs pick K7 almost everywhere; K7T 3.3 ms vs K7 4.1 ms
 // at equal counts on cfg3). mode >= 0 forces the choice.
 __global__ void taylor_pick_kernel(const int* __restrict__ n_tiles, int n_items, int n_flat, int k, int mode,
                                    int* __restrict__ pick) {
@@ -574,7 +574,7 @@ __global__ void taylor_pick_kernel(const int* __restrict__ n_tiles, int n_items,
   if (threadIdx.x == 0) {
     const long long k7 = 2 * (part[0] + part[1] + part[2] + part[3]);
     const long long k7t = (long long)n_flat * ((k + 1) / 2);
-    pick[bh] = mode >= 0 ? mode : (5 * k7 < 4 * k7t ? 0 : 1);
+    pick[bh] = mode >= 0 ? mode : (10 * k7 < 9 * k7t ? 0 : 1);
   }
 }
 
