@@ -559,8 +559,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
 // or K7T (each block's own tiles, no MMA waste, no load sharing). Operand
 // traffic decides (both kernels are bound by it): K7 streams 2 * n_tiles
 // tiles per 4-block item, K7T ceil(k/2) per block. K7 is taken when its tile
-// count is below 0.9 x K7T's (tuned on cfg3: iid inputs keep K7T, clustered inputs pick K7 almost everywhere; K7T 3.3 ms vs K7 4.1 ms
-// at equal counts on cfg3). mode >= 0 forces the choice.
+// count is below 0.9 x K7T's (tuned on cfg3: iid inputs keep K7T, clustered
+// inputs match a forced K7). mode >= 0 forces the choice.
 __global__ void taylor_pick_kernel(const int* __restrict__ n_tiles, int n_items, int n_flat, int k, int mode,
                                    int* __restrict__ pick) {
   const int bh = blockIdx.x;
