@@ -835,7 +835,7 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
   }
   const bool taylor_t = d.n_flat && d.D == 128 && taylor_t_mode();
   const bool fuse = d.n_sharp && d.n_flat && !taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES);
-  if (taylor_t && d.n_sharp && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES)) {
+  if (taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES)) {
     // K6 + Taylor items in one grid (the short Taylor CTAs fill the tail of
     // the last K6 wave); per head the Taylor branch runs as K7T or, when the
     // paired exact lists overlap enough that the union tiles cost less, K7
