@@ -253,3 +253,38 @@ def test_prepared_call_replays_as_cuda_graph():
     graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(prep.out, eager)
+
+
+def test_taylor_pick_modes_agree(tmp_path):
+    """The per-head Taylor kernel choice: forcing K7 (union tiles) or K7T
+    (transposed) gives the same outputs within bf16 rounding, and the automatic
+    pick equals one of them per head (the choice is read once per process, so
+    each mode runs in its own interpreter)."""
+    import os
+    import subprocess
+    import sys
+
+    script = (
+        "import sys, numpy as np, torch\n"
+        "sys.path.insert(0, '.')\n"
+        "import paper_2605_04569_b200 as P\n"
+        "from paper_2605_04569_b200.workload import WorkloadSpec, generate\n"
+        "q, k, v, _ = generate(WorkloadSpec(kind='clustered', heads=3, seq_len=8192, dim=128, seed=5))\n"
+        "t = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k, v)]\n"
+        "out, _ = P.isa_forward(*t, P.IclLayout(4096, 4096), P.IsaConfig(), collect_trace=False)\n"
+        "np.save(sys.argv[1], out.float().cpu().numpy())\n"
+    )
+    outs = {}
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for mode in ("7", "7t", "auto"):
+        env = dict(os.environ)
+        env.pop("ISA_TAYLOR_PICK", None)
+        if mode != "auto":
+            env["ISA_TAYLOR_PICK"] = mode
+        path = str(tmp_path / f"{mode}.npy")
+        subprocess.run([sys.executable, "-c", script, path], cwd=root, env=env, check=True, timeout=600)
+        outs[mode] = np.load(path)
+    a, b, c = outs["7"], outs["7t"], outs["auto"]
+    assert float(np.abs(a - b).max()) <= 2e-2
+    for h in range(a.shape[1]):
+        assert np.array_equal(c[:, h], a[:, h]) or np.array_equal(c[:, h], b[:, h])
