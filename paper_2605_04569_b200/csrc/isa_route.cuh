@@ -479,8 +479,11 @@ __global__ void __launch_bounds__(128) block_mask_kernel(const double* __restric
 // taken in ascending index order (the stable tie rule). Element j of the row
 // is (lane j%32, register j/32), so membership word m is one ballot.
 // ----------------------------------------------------------------------------
+#ifndef ISA_MASK_MINB
+#define ISA_MASK_MINB 8  // 64 registers, 8 CTAs per SM: 143 -> 135 us at cfg3, same masks
+#endif
 template <int MAXM>
-__global__ void __launch_bounds__(128) block_mask_thr_kernel(const double* __restrict__ scores, int rows, int n,
+__global__ void __launch_bounds__(128, ISA_MASK_MINB) block_mask_thr_kernel(const double* __restrict__ scores, int rows, int n,
                                                              const int* __restrict__ flat, int n_flat, int T, int k,
                                                              int W, int* __restrict__ mask_idx,
                                                              int64_t* __restrict__ mask64,
