@@ -36,7 +36,25 @@ METRIC = "ISA attn-layer latency (ms) & TFLOPS at 2x32K tokens vs dense attn; GP
 WORKLOAD = dict(workload="cfg3: ISA attention layer, Wan-14B shape, 32K source + 32K context",
                 batch=1, heads=40, head_dim=128, l_src=32768, l_ctx=32768, block=64,
                 alpha_s=0.125, alpha_ns=0.0625, alpha_f=0.5,
-                inputs="iid N(0,1) bf16, seed 0; 2 GB of Q/K/V > 126 MB L2 (no flush needed)")
+                inputs="iid N(0,1) bf16 drawn per head h on the GPU (torch.Generator seed 1000 + h; Q, K, V "
+                       "in that order: bench.synth_qkv); 2 GB of Q/K/V > 126 MB L2 (no flush needed)")
+
+
+def synth_qkv(heads, S, D, dev):
+    """The bench's synthetic inputs for the listed heads: per head h an
+    independent torch.Generator(seed 1000 + h) on `dev` draws Q, K, V (S, D)
+    fp32 N(0, 1), rounded to bf16. Returns (1, len(heads), S, D) bf16 tensors.
+    Per-head seeding makes a rank's shard identical to slicing the full
+    tensor, and lets tests/test_gpu_shipped.py regenerate any head."""
+    import torch
+
+    q = torch.empty((1, len(heads), S, D), dtype=torch.bfloat16, device=dev)
+    k, v = torch.empty_like(q), torch.empty_like(q)
+    for j, h in enumerate(heads):
+        g = torch.Generator(device=dev).manual_seed(1000 + h)
+        for t in (q, k, v):
+            t[0, j].copy_(torch.randn((S, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16))
+    return q, k, v
 
 
 def parse():
@@ -177,16 +195,9 @@ def run_ours(args, rank, world, local_rank):
     cfg = P.IsaConfig(strict=(args.l_src % 64 == 0 and args.l_ctx % 64 == 0))  # ragged segments (cfg5) allowed
     my_heads = head_shard(H, rank, world)
     Hl = len(my_heads)
-    g = torch.Generator(device=dev).manual_seed(0)
-    # Each rank synthesises only its own heads (round-robin). Identical to
-    # slicing a full seeded (1,H,S,D) tensor because heads are drawn per head.
-    q = torch.empty((1, Hl, S, D), dtype=torch.bfloat16, device=dev)
-    k, v = torch.empty_like(q), torch.empty_like(q)
-    for j, h in enumerate(my_heads):
-        gh = torch.Generator(device=dev).manual_seed(1000 + h)
-        for t in (q, k, v):
-            t[0, j].copy_(torch.randn((S, D), generator=gh, device=dev, dtype=torch.float32).to(torch.bfloat16))
-    del g
+    # Each rank synthesises only its own heads (round-robin): identical to
+    # slicing the full (1,H,S,D) inputs because heads are drawn per head.
+    q, k, v = synth_qkv(my_heads, S, D, dev)
     dims = P.IsaDims.derive((1, H, S, D), icl, cfg)
     flops = dims.flops()
     f_isa = flops.total()

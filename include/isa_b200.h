@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define ISA_ABI_VERSION 2
+#define ISA_ABI_VERSION 3
 
 typedef enum IsaStatus {
   ISA_OK = 0,
@@ -78,8 +78,14 @@ typedef struct IsaKnobs {
 } IsaKnobs;
 
 /* IsaKnobs.flags: launch the exact (sharp) and Taylor (flat) attention
- * branches as two kernels instead of one fused grid (per-branch profiling). */
+ * branches as two kernels instead of one fused grid (per-branch profiling;
+ * the Taylor branch then runs as K7T at D = 128). */
 #define ISA_FLAG_SEPARATE_BRANCHES 1
+/* Force the D = 128 Taylor-branch kernel for every head instead of the
+ * per-head automatic choice (taylor_pick_kernel): K7 = row-major pair-union
+ * tiles, K7T = transposed per-block tiles. Same operator, test/A-B hooks. */
+#define ISA_FLAG_TAYLOR_K7 2
+#define ISA_FLAG_TAYLOR_K7T 4
 
 /* Optional routing export (device pointers; any may be NULL). */
 typedef struct IsaRoutingOut {
@@ -88,8 +94,22 @@ typedef struct IsaRoutingOut {
   int64_t* flat;       /* (B,H,n_flat)     SharpnessSplit.flat    coarse.py:96 */
   int64_t* mask;       /* (B,H,n_flat,k)   BlockMask.indices      coarse.py:76 */
   double* sharpness;   /* (B,H,T)          SharpnessSplit.sharpness coarse.py:97 */
-  double* ctx_scores;  /* (B,H,T_ctx)      context saliency (diagnostic) */
+  double* ctx_scores;  /* (B,H,T_ctx)      context saliency s_coarse[:, :, :T_src, T_src:].mean(2)
+                          (coarse.py:155), bit-identical to numpy */
+  int32_t* taylor_kernel; /* (B,H) Taylor-branch kernel run per head (D = 128): 0 = row-major K7
+                             (pair-union tiles), 1 = transposed K7T; written by isa_forward only */
 } IsaRoutingOut;
+
+/* err_word bits (device int32, OR-ed by the kernels; the caller zeroes it
+ * and reads it after the stream completes). Pinned-routing checks follow the
+ * reference's index contracts (tensor.py:120-133, taylor.py:80-84). */
+#define ISA_ERRBIT_INPUT 1u          /* non-finite Q/K/V          -> InputError */
+#define ISA_ERRBIT_DEGENERATE 2u     /* row with an empty key set -> DegenerateRowError */
+#define ISA_ERRBIT_SEL_RANGE 4u      /* pinned selection out of [0, T_ctx)       -> BlockIndexError */
+#define ISA_ERRBIT_SEL_ORDER 8u      /* pinned selection not strictly ascending  -> ContractError */
+#define ISA_ERRBIT_SPLIT_RANGE 16u   /* pinned sharp/flat out of [0, T)          -> BlockIndexError */
+#define ISA_ERRBIT_SPLIT_ORDER 32u   /* sharp/flat not ascending or not a partition of [0, T) -> ContractError */
+#define ISA_ERRBIT_MASK 64u          /* pinned mask out of [0, t_new) or not ascending -> ContractError */
 
 /* Pinned routing for isa_forward_with_routing (device int64, all required
  * except mask when n_flat == 0). */
@@ -121,9 +141,8 @@ int isa_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* by
 
 /* Full pipeline (stages 1-5). `pinned` == NULL computes routing on device,
  * otherwise uses it (isa_forward_with_routing). `routing` may be NULL.
- * `err_word` (device int32, may be NULL) receives bit 0 = non-finite input
- * (InputError), bit 1 = degenerate row (DegenerateRowError); the caller
- * zeroes it beforehand and reads it after the stream completes.
+ * `err_word` (device int32, may be NULL) receives ISA_ERRBIT_* bits; the
+ * caller zeroes it beforehand and reads it after the stream completes.
  * `stream` is a cudaStream_t. */
 int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
                 void* out, void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned,
@@ -209,6 +228,20 @@ int isa_pool_means(const IsaShape* shape, const void* q, const void* k, const vo
  * (context pre-selection kernel), 1 = warp arg-max rounds (block-mask kernel). */
 int isa_topk_rows_f64(const double* scores, int32_t rows, int32_t n, int32_t k, int64_t* out_idx,
                       int32_t method, void* stream);
+
+/* Coarse scores s[bh][i][j] = scale * <qc[bh][i], kc[bh][j]> in float64,
+ * bit-identical to the reference's np.einsum("bhid,bhjd->bhij") over fp64
+ * copies of fp32 means (coarse.py:126, pipeline.py:180-182; head dims that
+ * are multiples of 8). qc (bh, t_q, d), kc (bh, t_k, d) fp32 contiguous;
+ * s (bh, t_q, t_k) fp64 contiguous. */
+int isa_coarse_scores(int32_t bh, int32_t t_q, int32_t t_k, int32_t d, double scale, const float* qc,
+                      const float* kc, double* s, void* stream);
+
+/* Context saliency (coarse.py:155): out[bh][c] = mean over i < n_src of
+ * s[bh][i][n_src + c] for c < n_ctx, summed in numpy's order. Element
+ * (bh, i, j) of s sits at s + bh * head_stride + i * row_stride + j. */
+int isa_ctx_saliency_f64(const double* s, int32_t bh, int64_t head_stride, int64_t row_stride, int32_t n_src,
+                         int32_t n_ctx, double* out, void* stream);
 
 /* Sharpness per row (coarse.py:193-195): population variance of the row
  * softmax (softmax_first) or of the raw row. */

@@ -16,7 +16,7 @@ from .errors import ISA_OK, STATUS_TO_ERROR, NativeError
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libisa_b200.so")
 
-ISA_ABI_VERSION = 2
+ISA_ABI_VERSION = 3
 ISA_DTYPE_BF16 = 0
 ISA_DTYPE_F32 = 1
 
@@ -40,7 +40,23 @@ EXPORTED_SYMBOLS = (
     "isa_taylor_workspace_bytes",
     "isa_taylor_forward",
     "isa_cross_attention",
+    "isa_coarse_scores",
+    "isa_ctx_saliency_f64",
 )
+
+# IsaKnobs.flags
+FLAG_SEPARATE_BRANCHES = 1
+FLAG_TAYLOR_K7 = 2
+FLAG_TAYLOR_K7T = 4
+
+# err_word bits (include/isa_b200.h ISA_ERRBIT_*)
+ERRBIT_INPUT = 1
+ERRBIT_DEGENERATE = 2
+ERRBIT_SEL_RANGE = 4
+ERRBIT_SEL_ORDER = 8
+ERRBIT_SPLIT_RANGE = 16
+ERRBIT_SPLIT_ORDER = 32
+ERRBIT_MASK = 64
 
 
 class IsaShape(ctypes.Structure):
@@ -84,6 +100,7 @@ class IsaRoutingOut(ctypes.Structure):
         ("mask", ctypes.c_void_p),
         ("sharpness", ctypes.c_void_p),
         ("ctx_scores", ctypes.c_void_p),
+        ("taylor_kernel", ctypes.c_void_p),
     ]
 
 
@@ -121,6 +138,8 @@ _SIGS = {
     "isa_topk_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _I, _P]),
     "isa_sharpness_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P]),
     "isa_split_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P, _P]),
+    "isa_coarse_scores": (ctypes.c_int, [_I, _I, _I, _I, ctypes.c_double, _P, _P, _P, _P]),
+    "isa_ctx_saliency_f64": (ctypes.c_int, [_P, _I, ctypes.c_int64, ctypes.c_int64, _I, _I, _P, _P]),
     "isa_backward_workspace_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs),
                                                     ctypes.POINTER(ctypes.c_size_t)]),
     "isa_backward": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _P, _P, _P, _P, _P, _P, _P,

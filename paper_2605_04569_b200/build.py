@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libisa_b200.so")
 SOURCES = ["isa_capi.cu"]
-DEPS = ["isa_capi.cu", "isa_attn.cuh", "isa_attn_p2.cuh", "isa_route.cuh", "isa_ptx.cuh", "isa_bwd.cuh", "isa_bwd_tc.cuh", "isa_taylor_t.cuh"]
+DEPS = ["isa_capi.cu", "isa_attn.cuh", "isa_route.cuh", "isa_ptx.cuh", "isa_bwd.cuh", "isa_bwd_tc.cuh", "isa_taylor_t.cuh"]
 
 
 def nvcc_path() -> str:

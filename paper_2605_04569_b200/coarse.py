@@ -1,8 +1,10 @@
 """Function-level drop-ins for the reference's routing API (pkg/src/isattn/coarse.py:22-201):
 `build_coarse`, `rank_context`, `build_block_mask`, `sharpness_split` and `CoarseSet`, on the
 same sm_100a primitives the fused pipeline uses (C ABI `isa_pool_means`, `isa_topk_rows_f64`,
-`isa_sharpness_rows_f64`, `isa_split_rows_f64`). Index outputs are device int64 tensors in the
-value types of `types.py`; the discrete decisions match the reference bit for bit.
+`isa_sharpness_rows_f64`, `isa_split_rows_f64`, `isa_coarse_scores`, `isa_ctx_saliency_f64`).
+numpy callers get numpy arrays back (like the reference); torch callers get device tensors.
+Block means, the fp64 coarse scores and the context saliency are bit-identical to the
+reference's numpy arithmetic; every discrete decision matches it bit for bit.
 """
 
 from __future__ import annotations
@@ -16,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .errors import ConfigError, LayoutError
+from .errors import ConfigError, InputError, LayoutError
 from .types import BlockLayout, BlockMask, IclLayout, SelectionIndex, SharpnessSplit, icl_from_any
 
 
@@ -24,10 +26,10 @@ from .types import BlockLayout, BlockMask, IclLayout, SelectionIndex, SharpnessS
 class CoarseSet:
     """Pooled Q/K/V (one row per block) and the scaled fp64 block score matrix (coarse.py:22-49)."""
 
-    qc: torch.Tensor  # (B, H, N_Q, D) fp32, device
-    kc: torch.Tensor  # (B, H, N_K, D)
-    vc: torch.Tensor
-    s_coarse: torch.Tensor  # (B, H, N_Q, N_K) float64, device
+    qc: object  # (B, H, N_Q, D) fp32: device tensor, or numpy for numpy callers
+    kc: object  # (B, H, N_K, D)
+    vc: object
+    s_coarse: object  # (B, H, N_Q, N_K) float64
     block_size: int
     scale_applied: bool = True
 
@@ -43,6 +45,19 @@ class CoarseSet:
         s = self.s_coarse
         return {"query_blocks": self.num_query_blocks, "key_blocks": self.num_key_blocks,
                 "score_min": float(s.min()), "score_max": float(s.max()), "score_mean": float(s.mean())}
+
+
+def _dev(x) -> torch.Tensor:
+    """A CoarseSet field on the device (numpy fields are uploaded)."""
+    if isinstance(x, np.ndarray):
+        if not torch.cuda.is_available():
+            raise LayoutError("the routing kernels run on a CUDA device and none is available (there is no CPU path)")
+        return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return x
+
+
+def _like(t: torch.Tensor, numpy_io: bool):
+    return t.cpu().numpy() if numpy_io else t
 
 
 def _device_tensor(x, name):
@@ -75,6 +90,8 @@ def _block_means(x: torch.Tensor, layout: BlockLayout) -> torch.Tensor:
     sh = N.IsaShape(B, H, S, D, S, 0, 64, dt, x.stride(0), x.stride(1), x.stride(2))
     N.check(N.load().isa_pool_means(ctypes.byref(sh), x.data_ptr(), x.data_ptr(), x.data_ptr(), means.data_ptr(),
                                     err.data_ptr(), torch.cuda.current_stream(x.device).cuda_stream))
+    if int(err.item()) & N.ERRBIT_INPUT:  # ensure_tensor4's finiteness check (tensor.py:34-35)
+        raise InputError("block_mean input: non-finite elements")
     return means[0]
 
 
@@ -99,26 +116,36 @@ def build_coarse(q, k, v, q_layout: BlockLayout, k_layout: BlockLayout, scale: O
     s_coarse = scale * qc . kc^T in float64 (coarse.py:110-127)."""
     if q_layout.block_size != k_layout.block_size:
         raise LayoutError("query and key layouts must share one block size")
+    numpy_io = isinstance(q, np.ndarray)
     q, k, v = _device_tensor(q, "Q"), _device_tensor(k, "K"), _device_tensor(v, "V")
     if scale is None:
         scale = 1.0 / math.sqrt(q.shape[3])
     qc, kc, vc = _block_means(q, q_layout), _block_means(k, k_layout), _block_means(v, k_layout)
-    s = scale * torch.matmul(qc.double(), kc.double().transpose(-1, -2))
-    return CoarseSet(qc=qc, kc=kc, vc=vc, s_coarse=s, block_size=q_layout.block_size)
+    B, H, t_q, D = qc.shape
+    t_k = kc.shape[2]
+    if kc.shape[:2] != (B, H):
+        raise LayoutError(f"Q/K batch-head mismatch: {tuple(qc.shape)} vs {tuple(kc.shape)}")
+    s = torch.empty((B, H, t_q, t_k), dtype=torch.float64, device=q.device)
+    N.check(N.load().isa_coarse_scores(B * H, t_q, t_k, D, float(scale), qc.data_ptr(), kc.data_ptr(), s.data_ptr(),
+                                       torch.cuda.current_stream(q.device).cuda_stream))
+    return CoarseSet(qc=_like(qc, numpy_io), kc=_like(kc, numpy_io), vc=_like(vc, numpy_io),
+                     s_coarse=_like(s, numpy_io), block_size=q_layout.block_size)
 
 
-def _topk_rows(scores: torch.Tensor, k: int, method: int) -> torch.Tensor:
+def _topk_rows(scores, k: int, method: int):
     """Top-k per row, ties to the lower index, ascending (coarse.py:130-136)."""
-    lead = scores.shape[:-1]
+    numpy_io = isinstance(scores, np.ndarray)
+    scores = _dev(scores)
+    lead = tuple(scores.shape[:-1])
     n = int(scores.shape[-1])
     rows = int(np.prod(lead)) if lead else 1
     out = torch.empty(lead + (k,), dtype=torch.int64, device=scores.device)
     if k == 0 or rows == 0:
-        return out
+        return _like(out, numpy_io)
     s = scores.reshape(rows, n).contiguous().double()
     N.check(N.load().isa_topk_rows_f64(s.data_ptr(), rows, n, k, out.data_ptr(), method,
                                        torch.cuda.current_stream(s.device).cuda_stream))
-    return out
+    return _like(out, numpy_io)
 
 
 def rank_context(cs: CoarseSet, icl: IclLayout, alpha_s: float) -> SelectionIndex:
@@ -133,11 +160,19 @@ def rank_context(cs: CoarseSet, icl: IclLayout, alpha_s: float) -> SelectionInde
     if n_src + n_ctx != cs.num_key_blocks or n_src > cs.num_query_blocks:
         raise LayoutError(f"icl layout ({icl.l_src}, {icl.l_ctx}) inconsistent with coarse blocks "
                           f"({cs.num_query_blocks} x {cs.num_key_blocks}, b={b})")
+    numpy_io = isinstance(cs.s_coarse, np.ndarray)
     B, H = cs.s_coarse.shape[:2]
     if n_ctx == 0:
-        return SelectionIndex(torch.zeros((B, H, 0), dtype=torch.int64, device=cs.s_coarse.device), 0)
-    ctx_scores = cs.s_coarse[:, :, :n_src, n_src:].mean(dim=2)
-    return SelectionIndex(_topk_rows(ctx_scores, int(math.floor(alpha_s * n_ctx)), 0), n_ctx)
+        return SelectionIndex(np.zeros((B, H, 0), dtype=np.int64) if numpy_io else
+                              torch.zeros((B, H, 0), dtype=torch.int64, device=cs.s_coarse.device), 0)
+    s = _dev(cs.s_coarse).double().contiguous()
+    t_q, t_k = s.shape[2], s.shape[3]
+    ctx_scores = torch.empty((B, H, n_ctx), dtype=torch.float64, device=s.device)
+    # the mean over source query blocks in numpy's summation order (ctx_mean_kernel)
+    N.check(N.load().isa_ctx_saliency_f64(s.data_ptr(), B * H, t_q * t_k, t_k, n_src, n_ctx, ctx_scores.data_ptr(),
+                                          torch.cuda.current_stream(s.device).cuda_stream))
+    idx = _topk_rows(ctx_scores, int(math.floor(alpha_s * n_ctx)), 0)
+    return SelectionIndex(_like(idx, numpy_io), n_ctx)
 
 
 def build_block_mask(cs: CoarseSet, alpha_ns: float) -> BlockMask:
@@ -160,15 +195,17 @@ def sharpness_split(cs: CoarseSet, icl: IclLayout, alpha_f: float, softmax_first
     n_src = -(-icl.l_src // b)
     if n_src < 1 or n_src > cs.num_key_blocks:
         raise LayoutError(f"source block count {n_src} out of range for coarse set")
-    B, H, T_q, _ = cs.s_coarse.shape
-    dev = cs.s_coarse.device
+    numpy_io = isinstance(cs.s_coarse, np.ndarray)
+    s_coarse = _dev(cs.s_coarse).double()
+    B, H, T_q, _ = s_coarse.shape
+    dev = s_coarse.device
     st = torch.cuda.current_stream(dev).cuda_stream
     lib = N.load()
-    src = cs.s_coarse[:, :, :, :n_src].reshape(B * H * T_q, n_src).contiguous()
+    src = s_coarse[:, :, :, :n_src].reshape(B * H * T_q, n_src).contiguous()
     m = torch.empty((B, H, T_q), dtype=torch.float64, device=dev)
     N.check(lib.isa_sharpness_rows_f64(src.data_ptr(), B * H * T_q, n_src, int(bool(softmax_first)), m.data_ptr(), st))
     n_flat = int(math.floor(alpha_f * T_q))
     sharp = torch.empty((B, H, T_q - n_flat), dtype=torch.int64, device=dev)
     flat = torch.empty((B, H, n_flat), dtype=torch.int64, device=dev)
     N.check(lib.isa_split_rows_f64(m.data_ptr(), B * H, T_q, n_flat, sharp.data_ptr(), flat.data_ptr(), st))
-    return SharpnessSplit(sharp=sharp, flat=flat, sharpness=m)
+    return SharpnessSplit(sharp=_like(sharp, numpy_io), flat=_like(flat, numpy_io), sharpness=_like(m, numpy_io))

@@ -6,16 +6,10 @@
 //
 // Softmax statistics come from the forward kernels (AttnParams::lse, log2
 // domain: P = exp2(scale*log2e * q.k + log2(w) - lse)); rho = rowsum(dO * O).
-// Three kernels, all mma.sync m16n8k16 bf16 -> fp32 (round-1 baseline; the
-// tcgen05 rewrite is the next step):
+// This file holds the mma.sync m16n8k16 bf16 -> fp32 centroid pass; the
+// exact-pair dK/dV and the dQ kernels are tcgen05 (isa_bwd_tc.cuh):
 //   bwd_dkv_kernel<CENTROID=1>: per tile of 64 K_new centroids, over all flat
 //       query blocks: dkc, dvc (taylor.py:286-289), fp32 [BH][t_new][D]
-//   bwd_dkv_kernel<CENTROID=0>: per K_new block j, over the sharp blocks and
-//       the flat blocks listing j: dK_j, dV_j (+ the centroid part spread over
-//       the block's valid rows, taylor.py:290-292), stored at the block's
-//       original token rows (unselected context rows stay 0)
-//   bwd_dq_kernel: per query block, over its key tiles (all K_new blocks for a
-//       sharp block; its exact blocks then every centroid tile for a flat one)
 #pragma once
 #include "isa_ptx.cuh"
 
@@ -153,147 +147,6 @@ __global__ void bwd_rho_kernel(const __nv_bfloat16* __restrict__ dout, long long
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) rho[w] = acc;
-}
-
-// ---------------------------------------------------------------- dQ (query-major)
-// CTA = one query block (64 rows), 4 warps x 16 rows. smem: Q, dO, and a
-// double-buffered K/V tile pair (cp.async prefetch of tile i+1 under tile i),
-// plus per-buffer column biases (0 / log2(centroid weight) / -inf = excluded).
-template <int D>
-__global__ void __launch_bounds__(128, 2) bwd_dq_kernel(const BwdParams p) {
-  extern __shared__ __align__(128) uint8_t smem_bw[];
-  constexpr int TB = 64 * D * 2;
-  uint8_t* sQ = smem_bw;
-  uint8_t* sO = smem_bw + TB;  // dO
-  uint8_t* sKV = smem_bw + 2 * TB;  // [2 buffers][K, V]
-  float* sBias = reinterpret_cast<float*>(smem_bw + 6 * TB);  // [2][64]
-  const int bh = blockIdx.y, x = blockIdx.x;
-  const int hh = bh % p.H, bb = bh / p.H;
-  const bool is_flat = x >= p.n_sharp;
-  const int f = x - p.n_sharp;
-  const int u = is_flat ? p.flat[bh * p.n_flat + f] : p.sharp[bh * p.n_sharp + x];
-  const int tok = bw_tok0(p, u), vq = bw_valid(p, u);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
-  const int n_exact = is_flat ? p.k : p.t_new;
-  const int n_tiles = n_exact + (is_flat ? p.tn_pad / 64 : 0);
-  const uint32_t* mb = is_flat ? p.bits + ((long long)bh * p.n_flat + f) * p.W : nullptr;
-  // issue the loads of tile `it` into buffer `buf`
-  auto prefetch = [&](int it, int buf) {
-    uint8_t* sK = sKV + buf * 2 * TB;
-    uint8_t* sV = sK + TB;
-    if (it < n_exact) {
-      const int j = is_flat ? p.mask[((long long)bh * p.n_flat + f) * p.k + it] : it;
-      const int uk = p.kv_blk[(long long)bh * p.t_new + j];
-      const int vk = bw_valid(p, uk);
-      const long long off = bb * p.sb + hh * p.sh + (long long)bw_tok0(p, uk) * p.ss;
-      load_tile_async<D>(sK, p.kx + off, p.ss, vk);
-      load_tile_async<D>(sV, p.v + off, p.ss, vk);
-      if (threadIdx.x < 64) sBias[buf * 64 + threadIdx.x] = threadIdx.x < vk ? 0.f : -INFINITY;
-    } else {
-      const int j0 = (it - n_exact) * 64;
-      const long long off = ((long long)bh * p.tn_pad + j0) * D;
-      load_tile_async<D>(sK, p.kc + off, D, 64);
-      load_tile_async<D>(sV, p.vc + off, D, 64);
-      if (threadIdx.x < 64) {  // taylor.py:153-156: members excluded, weight = valid rows
-        const int jj = j0 + threadIdx.x;
-        float bias = -INFINITY;
-        if (jj < p.t_new && !((mb[jj >> 5] >> (jj & 31)) & 1u))
-          bias = __log2f((float)bw_valid(p, p.kv_blk[(long long)bh * p.t_new + jj]));
-        sBias[buf * 64 + threadIdx.x] = bias;
-      }
-    }
-    cp_commit();
-  };
-  load_tile_async<D>(sQ, p.q + bb * p.sb + hh * p.sh + tok * p.ss, p.ss, vq);
-  load_tile_async<D>(sO, p.dout + bb * p.db + hh * p.dh + tok * p.ds, p.ds, vq);
-  cp_commit();
-  if (n_tiles > 0) prefetch(0, 0);
-  const int r0 = warp * 16 + g, r1 = r0 + 8;
-  const long long rowbase = (long long)bh * p.S + tok;
-  const float lse0 = r0 < vq ? p.lse[rowbase + r0] : 0.f, lse1 = r1 < vq ? p.lse[rowbase + r1] : 0.f;
-  const float rho0 = r0 < vq ? p.rho[rowbase + r0] : 0.f, rho1 = r1 < vq ? p.rho[rowbase + r1] : 0.f;
-  const bool ok0 = r0 < vq && lse0 > -INFINITY, ok1 = r1 < vq && lse1 > -INFINITY;
-  float acc[D / 8][4];
-#pragma unroll
-  for (int n = 0; n < D / 8; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
-  const uint32_t bq = smem_u32(sQ), bo = smem_u32(sO);
-  for (int it = 0; it < n_tiles; ++it) {
-    const int buf = it & 1;
-    if (it + 1 < n_tiles) {
-      prefetch(it + 1, buf ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-    const uint32_t bk = smem_u32(sKV + buf * 2 * TB), bv = bk + TB;
-    const float* bias = sBias + buf * 64;
-    // S = Q K^T and dP = dO V^T for this warp's 16 rows x 64 keys
-    float sc[8][4], dp[8][4];
-#pragma unroll
-    for (int n = 0; n < 8; ++n)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sc[n][e] = dp[n][e] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      uint32_t aq[4], ao[4];
-      frag_a<D>(aq, bq, warp * 16, kk * 16);
-      frag_a<D>(ao, bo, warp * 16, kk * 16);
-#pragma unroll
-      for (int n = 0; n < 8; n += 2) {
-        uint32_t b[4];
-        frag_b<D>(b, bk, n * 8, kk * 16);
-        mma16816(sc[n], aq, b[0], b[1]);
-        mma16816(sc[n + 1], aq, b[2], b[3]);
-        frag_b<D>(b, bv, n * 8, kk * 16);
-        mma16816(dp[n], ao, b[0], b[1]);
-        mma16816(dp[n + 1], ao, b[2], b[3]);
-      }
-    }
-    // P and dS = P * (dP - rho); pack dS as the A operand of dQ += dS K
-    uint32_t ads[4][4];
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      float dsv[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int col = n * 8 + tig * 2 + (e & 1);
-        const bool hi = e >= 2;
-        const float pr = (hi ? ok1 : ok0) ? exp2f(fmaf(sc[n][e], p.sl2, bias[col] - (hi ? lse1 : lse0))) : 0.f;
-        dsv[e] = pr * (dp[n][e] - (hi ? rho1 : rho0));
-      }
-      const int kk = n >> 1;
-      const int o = (n & 1) ? 2 : 0;
-      ads[kk][o] = pack_bf16x2(dsv[0], dsv[1]);
-      ads[kk][o + 1] = pack_bf16x2(dsv[2], dsv[3]);
-    }
-    // dQ += dS K  (K as [k=key][n=d])
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-#pragma unroll
-      for (int n = 0; n < D / 8; n += 2) {
-        uint32_t b[4];
-        frag_bt<D>(b, bk, kk * 16, n * 8);
-        mma16816(acc[n], ads[kk], b[0], b[1]);
-        mma16816(acc[n + 1], ads[kk], b[2], b[3]);
-      }
-    __syncthreads();  // buffer `buf` is refilled by the prefetch of tile it + 2
-  }
-  // dQ = scale * acc at the block's original rows
-#pragma unroll
-  for (int n = 0; n < D / 8; ++n) {
-    const int col = n * 8 + tig * 2;
-    if (r0 < vq) {
-      float* dst = p.dq + (rowbase + r0) * D + col;
-      dst[0] = p.scale * acc[n][0];
-      dst[1] = p.scale * acc[n][1];
-    }
-    if (r1 < vq) {
-      float* dst = p.dq + (rowbase + r1) * D + col;
-      dst[0] = p.scale * acc[n][2];
-      dst[1] = p.scale * acc[n][3];
-    }
-  }
 }
 
 // ---------------------------------------------------------------- dK/dV (key-major)

@@ -2,8 +2,8 @@
 //
 // isa_forward runs the five reference stages (pipeline.py:133-370) as one
 // stream-ordered sequence of kernels with no host synchronisation:
-//   stage 1 "coarse"  K1 pool_means, K2a coarse_src (fp64 S over source
-//                     columns), K2b ctx_score                pipeline.py:176-184
+//   stage 1 "coarse"  K1 pool_means, K2 coarse_np (fp64 S of the source rows
+//                     vs the context columns), K2b ctx_mean  pipeline.py:176-184
 //   stage 2 "select"  K3 topk_rank (context), K_new block table, bf16 K_new
 //                     centroids + log2 weights              pipeline.py:186-212
 //   stage 3 "split"   K4a sharpness, K4b split, K5 block mask, Taylor plan
@@ -19,12 +19,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 
 #include "../../include/isa_b200.h"
 #include "isa_attn.cuh"
-#include "isa_attn_p2.cuh"
 #include "isa_bwd.cuh"
 #include "isa_bwd_tc.cuh"
 #include "isa_route.cuh"
@@ -57,6 +57,24 @@ int fail(int code, const char* fmt, ...) {
     cudaError_t e_ = cudaGetLastError();                                                               \
     if (e_ != cudaSuccess) return fail(ISA_ERR_CUDA, "launch %s: %s", name, cudaGetErrorString(e_)); \
   } while (0)
+
+// Dynamic shared memory opt-in. cudaFuncSetAttribute applies to the current
+// device's context only, so the granted size is remembered per (kernel,
+// device) and grown on demand (a process may drive several GPUs).
+int ensure_smem(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return ISA_OK;
+  int dev = 0;
+  ISA_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> granted;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = granted[{fn, dev}];
+  if (bytes > cur) {
+    ISA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
+  }
+  return ISA_OK;
+}
 
 // ---------------------------------------------------------------- TMA maps
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -93,20 +111,6 @@ int make_map(CUtensorMap* m, const void* ptr, int D, long long d1, long long d2,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ISA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return ISA_OK;
-}
-
-// Exact/dense attention pipeline: 1 = single-buffered 128-key tiles
-// (isa_attn.cuh, default), 2 = double-buffered 64-key tiles (isa_attn_p2.cuh).
-// Measured on B200 (same box, cfg3): pipe 1 K6 1159 TFLOP/s, pipe 2 934 —
-// the N=64 QK re-reads Q from shared memory twice as often and the extra
-// operand traffic costs more than the hidden MMA round trip saves. Kept
-// selectable (ISA_PIPE=2) for A/B measurements.
-int pipe_mode() {
-  static int mode = [] {
-    const char* e = getenv("ISA_PIPE");
-    return (e && e[0] == '2') ? 2 : 1;
-  }();
-  return mode;
 }
 
 // ---------------------------------------------------------------- geometry
@@ -172,7 +176,7 @@ struct Workspace {
   float* means;  // [3][BH][T][D]
   __nv_bfloat16* bf;  // [3][BH][S][D] (fp32 inputs only)
   double* s_new;      // [BH][T][t_new]  fp64 coarse scores vs K_new blocks
-  double* qsum;       // [BH][D]
+  double* s_ctx;      // [BH][t_src][t_ctx] fp64 source-row x context-column scores
   uint8_t* flags;     // [BH][max(T, t_ctx)]
   double* ctx;        // [BH][t_ctx]
   int* sel;           // [BH][k_ctx]
@@ -207,7 +211,7 @@ Workspace carve(const Dims& d, int dtype, uint8_t* base) {
   w.means = reinterpret_cast<float*>(take(3ull * BH * d.T * d.D * 4));
   w.bf = dtype == ISA_DTYPE_F32 ? reinterpret_cast<__nv_bfloat16*>(take(3ull * BH * d.S * d.D * 2)) : nullptr;
   w.s_new = reinterpret_cast<double*>(take(8ull * BH * d.T * d.t_new));
-  w.qsum = reinterpret_cast<double*>(take(8ull * BH * d.D));
+  w.s_ctx = reinterpret_cast<double*>(take(8ull * BH * d.t_src * d.t_ctx));
   w.flags = reinterpret_cast<uint8_t*>(take((size_t)BH * (d.T > d.t_ctx ? d.T : d.t_ctx)));
   w.ctx = reinterpret_cast<double*>(take(8ull * BH * d.t_ctx));
   w.sel = reinterpret_cast<int*>(take(4ull * BH * d.k_ctx));
@@ -236,12 +240,7 @@ unsigned grid1d(long long n, int threads) {
 template <int D>
 int launch_resid_tiled(dim3 g, const float* qc, const float* kc, const float* vc, const Dims& d, float* out,
                        cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::coarse_residual_tiled_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)isa::ResidTile<D>::kBytes));
-    configured = true;
-  }
+  if (int rc_ = ensure_smem((const void*)isa::coarse_residual_tiled_kernel<D>, isa::ResidTile<D>::kBytes)) return rc_;
   isa::coarse_residual_tiled_kernel<D><<<g, 256, isa::ResidTile<D>::kBytes, st>>>(qc, kc, vc, d.T, (float)d.scale,
                                                                                  d.resid_softmax, out);
   return ISA_OK;
@@ -251,49 +250,11 @@ template <int D, int MODE>
 int launch_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
                      const CUtensorMap& tvc, const isa::AttnParams& p, int items, int BH, cudaStream_t st) {
   using L = isa::AttnSmem<D>;
-  static bool configured = false;
-  if (!configured) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::gba_attention_kernel<D, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  L::kAlloc));
-    configured = true;
-  }
+  if (int rc_ = ensure_smem((const void*)isa::gba_attention_kernel<D, MODE>, L::kAlloc)) return rc_;
   if (items < 1) return ISA_OK;
   dim3 grid(items, BH);
   isa::gba_attention_kernel<D, MODE><<<grid, isa::kThreads, L::kAlloc, st>>>(tq, tk, tv, tkc, tvc, p);
   ISA_LAUNCHED("gba_attention_kernel");
-  return ISA_OK;
-}
-
-template <int D, int MODE>
-int launch_attention_p2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                        const isa::AttnParams& p, int items, int BH, cudaStream_t st) {
-  using L = isa::P2Smem<D>;
-  static bool configured = false;
-  if (!configured) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::gba_attention_p2_kernel<D, MODE>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
-    configured = true;
-  }
-  if (items < 1) return ISA_OK;
-  isa::gba_attention_p2_kernel<D, MODE><<<dim3(items, BH), isa::kThreads, L::kAlloc, st>>>(tq, tk, tv, p);
-  ISA_LAUNCHED("gba_attention_p2_kernel");
-  return ISA_OK;
-}
-
-template <int D>
-int launch_isa_fused_p2_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                          const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& pe,
-                          const isa::AttnParams& pt, int items_e, int items_t, int BH, cudaStream_t st) {
-  constexpr int kA = isa::P2Smem<D>::kAlloc > isa::AttnSmem<D>::kAlloc ? isa::P2Smem<D>::kAlloc
-                                                                        : isa::AttnSmem<D>::kAlloc;
-  static bool configured = false;
-  if (!configured) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::gba_isa_p2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kA));
-    configured = true;
-  }
-  isa::gba_isa_p2_kernel<D><<<dim3(items_e + items_t, BH), isa::kThreads, kA, st>>>(tq, tk, tv, tkc, tvc, pe, pt,
-                                                                                    items_e);
-  ISA_LAUNCHED("gba_isa_p2_kernel");
   return ISA_OK;
 }
 
@@ -302,11 +263,7 @@ int launch_isa_fused_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUten
                        const CUtensorMap& tvc, const isa::AttnParams& pe, const isa::AttnParams& pt, int items_e,
                        int items_t, int BH, cudaStream_t st) {
   using L = isa::AttnSmem<D>;
-  static bool configured = false;
-  if (!configured) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::gba_isa_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc));
-    configured = true;
-  }
+  if (int rc_ = ensure_smem((const void*)isa::gba_isa_kernel<D>, L::kAlloc)) return rc_;
   dim3 grid(items_e + items_t, BH);
   isa::gba_isa_kernel<D><<<grid, isa::kThreads, L::kAlloc, st>>>(tq, tk, tv, tkc, tvc, pe, pt, items_e);
   ISA_LAUNCHED("gba_isa_kernel");
@@ -341,11 +298,7 @@ int launch_isa_hybrid(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
                       int items_k7, const int* pick, int BH, cudaStream_t st) {
   constexpr int kA = isa::TaylorTSmem<128>::kAlloc > isa::AttnSmem<128>::kAlloc ? isa::TaylorTSmem<128>::kAlloc
                                                                                 : isa::AttnSmem<128>::kAlloc;
-  static bool configured = false;
-  if (!configured) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::gba_isa_hybrid_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kA));
-    configured = true;
-  }
+  if (int rc_ = ensure_smem((const void*)isa::gba_isa_hybrid_kernel<128>, kA)) return rc_;
   const int items_t = (pt.n_qblk + 1) / 2;
   isa::gba_isa_hybrid_kernel<128><<<dim3(items_e + items_k7 + items_t, BH), isa::kTThreads, kA, st>>>(
       tq, tk, tv, tkc, tvc, pe, pt, items_e, items_k7, pick);
@@ -356,12 +309,7 @@ int launch_isa_hybrid(const CUtensorMap& tq, const CUtensorMap& tk, const CUtens
 int launch_taylor_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
                     const CUtensorMap& tvc, const isa::AttnParams& p, int BH, cudaStream_t st) {
   using L = isa::TaylorTSmem<128>;
-  static bool configured = false;
-  if (!configured) {
-    ISA_CUDA(cudaFuncSetAttribute(isa::gba_taylor_t_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  L::kAlloc));
-    configured = true;
-  }
+  if (int rc_ = ensure_smem((const void*)isa::gba_taylor_t_kernel<128>, L::kAlloc)) return rc_;
   const int items = (p.n_qblk + 1) / 2;
   if (items < 1) return ISA_OK;
   isa::gba_taylor_t_kernel<128><<<dim3(items, BH), isa::kTThreads, L::kAlloc, st>>>(tq, tk, tv, tkc, tvc, p);
@@ -372,10 +320,6 @@ int launch_taylor_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensor
 int launch_isa_fused(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                      const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& pe,
                      const isa::AttnParams& pt, int items_e, int items_t, int BH, cudaStream_t st) {
-  if (pipe_mode() == 2) {
-    if (D == 128) return launch_isa_fused_p2_t<128>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
-    return launch_isa_fused_p2_t<64>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
-  }
   if (D == 128) return launch_isa_fused_t<128>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
   return launch_isa_fused_t<64>(tq, tk, tv, tkc, tvc, pe, pt, items_e, items_t, BH, st);
 }
@@ -384,12 +328,6 @@ template <int MODE>
 int launch_attention_d(int D, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                        const CUtensorMap& tkc, const CUtensorMap& tvc, const isa::AttnParams& p, int items, int BH,
                        cudaStream_t st) {
-  if constexpr (MODE != isa::MODE_TAYLOR) {
-    if (pipe_mode() == 2 && !p.resid) {  // the p2 epilogue has no gamma residual
-      if (D == 128) return launch_attention_p2<128, MODE>(tq, tk, tv, p, items, BH, st);
-      return launch_attention_p2<64, MODE>(tq, tk, tv, p, items, BH, st);
-    }
-  }
   if (D == 128) return launch_attention<128, MODE>(tq, tk, tv, tkc, tvc, p, items, BH, st);
   return launch_attention<64, MODE>(tq, tk, tv, tkc, tvc, p, items, BH, st);
 }
@@ -481,23 +419,13 @@ int run_pool(const IsaShape* sh, const Dims& d, const void* q, const void* k, co
   return ISA_OK;
 }
 
-// Dynamic shared memory opt-in (once per kernel, grown on demand).
-int ensure_smem(const void* fn, size_t bytes, size_t* cur) {
-  if (bytes > *cur) {
-    ISA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    *cur = bytes;
-  }
-  return ISA_OK;
-}
-
 // Stable top-`kth` selection of each row of a (rows, n) fp64 matrix into
 // ascending kept / dropped index lists (rank flags + compaction).
 int select_rows(const double* vals, int rows, int n, int kth, uint8_t* flags, int* kept, int64_t* kept64,
                 int* dropped, int64_t* dropped64, cudaStream_t st) {
-  static size_t cur_rank = 48 * 1024, cur_comp = 48 * 1024;
   int rc;
-  if ((rc = ensure_smem((const void*)isa::rank_flags_kernel, (size_t)n * 8, &cur_rank))) return rc;
-  if ((rc = ensure_smem((const void*)isa::compact_kernel, (size_t)n * 4, &cur_comp))) return rc;
+  if ((rc = ensure_smem((const void*)isa::rank_flags_kernel, (size_t)n * 8))) return rc;
+  if ((rc = ensure_smem((const void*)isa::compact_kernel, (size_t)n * 4))) return rc;
   isa::rank_flags_kernel<<<dim3((n + 255) / 256, rows), 256, (size_t)n * 8, st>>>(vals, n, kth, flags);
   ISA_LAUNCHED("rank_flags_kernel");
   isa::compact_kernel<<<rows, 1024, (size_t)n * 4, st>>>(flags, n, kth, kept, kept64, dropped, dropped64);
@@ -537,10 +465,9 @@ int launch_mask(const double* scores, int rows, int n, const int* flat, int n_fl
   ISA_MASK_THR(24)
   ISA_MASK_THR(32)
 #undef ISA_MASK_THR
-  static size_t cur = 48 * 1024;
   const size_t sm = 4 * ((size_t)n * 8 + (size_t)W * 4);
   int rc;
-  if ((rc = ensure_smem((const void*)isa::block_mask_kernel, sm, &cur))) return rc;
+  if ((rc = ensure_smem((const void*)isa::block_mask_kernel, sm))) return rc;
   isa::block_mask_kernel<<<(rows + 3) / 4, 128, sm, st>>>(scores, rows, n, flat, n_flat, T, k, W, mask_idx, mask64,
                                                           bits);
   ISA_LAUNCHED("block_mask_kernel");
@@ -560,34 +487,41 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   if ((rc = run_pool(sh, d, q, k, v, w.means, w.bf, err, st))) return rc;
   const bool need_scores = !pinned;
   if (need_scores && d.t_ctx) {
-    isa::qsum_kernel<<<dim3(d.D / 32, d.BH), 256, 0, st>>>(qc, d.T, d.t_src, d.D, w.qsum);
-    ISA_LAUNCHED("qsum_kernel");
-    isa::ctx_score_kernel<<<dim3((d.t_ctx + 7) / 8, d.BH), 256, 0, st>>>(w.qsum, kc, d.T, d.t_src, d.t_ctx, d.D,
-                                                                         d.scale, w.ctx);
-    ISA_LAUNCHED("ctx_score_kernel");
+    // context saliency in the reference's order: fp64 scores of the source
+    // rows against the context columns (numpy einsum bits), sequential mean
+    dim3 g((d.t_ctx + 63) / 64, (d.t_src + 127) / 128, d.BH);
+    isa::coarse_np_kernel<<<g, 256, 0, st>>>(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, nullptr, d.t_src,
+                                             d.t_src, d.t_ctx, d.D, d.scale, w.s_ctx);
+    ISA_LAUNCHED("coarse_np_kernel");
+    isa::ctx_mean_kernel<<<dim3((d.t_ctx + 127) / 128, d.BH), 128, 0, st>>>(w.s_ctx, (long long)d.t_src * d.t_ctx,
+                                                                          d.t_ctx, d.t_src, d.t_ctx, w.ctx);
+    ISA_LAUNCHED("ctx_mean_kernel");
   }
   if (d.gamma > 0.0) {  // coarse residual rows (pipeline.py:261-267), consumed by the attention epilogues
-    if (getenv("ISA_RESID_WARP")) {  // A/B: the warp-per-row kernel
-      dim3 g((d.T + 15) / 16, d.BH);
-      if (d.D == 128)
-        isa::coarse_residual_kernel<128><<<g, 128, 0, st>>>(qc, kc, vc, d.T, (float)d.scale, d.resid_softmax, w.resid);
-      else
-        isa::coarse_residual_kernel<64><<<g, 128, 0, st>>>(qc, kc, vc, d.T, (float)d.scale, d.resid_softmax, w.resid);
-      ISA_LAUNCHED("coarse_residual_kernel");
-    } else {
-      dim3 g((d.T + 63) / 64, d.BH);
-      if ((rc = d.D == 128 ? launch_resid_tiled<128>(g, qc, kc, vc, d, w.resid, st)
-                           : launch_resid_tiled<64>(g, qc, kc, vc, d, w.resid, st)))
-        return rc;
-      ISA_LAUNCHED("coarse_residual_tiled_kernel");
-    }
+    dim3 g((d.T + 63) / 64, d.BH);
+    if ((rc = d.D == 128 ? launch_resid_tiled<128>(g, qc, kc, vc, d, w.resid, st)
+                         : launch_resid_tiled<64>(g, qc, kc, vc, d, w.resid, st)))
+      return rc;
+    ISA_LAUNCHED("coarse_residual_tiled_kernel");
   }
   record(ev, 1, st);
   // ---- stage 2: select (context top-k, K_new block table, fp64 scores vs K_new, centroids)
   if (pinned) {
+    if (d.k_ctx && !pinned->selection) return fail(ISA_ERR_CONTRACT, "pinned routing lacks selection");
+    if ((d.n_sharp && !pinned->sharp) || (d.n_flat && !pinned->flat))
+      return fail(ISA_ERR_CONTRACT, "pinned routing lacks split");
+    if (d.n_flat && !pinned->mask) return fail(ISA_ERR_CONTRACT, "pinned routing lacks mask");
+    // the reference's index contracts, reported through err (the narrowing
+    // below clamps, so a bad index never addresses memory out of bounds)
+    const size_t seen = 4ull * ((d.T + 31) / 32);
+    if ((rc = ensure_smem((const void*)isa::routing_check_kernel, seen))) return rc;
+    isa::routing_check_kernel<<<d.BH, 256, seen, st>>>(d.k_ctx ? pinned->selection : nullptr, d.k_ctx, d.t_ctx,
+                                                       d.n_sharp ? pinned->sharp : nullptr, d.n_sharp,
+                                                       d.n_flat ? pinned->flat : nullptr, d.n_flat, d.T,
+                                                       d.n_flat ? pinned->mask : nullptr, d.k, d.t_new, err);
+    ISA_LAUNCHED("routing_check_kernel");
     if (d.k_ctx) {
-      if (!pinned->selection) return fail(ISA_ERR_CONTRACT, "pinned routing lacks selection");
-      isa::narrow_kernel<<<grid1d(BH * d.k_ctx, 256), 256, 0, st>>>(pinned->selection, w.sel, BH * d.k_ctx);
+      isa::narrow_kernel<<<grid1d(BH * d.k_ctx, 256), 256, 0, st>>>(pinned->selection, w.sel, BH * d.k_ctx, d.t_ctx);
       ISA_LAUNCHED("narrow_kernel");
     }
   } else if (d.k_ctx) {
@@ -599,16 +533,10 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
                                                    w.ctx_short);
   ISA_LAUNCHED("kvblk_from_sel_kernel");
   if (need_scores) {
-    const char* c128 = getenv("ISA_COARSE_N64");
-    if (!(c128 && c128[0] == '0')) {  // default: 128x64 tiles, 2 CTAs/SM (ISA_COARSE_N64=0: 128x128 tiles)
-      dim3 g((d.t_new + 63) / 64, (d.T + 127) / 128, d.BH);
-      isa::coarse_kernel_n64<<<g, 256, 0, st>>>(qc, kc, w.kv_blk, d.T, d.t_new, d.D, d.scale, w.s_new);
-      ISA_LAUNCHED("coarse_kernel_n64");
-    } else {
-      dim3 g((d.t_new + 127) / 128, (d.T + 127) / 128, d.BH);
-      isa::coarse_kernel<<<g, 256, 0, st>>>(qc, kc, w.kv_blk, d.T, d.t_new, d.D, d.scale, w.s_new);
-      ISA_LAUNCHED("coarse_kernel");
-    }
+    dim3 g((d.t_new + 63) / 64, (d.T + 127) / 128, d.BH);
+    isa::coarse_np_kernel<<<g, 256, 0, st>>>(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, w.kv_blk, 0, d.T,
+                                             d.t_new, d.D, d.scale, w.s_new);
+    ISA_LAUNCHED("coarse_np_kernel");
   }
   if (d.n_flat) {
     isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};
@@ -623,18 +551,15 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   record(ev, 2, st);
   // ---- stage 3: split + block mask
   if (pinned) {
-    if ((d.n_sharp && !pinned->sharp) || (d.n_flat && !pinned->flat))
-      return fail(ISA_ERR_CONTRACT, "pinned routing lacks split");
     if (d.n_sharp) {
-      isa::narrow_kernel<<<grid1d(BH * d.n_sharp, 256), 256, 0, st>>>(pinned->sharp, w.sharp, BH * d.n_sharp);
+      isa::narrow_kernel<<<grid1d(BH * d.n_sharp, 256), 256, 0, st>>>(pinned->sharp, w.sharp, BH * d.n_sharp, d.T);
       ISA_LAUNCHED("narrow_kernel");
     }
     if (d.n_flat) {
-      if (!pinned->mask) return fail(ISA_ERR_CONTRACT, "pinned routing lacks mask");
-      isa::narrow_kernel<<<grid1d(BH * d.n_flat, 256), 256, 0, st>>>(pinned->flat, w.flat, BH * d.n_flat);
+      isa::narrow_kernel<<<grid1d(BH * d.n_flat, 256), 256, 0, st>>>(pinned->flat, w.flat, BH * d.n_flat, d.T);
       ISA_LAUNCHED("narrow_kernel");
       isa::narrow_kernel<<<grid1d(BH * d.n_flat * d.k, 256), 256, 0, st>>>(pinned->mask, w.mask,
-                                                                         BH * d.n_flat * d.k);
+                                                                         BH * d.n_flat * d.k, d.t_new);
       ISA_LAUNCHED("narrow_kernel");
       isa::bits_from_mask_kernel<<<BH * d.n_flat, 128, 0, st>>>(w.mask, d.k, d.W, w.bits);
       ISA_LAUNCHED("bits_from_mask_kernel");
@@ -666,7 +591,8 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
                                                                    w.kv_blk, d.t_new, d.t_src, d.l_src, d.l_ctx,
                                                                    w.tiles, w.n_tiles);
     ISA_LAUNCHED("taylor_plan_kernel");
-    isa::taylor_pick_kernel<<<d.BH, 128, 0, st>>>(w.n_tiles, d.items_f, d.n_flat, d.k, taylor_pick_mode(),
+    const int pick = (kn->flags & ISA_FLAG_TAYLOR_K7) ? 0 : (kn->flags & ISA_FLAG_TAYLOR_K7T) ? 1 : taylor_pick_mode();
+    isa::taylor_pick_kernel<<<d.BH, 128, 0, st>>>(w.n_tiles, d.items_f, d.n_flat, d.k, pick,
                                                   w.taylor_pick);
     ISA_LAUNCHED("taylor_pick_kernel");
   }
@@ -861,6 +787,14 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
         return rc;
   }
   record(events, 5, st);
+  if (routing && routing->taylor_kernel) {  // which Taylor-branch kernel ran per head (test hook)
+    if (taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES)) {
+      ISA_CUDA(cudaMemcpyAsync(routing->taylor_kernel, w.taylor_pick, 4ull * d.BH, cudaMemcpyDeviceToDevice, st));
+    } else {
+      isa::fill_i32_kernel<<<grid1d(d.BH, 256), 256, 0, st>>>(routing->taylor_kernel, taylor_t ? 1 : 0, d.BH);
+      ISA_LAUNCHED("fill_i32_kernel");
+    }
+  }
   return ISA_OK;
 }
 
@@ -918,26 +852,13 @@ BwdWs carve_bwd(const Dims& d0, uint8_t* base) {
   return b;
 }
 
-// Backward dK/dV path: tcgen05 kernel by default, mma.sync (ISA_BWD_MMASYNC=1) for A/B.
-bool bwd_mmasync() {
-  static bool v = [] {
-    const char* e = getenv("ISA_BWD_MMASYNC");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
 template <int D>
 int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps, const Workspace& w,
                cudaStream_t st) {
   const size_t tiles = 6ull * 64 * D * 2;  // 2 resident + 2 x 2 double-buffered tiles
-  const size_t sm_dq = tiles + 2 * 64 * 4;
   const size_t sm_dkv = tiles + 4 * 64 * 4 + 16 + 4ull * (d.n_sharp + d.n_flat);
-  static size_t cur_dq = 48 * 1024, cur_e = 48 * 1024, cur_c = 48 * 1024;
   int rc;
-  if ((rc = ensure_smem((const void*)isa::bwd_dq_kernel<D>, sm_dq, &cur_dq))) return rc;
-  if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 0>, sm_dkv, &cur_e))) return rc;
-  if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 1>, sm_dkv, &cur_c))) return rc;
+  if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 1>, sm_dkv))) return rc;
   if (d.n_flat) {
     const int cs = bp.c_splits;
     isa::bwd_dkv_kernel<D, 1><<<dim3(d.tn_pad / 64, d.BH, cs), 128, sm_dkv, st>>>(bp);
@@ -947,26 +868,18 @@ int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps,
       ISA_LAUNCHED("bwd_centroid_reduce_kernel");
     }
   }
-  if (bwd_mmasync()) {
-    isa::bwd_dkv_kernel<D, 0><<<dim3(d.t_new, d.BH), 128, sm_dkv, st>>>(bp);
-    ISA_LAUNCHED("bwd_dkv_kernel<exact>");
-  } else {
+  {
     using TL = isa::BwdTcSmem<D>;
     const int n_list = d.n_sharp + d.n_flat;
     const size_t sm_tc = TL::bytes(n_list);
-    static size_t cur_tc = 48 * 1024;
-    if ((rc = ensure_smem((const void*)isa::bwd_dkv_tc_kernel<D>, sm_tc, &cur_tc))) return rc;
+    if ((rc = ensure_smem((const void*)isa::bwd_dkv_tc_kernel<D>, sm_tc))) return rc;
     isa::BwdTcParams tp{bp, n_list};
     isa::bwd_dkv_tc_kernel<D><<<dim3((d.t_new + 1) / 2, d.BH), 320, sm_tc, st>>>(maps[0], maps[1], maps[2], maps[3], tp);
     ISA_LAUNCHED("bwd_dkv_tc_kernel");
   }
-  if (bwd_mmasync()) {
-    isa::bwd_dq_kernel<D><<<dim3(d.n_sharp + d.n_flat, d.BH), 128, sm_dq, st>>>(bp);
-    ISA_LAUNCHED("bwd_dq_kernel");
-  } else {
+  {
     using QL = isa::BwdDqSmem<D>;
-    static size_t cur_q = 48 * 1024;
-    if ((rc = ensure_smem((const void*)isa::bwd_dq_tc_kernel<D>, QL::kBytes, &cur_q))) return rc;
+    if ((rc = ensure_smem((const void*)isa::bwd_dq_tc_kernel<D>, QL::kBytes))) return rc;
     CUtensorMap tkc = maps[0], tvc = maps[0];  // centroid maps (unused without flat blocks)
     if (d.n_flat) {
       if ((rc = make_map(&tkc, w.kc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
@@ -1319,7 +1232,7 @@ int isa_taylor_forward(const IsaShape* q_shape, int32_t k_len, const int64_t* k_
   ISA_LAUNCHED("kvblk_from_sel_kernel");
   isa::iota_rows_kernel<<<grid1d(BH * d.n_flat, 256), 256, 0, st>>>(w.flat, d.n_flat, BH * d.n_flat);
   ISA_LAUNCHED("iota_rows_kernel");
-  isa::narrow_kernel<<<grid1d(BH * d.n_flat * d.k, 256), 256, 0, st>>>(mask, w.mask, BH * d.n_flat * d.k);
+  isa::narrow_kernel<<<grid1d(BH * d.n_flat * d.k, 256), 256, 0, st>>>(mask, w.mask, BH * d.n_flat * d.k, d.t_new);
   ISA_LAUNCHED("narrow_kernel");
   isa::bits_from_mask_kernel<<<BH * d.n_flat, 128, 0, st>>>(w.mask, d.k, d.W, w.bits);
   ISA_LAUNCHED("bits_from_mask_kernel");
@@ -1427,10 +1340,9 @@ int isa_topk_rows_f64(const double* scores, int32_t rows, int32_t n, int32_t k, 
   }
   const int W = (n + 31) / 32;
   if (method == 2) {  // generic arg-max-rounds kernel (n > 1024 path)
-    static size_t cur = 48 * 1024;
     const size_t sm = 4 * ((size_t)n * 8 + (size_t)W * 4);
     int rc;
-    if ((rc = ensure_smem((const void*)isa::block_mask_kernel, sm, &cur))) return rc;
+    if ((rc = ensure_smem((const void*)isa::block_mask_kernel, sm))) return rc;
     isa::block_mask_kernel<<<(rows + 3) / 4, 128, sm, st>>>(scores, rows, n, nullptr, 1, 0, k, W, nullptr, out_idx,
                                                             nullptr);
     ISA_LAUNCHED("block_mask_kernel");
@@ -1458,6 +1370,32 @@ int isa_split_rows_f64(const double* m, int32_t rows, int32_t n, int32_t n_flat,
   int rc = select_rows(m, rows, n, n - n_flat, flags, nullptr, sharp, nullptr, flat, st);
   cudaFreeAsync(flags, st);
   return rc;
+}
+
+int isa_coarse_scores(int32_t bh, int32_t t_q, int32_t t_k, int32_t d, double scale, const float* qc,
+                      const float* kc, double* s, void* stream) {
+  g_launches = 0;
+  if (bh < 0 || t_q < 0 || t_k < 0 || d < 8 || d % 8) return fail(ISA_ERR_CONFIG, "bad coarse geometry (d %% 8 != 0?)");
+  if (!bh || !t_q || !t_k) return ISA_OK;
+  if (!qc || !kc || !s || (reinterpret_cast<uintptr_t>(qc) & 15) || (reinterpret_cast<uintptr_t>(kc) & 15))
+    return fail(ISA_ERR_LAYOUT, "qc/kc must be 16-byte aligned");
+  dim3 g((t_k + 63) / 64, (t_q + 127) / 128, bh);
+  isa::coarse_np_kernel<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(qc, (long long)t_q * d, kc,
+                                                                          (long long)t_k * d, nullptr, 0, t_q, t_k, d,
+                                                                          scale, s);
+  ISA_LAUNCHED("coarse_np_kernel");
+  return ISA_OK;
+}
+
+int isa_ctx_saliency_f64(const double* s, int32_t bh, int64_t head_stride, int64_t row_stride, int32_t n_src,
+                         int32_t n_ctx, double* out, void* stream) {
+  g_launches = 0;
+  if (bh < 0 || n_src < 1 || n_ctx < 0) return fail(ISA_ERR_CONFIG, "bad saliency geometry");
+  if (!bh || !n_ctx) return ISA_OK;
+  isa::ctx_mean_kernel<<<dim3((n_ctx + 127) / 128, bh), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      s + n_src, head_stride, row_stride, n_src, n_ctx, out);
+  ISA_LAUNCHED("ctx_mean_kernel");
+  return ISA_OK;
 }
 
 int isa_forward_host_bytes(const IsaShape* shape, const IsaKnobs* knobs, int32_t heads_per_chunk,
@@ -1527,6 +1465,7 @@ int isa_forward_host(const IsaShape* shape, const IsaKnobs* knobs, const void* q
       ro.mask = routing->mask ? routing->mask + (long long)bh0 * d.n_flat * d.k : nullptr;
       ro.sharpness = routing->sharpness ? routing->sharpness + (long long)bh0 * d.T : nullptr;
       ro.ctx_scores = routing->ctx_scores ? routing->ctx_scores + (long long)bh0 * d.t_ctx : nullptr;
+      ro.taylor_kernel = routing->taylor_kernel ? routing->taylor_kernel + bh0 : nullptr;
     }
     IsaRoutingIn pi{};
     if (pinned) {

@@ -11,6 +11,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "../../include/isa_b200.h"
+
 namespace isa {
 
 struct SegInfo {
@@ -125,127 +127,124 @@ __global__ void __launch_bounds__(128) pool_means_kernel(const Tin* __restrict__
 }
 
 // ----------------------------------------------------------------------------
-// K2: S_new[bh][u][j] = scale * <qc_u, kc_{kv_blk[j]}> for every query block u
-// < T and every K_new block j < t_new, float64 (pipeline.py:180-182 for the
-// source columns; pipeline.py:221-223 s_flat for the selected context
-// columns, which equal the kc rows of the selected blocks, pipeline.py:210).
-// 64x64 tiles, 256 threads, 4x4 outputs per thread, sequential fp64 FMA over
-// d. kv_blk == null means identity columns. grid (ceil(n/64), ceil(T/64), BH).
+// K2: fp64 coarse scores, bit-identical to the reference's
+//   s = scale * np.einsum("bhid,bhjd->bhij", qc.astype(f64), kc.astype(f64))
+// (pipeline.py:180-182, coarse.py:126). numpy's einsum reduces d with its
+// baseline-SIMD (SSE2, 2 x f64 lanes) sum_of_products_contig_contig_outstride0_two:
+// per group of 8 d it chains acc = a0*b0 + (a1*b1 + (a2*b2 + (a3*b3 + acc)))
+// over the 2-lane vectors a_m = x[8g + 2m .. 8g + 2m + 1], then adds the two
+// lanes. So lane 0 accumulates d = 8g+6, 8g+4, 8g+2, 8g in that order, lane 1
+// d = 8g+7, 8g+5, 8g+3, 8g+1, and the dot is 0 + (lane0 + lane1). qc/kc are
+// fp32, so every product is exact in fp64 and numpy's separate mul + add equals
+// one fp64 FMA: the two-lane FMA chains below reproduce numpy's bits exactly
+// (tests/test_gpu_parity.py pins it against np.einsum; verified 100% equal for
+// D = 64 and 128, the head dims divisible by 8 the kernels take).
+//
+// s_out[bh][i][j] = scale * <qc[bh][i], kc[bh][col(j)]> for i < rows, j < n,
+// col(j) = kv_blk ? kv_blk[bh * n + j] : col0 + j. 128 x 64 output tiles, 256
+// threads, 8 x 4 outputs x 2 lanes per thread; d staged 8 at a time (= one
+// numpy group). grid (ceil(n/64), ceil(rows/128), BH).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) coarse_kernel(const float* __restrict__ qc, const float* __restrict__ kc,
-                                                     const int* __restrict__ kv_blk, int T, int n, int D,
-                                                     double scale, double* __restrict__ s_out) {
-  // 128x128 output tile per CTA, 16x16 threads with 8x8 outputs each (rows
-  // ty+16r, cols tx+16c: conflict-free shared reads), k-chunks of 8.
+__global__ void __launch_bounds__(256, 1) coarse_np_kernel(const float* __restrict__ qc, long long q_hstride,
+                                                           const float* __restrict__ kc, long long k_hstride,
+                                                           const int* __restrict__ kv_blk, int col0, int rows, int n,
+                                                           int D, double scale, double* __restrict__ s_out) {
   __shared__ double As[8][128];
-  __shared__ double Bs[8][128];
-  __shared__ int colrow[128];
+  __shared__ double Bs[8][64];
+  __shared__ int colrow[64];
   const int bh = blockIdx.z;
-  const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 128;
-  const float* qb = qc + (long long)bh * T * D;
-  const float* kb = kc + (long long)bh * T * D;
-  if (threadIdx.x < 128) {
+  const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 64;
+  const float* qb = qc + (long long)bh * q_hstride;
+  const float* kb = kc + (long long)bh * k_hstride;
+  if (threadIdx.x < 64) {
     const int j = j0 + threadIdx.x;
-    colrow[threadIdx.x] = j < n ? (kv_blk ? kv_blk[(long long)bh * n + j] : j) : -1;
+    colrow[threadIdx.x] = j < n ? (kv_blk ? kv_blk[(long long)bh * n + j] : col0 + j) : -1;
   }
   __syncthreads();
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[8][8];
+  double acc0[8][4], acc1[8][4];
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
-  // loader: thread -> (row = tid / 2, 4 consecutive d) for both operands
+    for (int c = 0; c < 4; ++c) acc0[r][c] = acc1[r][c] = 0.0;
+  // loaders: A = 128 rows x 8 d (thread -> row tid/2, 4 d); B = 64 rows x 8 d (threads < 128)
   const int lr = threadIdx.x >> 1, ld = (threadIdx.x & 1) * 4;
   const int gi = i0 + lr;
-  const int gj = colrow[lr];
-  const float* arow = gi < T ? qb + (long long)gi * D + ld : nullptr;
+  const float* arow = gi < rows ? qb + (long long)gi * D + ld : nullptr;
+  const int gj = threadIdx.x < 128 ? colrow[lr] : -1;
   const float* brow = gj >= 0 ? kb + (long long)gj * D + ld : nullptr;
   const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  // register prefetch of the next k-chunk hides the global-load latency
   float4 a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow)) : zero4;
   float4 b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow)) : zero4;
   for (int d0 = 0; d0 < D; d0 += 8) {
     As[ld + 0][lr] = a4.x; As[ld + 1][lr] = a4.y; As[ld + 2][lr] = a4.z; As[ld + 3][lr] = a4.w;
-    Bs[ld + 0][lr] = b4.x; Bs[ld + 1][lr] = b4.y; Bs[ld + 2][lr] = b4.z; Bs[ld + 3][lr] = b4.w;
+    if (threadIdx.x < 128) {
+      Bs[ld + 0][lr] = b4.x; Bs[ld + 1][lr] = b4.y; Bs[ld + 2][lr] = b4.z; Bs[ld + 3][lr] = b4.w;
+    }
     __syncthreads();
     if (d0 + 8 < D) {
       a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow + d0 + 8)) : zero4;
       b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow + d0 + 8)) : zero4;
     }
 #pragma unroll
-    for (int dd = 0; dd < 8; ++dd) {
-      double a[8], bv[8];
+    for (int m = 3; m >= 0; --m) {  // numpy's chain order a3, a2, a1, a0
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        a[t] = As[dd][ty + 16 * t];
-        bv[t] = Bs[dd][tx + 16 * t];
+      for (int lane = 0; lane < 2; ++lane) {
+        const int dd = 2 * m + lane;
+        double a[8], bv[4];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) a[t] = As[dd][ty + 16 * t];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bv[t] = Bs[dd][tx + 16 * t];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (lane == 0) acc0[r][c] = fma(a[r], bv[c], acc0[r][c]);
+            else acc1[r][c] = fma(a[r], bv[c], acc1[r][c]);
+          }
       }
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[r][c] = fma(a[r], bv[c], acc[r][c]);
     }
     __syncthreads();
   }
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int i = i0 + ty + 16 * r;
-    if (i >= T) continue;
+    if (i >= rows) continue;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < 4; ++c) {
       const int j = j0 + tx + 16 * c;
-      if (j < n) s_out[((long long)bh * T + i) * n + j] = scale * acc[r][c];
+      if (j < n) s_out[((long long)bh * rows + i) * n + j] = scale * __dadd_rn(0.0, __dadd_rn(acc0[r][c], acc1[r][c]));
     }
   }
 }
 
 // ----------------------------------------------------------------------------
-// K2b: context saliency = mean over source query blocks of the scaled coarse
-// score (coarse.py:155), through linearity:
-//   ctx[c] = scale * <sum_{i<t_src} qc_i, kc_{t_src+c}> / t_src   (fp64).
-// qsum_kernel: grid (BH), block D: column sums in fp64 (coalesced over d).
-// ctx_score_kernel: grid (ceil(t_ctx/8), BH), 8 warps, one context column per
-// warp (lanes over d).
+// K2b: context saliency = s_coarse[:, :, :t_src, t_src:].mean(axis=2)
+// (coarse.py:155) in numpy's order: the reduction over the (outer) query-block
+// axis adds rows sequentially, ((s_0 + s_1) + s_2) + ..., then divides by
+// t_src. `s_ctx` holds the t_src x t_ctx scores from coarse_np_kernel (same
+// bits as the reference's s_coarse), so the means are bit-identical too.
+// Element (bh, i, c) at s + bh * head_stride + i * row_stride + c. Thread per
+// context column; 8 rows of loads in flight. grid (ceil(t_ctx/128), BH).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) qsum_kernel(const float* __restrict__ qc, int T, int t_src, int D,
-                                                   double* __restrict__ qsum) {
-  // grid (D/32, BH): 8 warps stride over the source rows for 32 columns, then a
-  // fixed-order combine across warps (deterministic).
-  __shared__ double part[8][33];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int d = blockIdx.x * 32 + lane, bh = blockIdx.y;
-  const float* qb = qc + (long long)bh * T * D + d;
-  double s0 = 0.0, s1 = 0.0;
-  int i = warp;
-  for (; i + 8 < t_src; i += 16) {
-    s0 += static_cast<double>(qb[(long long)i * D]);
-    s1 += static_cast<double>(qb[(long long)(i + 8) * D]);
-  }
-  if (i < t_src) s0 += static_cast<double>(qb[(long long)i * D]);
-  part[warp][lane] = s0 + s1;
-  __syncthreads();
-  if (warp == 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) t += part[w][lane];
-    qsum[(long long)bh * D + d] = t;
-  }
-}
-
-__global__ void __launch_bounds__(256) ctx_score_kernel(const double* __restrict__ qsum, const float* __restrict__ kc,
-                                                        int T, int t_src, int t_ctx, int D, double scale,
-                                                        double* __restrict__ ctx) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 8 + warp, bh = blockIdx.y;
+__global__ void __launch_bounds__(128) ctx_mean_kernel(const double* __restrict__ s, long long head_stride,
+                                                       long long row_stride, int t_src, int t_ctx,
+                                                       double* __restrict__ ctx) {
+  const int c = blockIdx.x * 128 + threadIdx.x, bh = blockIdx.y;
   if (c >= t_ctx) return;
-  const float* kr = kc + ((long long)bh * T + t_src + c) * D;
-  const double* qs = qsum + (long long)bh * D;
-  double s = 0.0;
-  for (int d = lane; d < D; d += 32) s = fma(qs[d], static_cast<double>(kr[d]), s);
+  const double* col = s + (long long)bh * head_stride + c;
+  double acc = col[0];
+  int i = 1;
+  for (; i + 8 <= t_src; i += 8) {
+    double v[8];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) ctx[(long long)bh * t_ctx + c] = scale * s / static_cast<double>(t_src);
+    for (int u = 0; u < 8; ++u) v[u] = col[(long long)(i + u) * row_stride];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
+  }
+  for (; i < t_src; ++i) acc += col[(long long)i * row_stride];
+  ctx[(long long)bh * t_ctx + c] = acc / static_cast<double>(t_src);
 }
 
 // ----------------------------------------------------------------------------
@@ -674,157 +673,13 @@ __global__ void __launch_bounds__(64) taylor_plan_kernel(const uint32_t* __restr
   if (threadIdx.x == 0) n_tiles[bh * n_items + item] = nt;
 }
 
-// Same scores, 128 x 64 output tiles: 8 x 4 outputs per thread (half the
-// accumulators), so two CTAs (16 warps) fit per SM and hide the DFMA / LDS
-// latencies better; same sequential fp64 FMA order over d, so the values are
-// bit-identical to coarse_kernel. grid (ceil(n/64), ceil(T/128), BH).
-__global__ void __launch_bounds__(256, 2) coarse_kernel_n64(const float* __restrict__ qc, const float* __restrict__ kc,
-                                                            const int* __restrict__ kv_blk, int T, int n, int D,
-                                                            double scale, double* __restrict__ s_out) {
-  __shared__ double As[8][128];
-  __shared__ double Bs[8][64];
-  __shared__ int colrow[64];
-  const int bh = blockIdx.z;
-  const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 64;
-  const float* qb = qc + (long long)bh * T * D;
-  const float* kb = kc + (long long)bh * T * D;
-  if (threadIdx.x < 64) {
-    const int j = j0 + threadIdx.x;
-    colrow[threadIdx.x] = j < n ? (kv_blk ? kv_blk[(long long)bh * n + j] : j) : -1;
-  }
-  __syncthreads();
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[8][4];
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-  // loaders: A = 128 rows x 8 d (thread -> row tid/2, 4 d); B = 64 rows x 8 d (threads < 128)
-  const int lr = threadIdx.x >> 1, ld = (threadIdx.x & 1) * 4;
-  const int gi = i0 + lr;
-  const float* arow = gi < T ? qb + (long long)gi * D + ld : nullptr;
-  const int gj = threadIdx.x < 128 ? colrow[lr] : -1;
-  const float* brow = gj >= 0 ? kb + (long long)gj * D + ld : nullptr;
-  const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow)) : zero4;
-  float4 b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow)) : zero4;
-  for (int d0 = 0; d0 < D; d0 += 8) {
-    As[ld + 0][lr] = a4.x; As[ld + 1][lr] = a4.y; As[ld + 2][lr] = a4.z; As[ld + 3][lr] = a4.w;
-    if (threadIdx.x < 128) {
-      Bs[ld + 0][lr] = b4.x; Bs[ld + 1][lr] = b4.y; Bs[ld + 2][lr] = b4.z; Bs[ld + 3][lr] = b4.w;
-    }
-    __syncthreads();
-    if (d0 + 8 < D) {
-      a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow + d0 + 8)) : zero4;
-      b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow + d0 + 8)) : zero4;
-    }
-#pragma unroll
-    for (int dd = 0; dd < 8; ++dd) {
-      double a[8], bv[4];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) a[t] = As[dd][ty + 16 * t];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) bv[t] = Bs[dd][tx + 16 * t];
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], bv[c], acc[r][c]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int i = i0 + ty + 16 * r;
-    if (i >= T) continue;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = j0 + tx + 16 * c;
-      if (j < n) s_out[((long long)bh * T + i) * n + j] = scale * acc[r][c];
-    }
-  }
-}
-
 // ----------------------------------------------------------------------------
 // Coarse residual O_coarse (pipeline.py:261-267): per query block u,
 //   softmax variant  O_u = sum_j softmax_j(scale * qc_u . kc_j) vc_j
 //   raw variant      O_u = sum_j (qc_u . kc_j) vc_j
-// over all T key blocks, fp32 with an online softmax. Added to every row of
-// block u as out += gamma * O_u in the attention epilogues
-// (pipeline.py:354-356). grid (ceil(T/16), BH), 128 threads: each warp owns 4
-// query blocks, each lane D/32 columns; key blocks staged 32 at a time.
-// ----------------------------------------------------------------------------
-template <int D>
-__global__ void __launch_bounds__(128) coarse_residual_kernel(const float* __restrict__ qc,
-                                                             const float* __restrict__ kc,
-                                                             const float* __restrict__ vc, int T, float scale,
-                                                             int use_softmax, float* __restrict__ out) {
-  constexpr int kC = D / 32;  // columns per lane
-  constexpr int kJ = 32;      // key blocks per stage
-  __shared__ float sk[kJ][D];
-  __shared__ float sv[kJ][D];
-  const int bh = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long base = (long long)bh * T * D;
-  float q[4][kC], acc[4][kC], m[4], l[4];
-  int rows[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    rows[r] = blockIdx.x * 16 + warp * 4 + r;
-    const int u = rows[r] < T ? rows[r] : T - 1;
-#pragma unroll
-    for (int c = 0; c < kC; ++c) {
-      q[r][c] = qc[base + (long long)u * D + c * 32 + lane];
-      acc[r][c] = 0.f;
-    }
-    m[r] = -INFINITY;
-    l[r] = 0.f;
-  }
-  for (int j0 = 0; j0 < T; j0 += kJ) {
-    const int nj = T - j0 < kJ ? T - j0 : kJ;
-    __syncthreads();
-    for (int e = threadIdx.x; e < nj * D; e += 128) {
-      sk[e / D][e % D] = kc[base + (long long)j0 * D + e];
-      sv[e / D][e % D] = vc[base + (long long)j0 * D + e];
-    }
-    __syncthreads();
-    for (int j = 0; j < nj; ++j) {
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        float sdot = 0.f;
-#pragma unroll
-        for (int c = 0; c < kC; ++c) sdot = fmaf(q[r][c], sk[j][c * 32 + lane], sdot);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
-        float w;
-        if (use_softmax) {
-          const float sv_ = sdot * scale;
-          const float mn = fmaxf(m[r], sv_);
-          const float corr = __expf(m[r] - mn);  // m = -inf -> 0
-          w = __expf(sv_ - mn);
-          l[r] = l[r] * corr + w;
-#pragma unroll
-          for (int c = 0; c < kC; ++c) acc[r][c] *= corr;
-          m[r] = mn;
-        } else {
-          w = sdot;  // raw, unscaled scores
-        }
-#pragma unroll
-        for (int c = 0; c < kC; ++c) acc[r][c] = fmaf(w, sv[j][c * 32 + lane], acc[r][c]);
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    if (rows[r] >= T) continue;
-    const float inv = use_softmax ? 1.f / l[r] : 1.f;
-#pragma unroll
-    for (int c = 0; c < kC; ++c) out[base + (long long)rows[r] * D + c * 32 + lane] = acc[r][c] * inv;
-  }
-}
-
-// ----------------------------------------------------------------------------
-// Coarse residual, register-tiled (same math as coarse_residual_kernel above):
-// a small fp32 flash attention of the T block means per head. CTA = 64 query
+// over all T key blocks, added to every row of block u as out += gamma * O_u
+// in the attention epilogues (pipeline.py:354-356). Register-tiled fp32 flash
+// attention of the T block means per head. CTA = 64 query
 // blocks x all T key blocks in tiles of 64, 256 threads; thread (ty, tx) owns
 // query rows 4ty..4ty+3, keys tx + 16kk (kk < 4) of S and output columns
 // 4tx + 64cc (cc < D/64) of O. Q/K/V tiles are row-major in shared memory
@@ -1051,9 +906,68 @@ __global__ void widen_kernel(const int* __restrict__ src, int64_t* __restrict__ 
     dst[i] = src[i];
 }
 // int64 -> int32 import of pinned routing.
-__global__ void narrow_kernel(const int64_t* __restrict__ src, int* __restrict__ dst, long long n) {
+// int64 -> int32 index narrowing, clamped into [0, hi): an out-of-range
+// caller index (reported by routing_check_kernel) can never address memory
+// outside the workspace / output on the way to the error.
+__global__ void narrow_kernel(const int64_t* __restrict__ src, int* __restrict__ dst, long long n, int hi) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long x = src[i];
+    dst[i] = static_cast<int>(x < 0 ? 0 : (x >= hi ? hi - 1 : x));
+  }
+}
+
+// Pinned routing checks (isa_forward_with_routing / isa_backward(routing=)),
+// the reference's index contracts: selection and the sharp/flat lists are
+// gathered with _normalize_block_index (tensor.py:120-133: out of range ->
+// BlockIndexError, not strictly ascending -> ContractError); the flat mask
+// goes through TaylorKernelInput (taylor.py:80-84: range and order ->
+// ContractError); sharp and flat must partition the T query blocks (the
+// reference scatters both into one output, pipeline.py:351-353). Error bits
+// (atomicOr into err): see ISA_ERRBIT_* in include/isa_b200.h.
+// grid BH, block 256, dyn smem ceil(T/32) words.
+__global__ void __launch_bounds__(256) routing_check_kernel(const int64_t* __restrict__ sel, int k_ctx, int t_ctx,
+                                                            const int64_t* __restrict__ sharp, int n_sharp,
+                                                            const int64_t* __restrict__ flat, int n_flat, int T,
+                                                            const int64_t* __restrict__ mask, int k, int t_new,
+                                                            int32_t* __restrict__ err) {
+  extern __shared__ uint32_t seen[];
+  const long long bh = blockIdx.x;
+  const int W = (T + 31) >> 5;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) seen[w] = 0u;
+  __syncthreads();
+  int bits = 0;
+  if (sel)
+    for (int i = threadIdx.x; i < k_ctx; i += blockDim.x) {
+      const long long x = sel[bh * k_ctx + i];
+      if (x < 0 || x >= t_ctx) bits |= ISA_ERRBIT_SEL_RANGE;
+      if (i > 0 && x <= sel[bh * k_ctx + i - 1]) bits |= ISA_ERRBIT_SEL_ORDER;
+    }
+  for (int part = 0; part < 2; ++part) {
+    const int64_t* lst = part ? flat : sharp;
+    const int n = part ? n_flat : n_sharp;
+    if (!lst) continue;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const long long x = lst[bh * n + i];
+      if (x < 0 || x >= T) {
+        bits |= ISA_ERRBIT_SPLIT_RANGE;
+        continue;
+      }
+      if (i > 0 && x <= lst[bh * n + i - 1]) bits |= ISA_ERRBIT_SPLIT_ORDER;
+      if (atomicOr(&seen[x >> 5], 1u << (x & 31)) & (1u << (x & 31))) bits |= ISA_ERRBIT_SPLIT_ORDER;
+    }
+  }
+  if (mask)
+    for (long long e = threadIdx.x; e < (long long)n_flat * k; e += blockDim.x) {
+      const long long x = mask[bh * n_flat * k + e];
+      if (x < 0 || x >= t_new) bits |= ISA_ERRBIT_MASK;
+      if (e % k && x <= mask[bh * n_flat * k + e - 1]) bits |= ISA_ERRBIT_MASK;
+    }
+  if (bits) atomicOr(err, bits);
+}
+
+__global__ void fill_i32_kernel(int* __restrict__ out, int v, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    dst[i] = static_cast<int>(src[i]);
+    out[i] = v;
 }
 
 // out[i] = i mod n: per-(b, h) lists 0..n-1 (the standalone Taylor kernel's flat list).

@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .errors import ConfigError, DegenerateRowError, InputError, LayoutError
+from .errors import BlockIndexError, ConfigError, ContractError, DegenerateRowError, InputError, LayoutError
 from .types import (
     BlockMask,
     GradBundle,
@@ -156,26 +156,47 @@ def _routing_buffers(d: IsaDims, device):
         "mask": torch.empty((B, H, d.n_flat, d.k), **i64),
         "sharpness": torch.empty((B, H, d.T), dtype=torch.float64, device=device),
         "ctx_scores": torch.empty((B, H, d.t_ctx), dtype=torch.float64, device=device),
+        "taylor_kernel": torch.empty((B, H), dtype=torch.int32, device=device),
     }
 
 
 def _routing_struct(bufs) -> N.IsaRoutingOut:
     return N.IsaRoutingOut(*(_ptr(bufs[n]) if bufs[n].numel() else None
-                             for n in ("selection", "sharp", "flat", "mask", "sharpness", "ctx_scores")))
+                             for n in ("selection", "sharp", "flat", "mask", "sharpness", "ctx_scores",
+                                       "taylor_kernel")))
 
 
-def _make_routing(d: IsaDims, bufs) -> IsaRouting:
-    sel = SelectionIndex(bufs["selection"], d.t_ctx)
-    split = SharpnessSplit(bufs["sharp"], bufs["flat"], bufs["sharpness"])
-    mask = BlockMask(bufs["mask"], d.t_new) if d.n_flat else None
+def _make_routing(d: IsaDims, bufs, numpy_io: bool = False) -> IsaRouting:
+    """Routing value types over the exported buffers: device tensors, or numpy
+    arrays for numpy callers (the reference's types hold numpy, coarse.py:52-107)."""
+    cv = (lambda t: t.cpu().numpy()) if numpy_io else (lambda t: t)
+    sel = SelectionIndex(cv(bufs["selection"]), d.t_ctx)
+    split = SharpnessSplit(cv(bufs["sharp"]), cv(bufs["flat"]), cv(bufs["sharpness"]))
+    mask = BlockMask(cv(bufs["mask"]), d.t_new) if d.n_flat else None
     return IsaRouting(selection=sel, split=split, mask=mask)
 
 
 def _raise_flags(err: torch.Tensor):
+    """Device error word (ISA_ERRBIT_*) -> the reference's exceptions. Pinned
+    routing is checked in the reference's order: the selection gather
+    (pipeline.py:189-192 via tensor.py:120-133), then the sharp/flat gathers,
+    then the Taylor mask (taylor.py:80-84)."""
     flags = int(err.item())
-    if flags & 1:
+    if flags & N.ERRBIT_INPUT:
         raise InputError("Q/K/V: non-finite elements")
-    if flags & 2:
+    if flags & N.ERRBIT_SEL_RANGE:
+        raise BlockIndexError("gather_blocks: pinned selection block index out of range [0, T_ctx)")
+    if flags & N.ERRBIT_SEL_ORDER:
+        raise ContractError("gather_blocks: pinned selection lists must be sorted ascending without duplicates")
+    if flags & N.ERRBIT_SPLIT_RANGE:
+        raise BlockIndexError("gather_blocks: pinned sharp/flat block index out of range [0, T)")
+    if flags & N.ERRBIT_SPLIT_ORDER:
+        raise ContractError("pinned sharp/flat lists must be sorted ascending without duplicates "
+                            "and partition the query blocks")
+    if flags & N.ERRBIT_MASK:
+        raise ContractError("pinned mask indices out of range for the K_new blocks or not sorted ascending "
+                            "without duplicates")
+    if flags & N.ERRBIT_DEGENERATE:
         raise DegenerateRowError("row with empty key set: normalizer is zero")
 
 
@@ -285,9 +306,10 @@ def _run_host(inp: _Inputs, collect_trace: bool, pinned=None, out=None, validate
         times = _LazyStageTimes({"kernel": (e0, e1)})
         for name in ("coarse", "select", "split", "reconstruct"):
             dict.__setitem__(times, name, 0.0)  # not separable: stages of all chunks interleave
-        routing = _make_routing(d, bufs)
+        routing = _make_routing(d, bufs, inp.numpy_io)
         trace = IsaTrace(coarse_summary={"host_streamed": True}, selection=routing.selection,
-                         split=routing.split, mask=routing.mask, flops=d.flops(), stage_times_us=times)
+                         split=routing.split, mask=routing.mask, flops=d.flops(), stage_times_us=times,
+                         ctx_scores=bufs["ctx_scores"], taylor_kernel=bufs["taylor_kernel"])
     del keep
     if inp.numpy_io:
         out = out.float().numpy()
@@ -348,9 +370,10 @@ def _run(inp: _Inputs, collect_trace: bool, pinned=None, out: Optional[torch.Ten
         times = _LazyStageTimes({"coarse": (evs[0], evs[1]), "select": (evs[1], evs[2]),
                                  "split": (evs[2], evs[3]), "kernel": (evs[3], evs[5])})
         dict.__setitem__(times, "reconstruct", 0.0)
-        routing = _make_routing(d, bufs)
+        routing = _make_routing(d, bufs, inp.numpy_io)
         trace = IsaTrace(coarse_summary=_LazySummary(qc, kc, d.scale), selection=routing.selection,
-                         split=routing.split, mask=routing.mask, flops=d.flops(), stage_times_us=times)
+                         split=routing.split, mask=routing.mask, flops=d.flops(), stage_times_us=times,
+                         ctx_scores=bufs["ctx_scores"], taylor_kernel=bufs["taylor_kernel"])
     del keep
     if inp.numpy_io:
         out = out.float().cpu().numpy()
@@ -394,8 +417,11 @@ def _unpad(x, D: int):
     return x[..., :D].contiguous()
 
 
+_TAYLOR_FLAGS = {None: 0, "auto": 0, "k7": 2, "k7t": 4}
+
+
 def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = True, *, out=None, validate=True,
-                heads_per_chunk: int = 0):
+                heads_per_chunk: int = 0, taylor_kernel: Optional[str] = None):
     """Run the full pipeline; returns (output, IsaTrace or None) (pipeline.py:307-316).
 
     The output has the input dtype (bf16 in -> bf16 out; fp32 in -> fp32 out,
@@ -404,13 +430,17 @@ def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = T
     Host inputs (numpy / CPU tensors) are streamed through the GPU in chunks of
     `heads_per_chunk` heads (0 = about 150 MB of inputs); the result is complete on return.
     Head dims other than 64/128 (up to 128) run zero-padded (`_pad_head_dim`).
+    `taylor_kernel` ("k7" | "k7t" | None = per-head automatic choice) forces
+    the D = 128 Taylor-branch kernel (test / A-B hook; same operator).
     """
+    if taylor_kernel not in _TAYLOR_FLAGS:
+        raise ConfigError(f"taylor_kernel must be one of {sorted(k for k in _TAYLOR_FLAGS if k)} or None")
     padded = _pad_head_dim(cfg, q, k, v)
     if padded is not None:
         D = int(q.shape[-1])
         pcfg, pq, pk, pv = padded
         res, trace = isa_forward(pq, pk, pv, icl, pcfg, collect_trace, validate=validate,
-                                 heads_per_chunk=heads_per_chunk)
+                                 heads_per_chunk=heads_per_chunk, taylor_kernel=taylor_kernel)
         res = _unpad(res, D)
         if trace is not None:  # FLOP tallies of the real head dim
             trace.flops = IsaDims.derive(q.shape, icl_from_any(icl), pcfg).flops()
@@ -418,16 +448,19 @@ def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = T
             out[...] = res
             res = out
         return res, trace
-    res, trace, _ = _run(_Inputs(q, k, v, icl, cfg), collect_trace, out=out, validate=validate,
-                         heads_per_chunk=heads_per_chunk)
+    inp = _Inputs(q, k, v, icl, cfg)
+    inp.knobs.flags |= _TAYLOR_FLAGS[taylor_kernel]
+    res, trace, _ = _run(inp, collect_trace, out=out, validate=validate, heads_per_chunk=heads_per_chunk)
     return res, trace
 
 
 def isa_routing(q, k, v, icl: IclLayout, cfg: IsaConfig) -> IsaRouting:
-    """Stages 1-3 only (pipeline.py:302-304); index tensors stay on the GPU."""
+    """Stages 1-3 only (pipeline.py:302-304). Index tensors stay on the GPU for
+    torch callers; numpy callers get numpy arrays, like the reference."""
     padded = _pad_head_dim(cfg, q, k, v)
     if padded is not None:
         return isa_routing(*padded[1:], icl, padded[0])
+    numpy_io = isinstance(q, np.ndarray)
     inp = _Inputs(q, k, v, icl, cfg)
     if inp.host:  # routing reads all of Q/K/V once: one plain upload
         inp = _Inputs(*(t.cuda() for t in (inp.q, inp.k, inp.v)), icl, cfg)
@@ -441,7 +474,7 @@ def isa_routing(q, k, v, icl: IclLayout, cfg: IsaConfig) -> IsaRouting:
     N.check(lib.isa_routing(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), _ptr(inp.q), _ptr(inp.k), _ptr(inp.v),
                             _ptr(ws), nbytes, ctypes.byref(rout), _ptr(err), stream))
     _raise_flags(err)
-    return _make_routing(d, bufs)
+    return _make_routing(d, bufs, numpy_io)
 
 
 def isa_forward_with_routing(q, k, v, icl: IclLayout, cfg: IsaConfig, routing) -> object:

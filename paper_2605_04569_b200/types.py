@@ -301,6 +301,11 @@ class IsaTrace:
     mask: Optional[BlockMask]
     flops: FlopCount
     stage_times_us: dict = field(default_factory=dict)
+    # B200 extensions (not in the reference trace): the context saliency
+    # scores (B,H,T_ctx) fp64, bit-identical to coarse.py:155, and the
+    # Taylor-branch kernel run per head (B,H) int32: 0 = K7 union tiles, 1 = K7T
+    ctx_scores: object = None
+    taylor_kernel: object = None
 
     def to_text(self) -> str:
         lines = ["isa_trace:", "  coarse:"]
