@@ -185,7 +185,7 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_2605_04569_b200 as P
     from paper_2605_04569_b200 import _native as N
-    from paper_2605_04569_b200.parallel import head_shard, isa_forward_sharded
+    from paper_2605_04569_b200.parallel import ShardedIsa, head_shard
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -207,6 +207,9 @@ def run_ours(args, rank, world, local_rank):
 
     out_full = torch.empty((1, H, S, D), dtype=torch.bfloat16, device=dev) if world > 1 else None
     prep = P.prepare(q, k, v, icl, cfg)
+    # N > 1: chunked schedule, one local head per chunk on two alternating
+    # compute streams, chunk c's NCCL all-gather under chunk c+1's compute
+    sharded = ShardedIsa(q, k, v, icl, cfg, world) if world > 1 else None
 
     # per-kernel CUDA events recorded by the C ABI inside every timed step
     # (N = 1): the stage / roofline durations come from the timed region itself
@@ -222,7 +225,7 @@ def run_ours(args, rank, world, local_rank):
 
     def step():
         if world > 1:
-            return isa_forward_sharded(prep, out_full, my_heads, world)
+            return sharded(out_full)
         if timed_step[0] is not None:
             _call_with_events(prep, step_structs[timed_step[0]], 0)
             timed_step[0] += 1
@@ -255,10 +258,32 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     clocks = clk.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    compute_only_ms = gather_ok = None
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        # the same schedule without the all-gathers (scaling without the collective)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            sharded(out_full, gather=False)
+        e1.record(st)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        compute_only_ms = float(t.item())
+        # placement check: every head slab of the gathered output equals its
+        # owner's local result (per-head sums, exact: same bits, same reduction)
+        sharded(out_full)
+        torch.cuda.synchronize()
+        mine_sums = torch.stack([o[0, 0].float().sum() for o in sharded.local_output()]).to(dev)
+        all_sums = [torch.empty_like(mine_sums) for _ in range(world)]
+        dist.all_gather(all_sums, mine_sums)
+        full_sums = torch.stack([out_full[0, h].float().sum() for h in range(H)])
+        gather_ok = all(bool(torch.equal(full_sums[c * world + r], all_sums[r][c]))
+                        for r in range(world) for c in range(Hl))
 
     # ---- per-stage / per-kernel times (events recorded by the C ABI on the launching stream)
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
@@ -325,6 +350,11 @@ def run_ours(args, rank, world, local_rank):
         "flops": {"isa": f_isa, "dense": f_dense, "sharp": f_sharp * world, "taylor_alg": f_taylor_alg * world},
         "stage_ms": stage,
         "step_ms_stats": step_stats,
+        "sharded": None if world == 1 else {
+            "compute_only_ms": compute_only_ms, "heads_per_rank": Hl, "chunk_heads": 1,
+            "gather_check": gather_ok, "backend": os.environ.get("ISA_BENCH_BACKEND", "nccl"),
+            "note": "value = max over ranks of the chunked compute + overlapped NCCL all-gather step; "
+                    "compute_only_ms = the same schedule without the gathers (max over ranks)"},
         "gpu_launches": launches * args.steps,
         "roofline": {
             "kernel": "gba_isa_hybrid_kernel<128> (K6 sharp items + per-head K7T / K7 Taylor items, one launch)",
@@ -495,9 +525,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and world == 1 and args.gpus > 1:
-        print(json.dumps({"error": "--gpus > 1 must be launched with torch.distributed.run"}))
-        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # self-launch: one process per GPU under torch.distributed.run (rank 0 prints)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -505,8 +545,14 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("ISA_BENCH_BACKEND", "nccl")
+        if backend == "gloo":  # functional check of the N > 1 schedule on fewer GPUs than ranks
+            local_rank %= torch.cuda.device_count()
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -14,7 +14,8 @@ import threading
 from .errors import ISA_OK, STATUS_TO_ERROR, NativeError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libisa_b200.so")
+# ISA_B200_LIB points at an alternative build of the same C ABI (A/B kernel measurements)
+LIB_PATH = os.environ.get("ISA_B200_LIB") or os.path.join(HERE, "libisa_b200.so")
 
 ISA_ABI_VERSION = 3
 ISA_DTYPE_BF16 = 0

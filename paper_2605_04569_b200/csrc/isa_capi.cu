@@ -489,8 +489,8 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   if (need_scores && d.t_ctx) {
     // context saliency in the reference's order: fp64 scores of the source
     // rows against the context columns (numpy einsum bits), sequential mean
-    dim3 g((d.t_ctx + 63) / 64, (d.t_src + 127) / 128, d.BH);
-    isa::coarse_np_kernel<<<g, 256, 0, st>>>(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, nullptr, d.t_src,
+    dim3 g((d.t_ctx + 63) / 64, (d.t_src + 63) / 64, d.BH);
+    isa::coarse_np_kernel<<<g, 128, 0, st>>>(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, nullptr, d.t_src,
                                              d.t_src, d.t_ctx, d.D, d.scale, w.s_ctx);
     ISA_LAUNCHED("coarse_np_kernel");
     isa::ctx_mean_kernel<<<dim3((d.t_ctx + 127) / 128, d.BH), 128, 0, st>>>(w.s_ctx, (long long)d.t_src * d.t_ctx,
@@ -533,8 +533,8 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
                                                    w.ctx_short);
   ISA_LAUNCHED("kvblk_from_sel_kernel");
   if (need_scores) {
-    dim3 g((d.t_new + 63) / 64, (d.T + 127) / 128, d.BH);
-    isa::coarse_np_kernel<<<g, 256, 0, st>>>(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, w.kv_blk, 0, d.T,
+    dim3 g((d.t_new + 63) / 64, (d.T + 63) / 64, d.BH);
+    isa::coarse_np_kernel<<<g, 128, 0, st>>>(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, w.kv_blk, 0, d.T,
                                              d.t_new, d.D, d.scale, w.s_new);
     ISA_LAUNCHED("coarse_np_kernel");
   }
@@ -1379,8 +1379,8 @@ int isa_coarse_scores(int32_t bh, int32_t t_q, int32_t t_k, int32_t d, double sc
   if (!bh || !t_q || !t_k) return ISA_OK;
   if (!qc || !kc || !s || (reinterpret_cast<uintptr_t>(qc) & 15) || (reinterpret_cast<uintptr_t>(kc) & 15))
     return fail(ISA_ERR_LAYOUT, "qc/kc must be 16-byte aligned");
-  dim3 g((t_k + 63) / 64, (t_q + 127) / 128, bh);
-  isa::coarse_np_kernel<<<g, 256, 0, static_cast<cudaStream_t>(stream)>>>(qc, (long long)t_q * d, kc,
+  dim3 g((t_k + 63) / 64, (t_q + 63) / 64, bh);
+  isa::coarse_np_kernel<<<g, 128, 0, static_cast<cudaStream_t>(stream)>>>(qc, (long long)t_q * d, kc,
                                                                           (long long)t_k * d, nullptr, 0, t_q, t_k, d,
                                                                           scale, s);
   ISA_LAUNCHED("coarse_np_kernel");

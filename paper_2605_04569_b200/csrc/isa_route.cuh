@@ -141,19 +141,31 @@ __global__ void __launch_bounds__(128) pool_means_kernel(const Tin* __restrict__
 // D = 64 and 128, the head dims divisible by 8 the kernels take).
 //
 // s_out[bh][i][j] = scale * <qc[bh][i], kc[bh][col(j)]> for i < rows, j < n,
-// col(j) = kv_blk ? kv_blk[bh * n + j] : col0 + j. 128 x 64 output tiles, 256
-// threads, 8 x 4 outputs x 2 lanes per thread; d staged 8 at a time (= one
-// numpy group). grid (ceil(n/64), ceil(rows/128), BH).
+// col(j) = kv_blk ? kv_blk[bh * n + j] : col0 + j. 64 x 64 output tile per
+// CTA, 128 threads = 64 thread PAIRS: the two threads of a pair own the same
+// 8 x 8 outputs, the even one numpy's lane 0 (even d), the odd one lane 1
+// (odd d), each a sequential FMA chain; the pair adds its lanes through one
+// shuffle at the end. 64 accumulators per thread and 16 operand loads per 64
+// DFMA (2 B/DFMA of shared-memory traffic: the SM's LDS bandwidth at the DFMA
+// rate); 2 CTAs (8 warps) per SM at 206 registers (3 CTAs spill: 384 vs
+// 342 us at cfg3; 4 CTAs: 1618 us). d is staged 8 at a time (= one numpy
+// group) in two alternating shared stages (one barrier per group); row strides
+// padded so a pair's two d rows sit in disjoint banks.
+// grid (ceil(n/64), ceil(rows/64), BH).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 1) coarse_np_kernel(const float* __restrict__ qc, long long q_hstride,
+constexpr int kCnS = 72;  // stage row stride (doubles): +16 banks per d row
+#ifndef ISA_COARSE_MINB
+#define ISA_COARSE_MINB 2
+#endif
+__global__ void __launch_bounds__(128, ISA_COARSE_MINB) coarse_np_kernel(const float* __restrict__ qc, long long q_hstride,
                                                            const float* __restrict__ kc, long long k_hstride,
                                                            const int* __restrict__ kv_blk, int col0, int rows, int n,
                                                            int D, double scale, double* __restrict__ s_out) {
-  __shared__ double As[8][128];
-  __shared__ double Bs[8][64];
+  __shared__ __align__(16) double As[2][8][kCnS];
+  __shared__ __align__(16) double Bs[2][8][kCnS];
   __shared__ int colrow[64];
   const int bh = blockIdx.z;
-  const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 64;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
   const float* qb = qc + (long long)bh * q_hstride;
   const float* kb = kc + (long long)bh * k_hstride;
   if (threadIdx.x < 64) {
@@ -161,60 +173,62 @@ __global__ void __launch_bounds__(256, 1) coarse_np_kernel(const float* __restri
     colrow[threadIdx.x] = j < n ? (kv_blk ? kv_blk[(long long)bh * n + j] : col0 + j) : -1;
   }
   __syncthreads();
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc0[8][4], acc1[8][4];
+  const int lane = threadIdx.x & 1, pair = threadIdx.x >> 1;
+  const int ty = pair >> 3, tx = pair & 7;  // rows ty + 8 r, cols tx + 8 c
+  double acc[8][8];
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc0[r][c] = acc1[r][c] = 0.0;
-  // loaders: A = 128 rows x 8 d (thread -> row tid/2, 4 d); B = 64 rows x 8 d (threads < 128)
+    for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+  // loaders: thread -> row tid/2 (of 64), 4 consecutive d, for both operands;
+  // group g+1 is fetched into registers before group g's FMAs
   const int lr = threadIdx.x >> 1, ld = (threadIdx.x & 1) * 4;
-  const int gi = i0 + lr;
+  const int gi = i0 + lr, gj = colrow[lr];
   const float* arow = gi < rows ? qb + (long long)gi * D + ld : nullptr;
-  const int gj = threadIdx.x < 128 ? colrow[lr] : -1;
   const float* brow = gj >= 0 ? kb + (long long)gj * D + ld : nullptr;
   const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow)) : zero4;
   float4 b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow)) : zero4;
-  for (int d0 = 0; d0 < D; d0 += 8) {
-    As[ld + 0][lr] = a4.x; As[ld + 1][lr] = a4.y; As[ld + 2][lr] = a4.z; As[ld + 3][lr] = a4.w;
-    if (threadIdx.x < 128) {
-      Bs[ld + 0][lr] = b4.x; Bs[ld + 1][lr] = b4.y; Bs[ld + 2][lr] = b4.z; Bs[ld + 3][lr] = b4.w;
+  auto stage_in = [&](int buf) {
+    As[buf][ld + 0][lr] = a4.x; As[buf][ld + 1][lr] = a4.y; As[buf][ld + 2][lr] = a4.z; As[buf][ld + 3][lr] = a4.w;
+    Bs[buf][ld + 0][lr] = b4.x; Bs[buf][ld + 1][lr] = b4.y; Bs[buf][ld + 2][lr] = b4.z; Bs[buf][ld + 3][lr] = b4.w;
+  };
+  stage_in(0);
+  __syncthreads();
+  const int G = D / 8;
+  for (int g = 0; g < G; ++g) {
+    const int buf = g & 1;
+    if (g + 1 < G) {
+      a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow + 8 * (g + 1))) : zero4;
+      b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow + 8 * (g + 1))) : zero4;
     }
-    __syncthreads();
-    if (d0 + 8 < D) {
-      a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow + d0 + 8)) : zero4;
-      b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow + d0 + 8)) : zero4;
-    }
 #pragma unroll
-    for (int m = 3; m >= 0; --m) {  // numpy's chain order a3, a2, a1, a0
+    for (int m = 3; m >= 0; --m) {  // numpy's chain order a3, a2, a1, a0 within the group
+      const int dd = 2 * m + lane;
+      double bv[8];
 #pragma unroll
-      for (int lane = 0; lane < 2; ++lane) {
-        const int dd = 2 * m + lane;
-        double a[8], bv[4];
+      for (int t = 0; t < 8; ++t) bv[t] = Bs[buf][dd][tx + 8 * t];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) a[t] = As[dd][ty + 16 * t];
+      for (int r = 0; r < 8; ++r) {
+        const double a = As[buf][dd][ty + 8 * r];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) bv[t] = Bs[dd][tx + 16 * t];
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            if (lane == 0) acc0[r][c] = fma(a[r], bv[c], acc0[r][c]);
-            else acc1[r][c] = fma(a[r], bv[c], acc1[r][c]);
-          }
+        for (int c = 0; c < 8; ++c) acc[r][c] = fma(a, bv[c], acc[r][c]);
       }
     }
+    if (g + 1 < G) stage_in(buf ^ 1);
     __syncthreads();
   }
+  // dot = 0 + (lane0 + lane1); the even thread stores columns c < 4, the odd one c >= 4
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const int i = i0 + ty + 16 * r;
-    if (i >= rows) continue;
+    const int i = i0 + ty + 8 * r;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = j0 + tx + 16 * c;
-      if (j < n) s_out[((long long)bh * rows + i) * n + j] = scale * __dadd_rn(0.0, __dadd_rn(acc0[r][c], acc1[r][c]));
+    for (int c = 0; c < 8; ++c) {
+      const double other = __shfl_xor_sync(0xffffffffu, acc[r][c], 1);
+      const double dot = lane ? __dadd_rn(other, acc[r][c]) : __dadd_rn(acc[r][c], other);
+      const int j = j0 + tx + 8 * c;
+      if ((c >> 2) == lane && i < rows && j < n)
+        s_out[((long long)bh * rows + i) * n + j] = scale * __dadd_rn(0.0, dot);
     }
   }
 }
@@ -226,7 +240,7 @@ __global__ void __launch_bounds__(256, 1) coarse_np_kernel(const float* __restri
 // t_src. `s_ctx` holds the t_src x t_ctx scores from coarse_np_kernel (same
 // bits as the reference's s_coarse), so the means are bit-identical too.
 // Element (bh, i, c) at s + bh * head_stride + i * row_stride + c. Thread per
-// context column; 8 rows of loads in flight. grid (ceil(t_ctx/128), BH).
+// context column. grid (ceil(t_ctx/128), BH).
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) ctx_mean_kernel(const double* __restrict__ s, long long head_stride,
                                                        long long row_stride, int t_src, int t_ctx,
@@ -234,14 +248,26 @@ __global__ void __launch_bounds__(128) ctx_mean_kernel(const double* __restrict_
   const int c = blockIdx.x * 128 + threadIdx.x, bh = blockIdx.y;
   if (c >= t_ctx) return;
   const double* col = s + (long long)bh * head_stride + c;
+  // the sum is one dependent chain per column: keep 2 x 16 rows of loads in
+  // flight (the next batch is fetched while the current one is added)
+  constexpr int kU = 16;
   double acc = col[0];
+  double v[kU], w[kU];
   int i = 1;
-  for (; i + 8 <= t_src; i += 8) {
-    double v[8];
+  const int full = 1 + ((t_src - 1) / kU) * kU;  // rows [1, full) come in batches of kU
+  if (i < full) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = col[(long long)(i + u) * row_stride];
+    for (int u = 0; u < kU; ++u) v[u] = col[(long long)(i + u) * row_stride];
+  }
+  for (; i < full; i += kU) {
+    if (i + kU < full) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc += v[u];
+      for (int u = 0; u < kU; ++u) w[u] = col[(long long)(i + kU + u) * row_stride];
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc += v[u];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) v[u] = w[u];
   }
   for (; i < t_src; ++i) acc += col[(long long)i * row_stride];
   ctx[(long long)bh * t_ctx + c] = acc / static_cast<double>(t_src);

@@ -4,16 +4,23 @@ Every ISA stage is per (batch, head) — coarse scores, selection, split, mask
 and both attention branches (coarse.py:5-6; every reference loop
 is `for bi: for hi:`, e.g. reference.py:159-160, taylor.py:176-177) — so heads
 shard with no exchange during compute. Heads are assigned round-robin (rank r
-owns heads r, r+P, r+2P, ...), so the c-th chunked all-gather (head c*P + r
+owns heads r, r+P, r+2P, ...), so the all-gather of local head c (head c*P + r
 from every rank r) lands as one contiguous [c*P, (c+1)*P) head slab of the
-final (1, H, S, D) output: no permute copy. The only collective is the NCCL
-all-gather over NVLink that reassembles the output; chunk c's all-gather runs
-on a side stream while chunk c+1 computes.
+final (1, H, S, D) output: no permute copy. The only collective is that NCCL
+all-gather over NVLink, which reassembles the output.
+
+`ShardedIsa` overlaps it with compute: the local heads are cut into chunks,
+each chunk is a prepared ISA call (own workspace and output) on one of two
+compute streams (alternating, so chunk c+1's routing kernels start under the
+tail of chunk c's attention grid), and chunk c's all-gathers run on a
+communication stream as soon as chunk c's event fires, while chunk c+1
+computes. The same schedule code drives the CPU (gloo) tests through a
+stream adapter whose "streams" execute inline.
 """
 
 from __future__ import annotations
 
-from typing import List, Optional
+from typing import Callable, List, Optional
 
 import torch
 import torch.distributed as dist
@@ -31,21 +38,37 @@ def local_heads(x: torch.Tensor, rank: int, world: int) -> torch.Tensor:
     return x[:, rank::world]
 
 
+def chunk_ranges(n_local: int, chunk_heads: int) -> List[range]:
+    """Local head index ranges of the compute/gather chunks."""
+    if chunk_heads < 1:
+        raise ValueError("chunk_heads must be >= 1")
+    return [range(c, min(c + chunk_heads, n_local)) for c in range(0, n_local, chunk_heads)]
+
+
+def gather_slab(out_chunk: torch.Tensor, first_local: int, out_full: torch.Tensor, world: int, group=None) -> None:
+    """All-gather the local heads of one chunk (out_chunk (1, m, S, D), local
+    heads first_local .. first_local + m - 1) into out_full: local head c of
+    every rank is the contiguous slab out_full[0, c*P:(c+1)*P], viewed as
+    (P*S, D) — NCCL and gloo both take it, so the CPU tests run this path."""
+    S, D = out_chunk.shape[2], out_chunk.shape[3]
+    for j in range(out_chunk.shape[1]):
+        c = first_local + j
+        dist.all_gather_into_tensor(out_full[0, c * world:(c + 1) * world].view(world * S, D),
+                                    out_chunk[0, j].contiguous().view(S, D), group=group)
+
+
 def gather_heads(out_local: torch.Tensor, out_full: torch.Tensor, world: int, group=None,
                  chunks: Optional[List[int]] = None) -> None:
     """All-gather head shards into out_full (B, H, S, D) (round-robin layout).
 
-    B == 1 with H % P == 0: one all_gather_into_tensor per local head chunk c
-    straight into the contiguous slab out_full[0, c*P:(c+1)*P] (viewed as the
-    concatenation (P*S, D), which NCCL and gloo both accept, so the CPU gloo
-    tests run this exact path). Otherwise a generic all_gather of shards
-    padded to ceil(H/P) heads and a strided scatter (uneven head counts, B > 1)."""
+    B == 1 with H % P == 0 and a contiguous out_full: per-local-head slabs
+    (gather_slab). Otherwise a generic all_gather of shards padded to
+    ceil(H/P) heads and a strided scatter (uneven head counts, B > 1)."""
     B, Hl, S, D = out_local.shape
     H = out_full.shape[1]
     if B == 1 and out_full.is_contiguous() and H % world == 0:
         for c in (chunks if chunks is not None else range(Hl)):
-            dist.all_gather_into_tensor(out_full[0, c * world:(c + 1) * world].view(world * S, D),
-                                        out_local[0, c].contiguous(), group=group)
+            gather_slab(out_local[:, c:c + 1], c, out_full, world, group)
         return
     h_max = -(-H // world)
     send = out_local
@@ -58,35 +81,120 @@ def gather_heads(out_local: torch.Tensor, out_full: torch.Tensor, world: int, gr
         out_full[:, r::world] = parts[r][:, :n_r]
 
 
-def isa_forward_sharded(prepared, out_full: torch.Tensor, my_heads: List[int], world: int, group=None,
-                        comm_stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
-    """One ISA layer over this rank's heads (a `pipeline.prepare()`d call on the
-    local (1, H/P, S, D) inputs), then the head all-gather into `out_full`.
+# ---------------------------------------------------------------- stream adapters
+class CudaStreams:
+    """Two compute streams (alternating per chunk) and one comm stream, joined
+    with the caller's current stream at the start and end of a step."""
 
-    The gather is issued on `comm_stream` (created on demand) after an event on
-    the compute stream, so NCCL traffic overlaps whatever the caller enqueues
-    next; the function returns after enqueuing and makes the compute stream
-    wait for the gather."""
-    out_local = prepared()
-    if world == 1:
-        out_full.copy_(out_local)
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self.compute = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)]
+        self.comm = torch.cuda.Stream(self.device)
+
+    def begin(self):
+        self.main = torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(self.main)
+        for s in (*self.compute, self.comm):
+            s.wait_event(ev)
+
+    def run(self, i: int, fn: Callable[[], None]):
+        s = self.compute[i % 2]
+        with torch.cuda.stream(s):
+            fn()
+        ev = torch.cuda.Event()
+        ev.record(s)
+        return ev
+
+    def after(self, ev, fn: Callable[[], None]) -> None:
+        self.comm.wait_event(ev)
+        with torch.cuda.stream(self.comm):
+            fn()
+
+    def end(self):
+        for s in (*self.compute, self.comm):
+            self.main.wait_stream(s)
+
+
+class InlineStreams:
+    """CPU stand-in: every 'stream' executes inline, in issue order (gloo tests)."""
+
+    def begin(self):
+        pass
+
+    def run(self, i: int, fn):
+        fn()
+        return None
+
+    def after(self, ev, fn):
+        fn()
+
+    def end(self):
+        pass
+
+
+# ---------------------------------------------------------------- the sharded layer
+class ShardedIsa:
+    """One ISA layer over this rank's heads with the chunked, overlapped
+    output all-gather.
+
+    q/k/v: this rank's (1, H/P, S, D) inputs (heads head_shard(H, rank, P)).
+    `compute(lo, hi)` (optional) replaces the prepared ISA call for local
+    heads [lo, hi) and returns their (1, hi-lo, S, D) output — the CPU tests
+    use it; on CUDA each chunk is a `pipeline.prepare()`d call.
+    """
+
+    def __init__(self, q, k, v, icl, cfg, world: int, group=None, chunk_heads: int = 1,
+                 compute: Optional[Callable[[int, int], torch.Tensor]] = None, streams=None):
+        self.world, self.group = world, group
+        self.shape = tuple(q.shape)
+        if self.shape[0] != 1:
+            raise ValueError("ShardedIsa takes B = 1 (the head-sharded north-star layout)")
+        self.chunks = chunk_ranges(self.shape[1], chunk_heads)
+        if compute is None:
+            from .pipeline import prepare
+
+            preps = [prepare(q[:, r.start:r.stop], k[:, r.start:r.stop], v[:, r.start:r.stop], icl, cfg)
+                     for r in self.chunks]
+            self._calls = [p.__call__ for p in preps]
+            self._outs = [p.out for p in preps]
+        else:
+            self._outs = [None] * len(self.chunks)
+
+            def host_call(i, r):
+                def call():
+                    self._outs[i] = compute(r.start, r.stop)
+                return call
+
+            self._calls = [host_call(i, r) for i, r in enumerate(self.chunks)]
+        self.streams = streams or (CudaStreams(q.device) if q.is_cuda else InlineStreams())
+
+    def __call__(self, out_full: torch.Tensor, gather: bool = True) -> torch.Tensor:
+        """Compute every chunk and (gather=True) all-gather it into out_full
+        (1, H, S, D), chunk c's gather overlapping chunk c+1's compute.
+        gather=False runs the compute schedule alone (scaling without the
+        collective). Returns out_full; the caller's stream is ordered after
+        all of it."""
+        n_local = self.shape[1]
+        if tuple(out_full.shape[2:]) != self.shape[2:] or out_full.shape[1] != n_local * self.world:
+            raise ValueError(f"out_full {tuple(out_full.shape)} must be (1, {n_local * self.world}, S, D): "
+                             "the slab gather needs H divisible by the world size")
+        st = self.streams
+        st.begin()
+        for i, r in enumerate(self.chunks):
+            ev = st.run(i, self._calls[i])
+            if gather and self.world > 1:
+                st.after(ev, lambda i=i, r=r: gather_slab(self._outs[i], r.start, out_full, self.world, self.group))
+            elif gather:
+                st.after(ev, lambda i=i, r=r: out_full[:, r.start:r.stop].copy_(self._outs[i]))
+        st.end()
         return out_full
-    compute = torch.cuda.current_stream()
-    comm = comm_stream or _comm_stream(out_local.device)
-    ev = torch.cuda.Event()
-    ev.record(compute)
-    comm.wait_event(ev)
-    with torch.cuda.stream(comm):
-        gather_heads(out_local, out_full, world, group)
-    compute.wait_stream(comm)
-    return out_full
+
+    def local_output(self) -> List[torch.Tensor]:
+        return list(self._outs)
 
 
-_COMM = {}
-
-
-def _comm_stream(device) -> torch.cuda.Stream:
-    key = str(device)
-    if key not in _COMM:
-        _COMM[key] = torch.cuda.Stream(device=device)
-    return _COMM[key]
+def isa_forward_sharded(q, k, v, icl, cfg, out_full: torch.Tensor, world: int, group=None,
+                        chunk_heads: int = 1) -> torch.Tensor:
+    """One-shot convenience: ShardedIsa over this rank's (1, H/P, S, D) heads."""
+    return ShardedIsa(q, k, v, icl, cfg, world, group, chunk_heads)(out_full)
