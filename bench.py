@@ -207,9 +207,10 @@ def run_ours(args, rank, world, local_rank):
 
     out_full = torch.empty((1, H, S, D), dtype=torch.bfloat16, device=dev) if world > 1 else None
     prep = P.prepare(q, k, v, icl, cfg)
-    # N > 1: chunked schedule, one local head per chunk on two alternating
-    # compute streams, chunk c's NCCL all-gather under chunk c+1's compute
-    sharded = ShardedIsa(q, k, v, icl, cfg, world) if world > 1 else None
+    # N > 1: one fused call over the local heads publishing per-head completion;
+    # head c's NCCL all-gather waits on its counter and runs under the later heads
+    shard_mode = os.environ.get("ISA_SHARD_MODE", "signal")
+    sharded = ShardedIsa(q, k, v, icl, cfg, world, mode=shard_mode) if world > 1 else None
 
     # per-kernel CUDA events recorded by the C ABI inside every timed step
     # (N = 1): the stage / roofline durations come from the timed region itself
@@ -351,10 +352,10 @@ def run_ours(args, rank, world, local_rank):
         "stage_ms": stage,
         "step_ms_stats": step_stats,
         "sharded": None if world == 1 else {
-            "compute_only_ms": compute_only_ms, "heads_per_rank": Hl, "chunk_heads": 1,
+            "compute_only_ms": compute_only_ms, "heads_per_rank": Hl, "schedule": shard_mode,
             "gather_check": gather_ok, "backend": os.environ.get("ISA_BENCH_BACKEND", "nccl"),
-            "note": "value = max over ranks of the chunked compute + overlapped NCCL all-gather step; "
-                    "compute_only_ms = the same schedule without the gathers (max over ranks)"},
+            "note": "value = max over ranks of the step (compute + per-head NCCL all-gathers overlapped with "
+                    "it); compute_only_ms = the same schedule without the gathers (max over ranks)"},
         "gpu_launches": launches * args.steps,
         "roofline": {
             "kernel": "gba_isa_hybrid_kernel<128> (K6 sharp items + per-head K7T / K7 Taylor items, one launch)",

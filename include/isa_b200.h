@@ -148,6 +148,20 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
                 void* out, void* workspace, size_t workspace_bytes, const IsaRoutingIn* pinned,
                 IsaRoutingOut* routing, int32_t* err_word, const IsaEvents* events, void* stream);
 
+/* isa_forward (computed routing, no trace) that also publishes per-head
+ * completion for multi-GPU overlap: head_done (device int32 [B*H], zeroed
+ * once by the caller, never reset) grows by *done_inc per call for every
+ * head, the increments landing as that head's output rows become final (the
+ * fused attention grid counts its CTAs per head in-kernel). A comm stream
+ * then waits with isa_stream_wait_geq(comm, head_done + h, calls * inc)
+ * before moving head h (parallel.py). *done_inc is written on the host. */
+int isa_forward_signal(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
+                       void* out, void* workspace, size_t workspace_bytes, int32_t* err_word, int32_t* head_done,
+                       int32_t* done_inc, void* stream);
+
+/* Stream-ordered wait until *addr >= value (cuStreamWaitValue32 GEQ). */
+int isa_stream_wait_geq(void* stream, const int32_t* addr, int32_t value);
+
 /* Host-streamed pipeline: q/k/v/out are HOST pointers (contiguous (B,H,S,D);
  * page-locked for copy/compute overlap). The flattened (b,h) range is processed
  * in chunks of `heads_per_chunk` heads (<= 0: about 150 MB of inputs); the H2D copy of

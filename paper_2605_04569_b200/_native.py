@@ -43,6 +43,8 @@ EXPORTED_SYMBOLS = (
     "isa_cross_attention",
     "isa_coarse_scores",
     "isa_ctx_saliency_f64",
+    "isa_forward_signal",
+    "isa_stream_wait_geq",
 )
 
 # IsaKnobs.flags
@@ -139,6 +141,9 @@ _SIGS = {
     "isa_topk_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _I, _P]),
     "isa_sharpness_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P]),
     "isa_split_rows_f64": (ctypes.c_int, [_P, _I, _I, _I, _P, _P, _P]),
+    "isa_forward_signal": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs), _P, _P, _P, _P, _P,
+                                          ctypes.c_size_t, _P, _P, ctypes.POINTER(ctypes.c_int32), _P]),
+    "isa_stream_wait_geq": (ctypes.c_int, [_P, _P, _I]),
     "isa_coarse_scores": (ctypes.c_int, [_I, _I, _I, _I, ctypes.c_double, _P, _P, _P, _P]),
     "isa_ctx_saliency_f64": (ctypes.c_int, [_P, _I, ctypes.c_int64, ctypes.c_int64, _I, _I, _P, _P]),
     "isa_backward_workspace_bytes": (ctypes.c_int, [ctypes.POINTER(IsaShape), ctypes.POINTER(IsaKnobs),

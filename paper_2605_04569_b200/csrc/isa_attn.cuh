@@ -70,6 +70,10 @@ struct AttnParams {
   // transposed Taylor kernel (isa_taylor_t.cuh): exact K_new lists [BH][n_qblk][kmask]
   const int* mask;
   int kmask;
+  // per-head completion counters [BH] (multi-GPU overlap, isa_forward_signal):
+  // every CTA of the hybrid grid adds 1 to its head's counter after its
+  // output stores are visible device-wide; null = off
+  int* head_done;
 };
 
 #ifndef ISA_TRACE_Q

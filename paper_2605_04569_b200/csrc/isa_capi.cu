@@ -709,7 +709,8 @@ namespace {
 // log2-domain softmax normaliser for the backward.
 int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, const void* q, const void* k,
                  const void* v, void* out, const Workspace& w, const IsaRoutingIn* pinned, IsaRoutingOut* routing,
-                 int32_t* err_word, const IsaEvents* events, float* lse, cudaStream_t st) {
+                 int32_t* err_word, const IsaEvents* events, float* lse, cudaStream_t st,
+                 int32_t* head_done = nullptr, int32_t* done_inc = nullptr) {
   int rc;
   record(events, 0, st);
   if ((rc = run_routing(shape, d, knobs, q, k, v, w, pinned, routing, err_word, events, st))) return rc;
@@ -765,8 +766,11 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
     // K6 + Taylor items in one grid (the short Taylor CTAs fill the tail of
     // the last K6 wave); per head the Taylor branch runs as K7T or, when the
     // paired exact lists overlap enough that the union tiles cost less, K7
+    ps.head_done = head_done;  // in-kernel per-head completion (every CTA of the grid counts)
+    if (done_inc) *done_inc = d.items_s + d.items_f + (pf.n_qblk + 1) / 2;
     if ((rc = launch_isa_hybrid(tq, tk, tv, tkc, tvc, ps, pf, d.items_s, d.items_f, w.taylor_pick, d.BH, st)))
       return rc;
+    head_done = nullptr;
     record(events, 4, st);
   } else if (taylor_t) {
     // K6 over the sharp blocks, then K7T over the flat ones (per-branch attribution)
@@ -787,6 +791,11 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
         return rc;
   }
   record(events, 5, st);
+  if (head_done) {  // separate launches: one stream-ordered increment per head after them
+    isa::head_bump_kernel<<<grid1d(d.BH, 128), 128, 0, st>>>(head_done, d.BH);
+    ISA_LAUNCHED("head_bump_kernel");
+    if (done_inc) *done_inc = 1;
+  }
   if (routing && routing->taylor_kernel) {  // which Taylor-branch kernel ran per head (test hook)
     if (taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES)) {
       ISA_CUDA(cudaMemcpyAsync(routing->taylor_kernel, w.taylor_pick, 4ull * d.BH, cudaMemcpyDeviceToDevice, st));
@@ -915,6 +924,43 @@ int isa_forward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, con
     return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, w.bytes);
   return forward_impl(shape, knobs, d, q, k, v, out, w, pinned, routing, err_word, events, nullptr,
                       static_cast<cudaStream_t>(stream));
+}
+
+int isa_forward_signal(const IsaShape* shape, const IsaKnobs* knobs, const void* q, const void* k, const void* v,
+                       void* out, void* workspace, size_t workspace_bytes, int32_t* err_word, int32_t* head_done,
+                       int32_t* done_inc, void* stream) {
+  g_launches = 0;
+  if (!head_done || !done_inc) return fail(ISA_ERR_CONFIG, "isa_forward_signal needs head_done and done_inc");
+  Dims d;
+  int rc = derive(shape, knobs, &d);
+  if (rc) return rc;
+  if ((rc = check_io(shape, q, k, v))) return rc;
+  if ((rc = check_out(shape, out))) return rc;
+  Workspace w = carve(d, shape->dtype, static_cast<uint8_t*>(workspace));
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(ISA_ERR_CONFIG, "workspace too small (%zu < %zu)", workspace_bytes, w.bytes);
+  return forward_impl(shape, knobs, d, q, k, v, out, w, nullptr, nullptr, err_word, nullptr, nullptr,
+                      static_cast<cudaStream_t>(stream), head_done, done_inc);
+}
+
+int isa_stream_wait_geq(void* stream, const int32_t* addr, int32_t value) {
+  using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static WaitFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitFn>(p);
+  });
+  if (!fn) return fail(ISA_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  // GEQ on a monotonically growing counter: no reset between steps, so a
+  // wait can never be satisfied by an earlier step's completions
+  CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr), (cuuint32_t)value,
+                  CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(ISA_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  return ISA_OK;
 }
 
 int isa_backward_workspace_bytes(const IsaShape* shape, const IsaKnobs* knobs, size_t* bytes) {

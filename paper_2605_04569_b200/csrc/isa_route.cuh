@@ -991,6 +991,16 @@ __global__ void __launch_bounds__(256) routing_check_kernel(const int64_t* __res
   if (bits) atomicOr(err, bits);
 }
 
+// Per-head completion counters when the attention ran as separate launches:
+// stream-ordered after them, one increment per head.
+__global__ void head_bump_kernel(int* __restrict__ head_done, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    __threadfence();
+    atomicAdd(head_done + i, 1);
+  }
+}
+
 __global__ void fill_i32_kernel(int* __restrict__ out, int v, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     out[i] = v;

@@ -592,6 +592,11 @@ __global__ void __launch_bounds__(kTThreads, 1)
   } else {
     if (__ldg(pick + bh) == 1) taylor_t_body<D>(tm_q, tm_k, tm_v, tm_kc, tm_vc, pt, x - n_exact - n_k7, bh);
   }
+  if (pe.head_done) {  // head bh's output rows of this CTA are final: publish (release) for the comm stream
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(pe.head_done + bh, 1);
+  }
 }
 
 }  // namespace isa

@@ -601,31 +601,54 @@ def apply_decoupled_rope(x, icl: IclLayout, base: float = 10000.0, *, out: Optio
     return out
 
 
-def prepare(q, k, v, icl, cfg, separate_branches: bool = False):
+def prepare(q, k, v, icl, cfg, separate_branches: bool = False, signal: bool = False):
     """Validated inputs + a reusable workspace for repeated calls (bench/CUDA graphs).
 
     separate_branches launches the exact and Taylor attention branches as two
-    kernels (per-branch profiling) instead of the default fused grid."""
+    kernels (per-branch profiling) instead of the default fused grid;
+    signal publishes per-head completion counters (see _Prepared)."""
     inp = _Inputs(q, k, v, icl, cfg)
     if separate_branches:
-        inp.knobs.flags |= 1
+        inp.knobs.flags |= N.FLAG_SEPARATE_BRANCHES
     ws, nbytes = inp.workspace()
-    return _Prepared(inp, ws, nbytes)
+    return _Prepared(inp, ws, nbytes, signal=signal)
 
 
 class _Prepared:
-    """Pre-validated call: no per-call allocation except nothing; graph-capturable."""
+    """Pre-validated call: no per-call allocation; graph-capturable.
 
-    def __init__(self, inp: _Inputs, ws, nbytes):
+    signal=True publishes per-head completion (isa_forward_signal): after
+    the n-th call, head_done[b*H + h] reaches n * done_inc once head h's output
+    rows are final; `wait_head(stream, h)` makes another stream wait for that
+    (the multi-GPU overlap in parallel.py)."""
+
+    def __init__(self, inp: _Inputs, ws, nbytes, signal: bool = False):
         self.inp, self.ws, self.nbytes = inp, ws, nbytes
         d = inp.dims
         self.out = torch.empty((d.B, d.H, d.S, d.D), dtype=inp.q.dtype, device=inp.q.device)
         self.err = torch.zeros(1, dtype=torch.int32, device=inp.q.device)
+        self.head_done = torch.zeros(d.B * d.H, dtype=torch.int32, device=inp.q.device) if signal else None
+        self.done_inc = ctypes.c_int32(0)
+        self.calls = 0
 
     def __call__(self, stream=None):
         inp = self.inp
         st = stream if stream is not None else torch.cuda.current_stream(inp.q.device).cuda_stream
+        if self.head_done is not None:
+            N.check(N.load().isa_forward_signal(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), _ptr(inp.q),
+                                                _ptr(inp.k), _ptr(inp.v), _ptr(self.out), _ptr(self.ws), self.nbytes,
+                                                _ptr(self.err), _ptr(self.head_done), ctypes.byref(self.done_inc),
+                                                st))
+            self.calls += 1
+            return self.out
         N.check(N.load().isa_forward(ctypes.byref(inp.shape), ctypes.byref(inp.knobs), _ptr(inp.q), _ptr(inp.k),
                                      _ptr(inp.v), _ptr(self.out), _ptr(self.ws), self.nbytes, None, None,
                                      _ptr(self.err), None, st))
         return self.out
+
+    def wait_head(self, stream, bh: int) -> None:
+        """Enqueue on `stream` a wait until head bh of the latest call is final."""
+        target = self.calls * self.done_inc.value
+        if target >= 2 ** 31:
+            raise OverflowError("head_done counter range exhausted; re-prepare")
+        N.check(N.load().isa_stream_wait_geq(stream.cuda_stream, self.head_done.data_ptr() + 4 * bh, target))

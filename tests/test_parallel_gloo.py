@@ -69,7 +69,7 @@ def test_head_sharded_gather_matches_single_process(world, H, B):
     assert all(ok for _, ok in res), res
 
 
-def _chunk_worker(rank, world, port, H, S, D, chunk_heads, q):
+def _chunk_worker(rank, world, port, H, S, D, chunk_heads, q, mode="chunks"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -84,27 +84,32 @@ def _chunk_worker(rank, world, port, H, S, D, chunk_heads, q):
             calls.append((lo, hi))
             return _per_head(x_local[:, lo:hi], mine[lo:hi])
 
-        layer = ShardedIsa(x_local, x_local, x_local, None, None, world, chunk_heads=chunk_heads, compute=compute)
+        layer = ShardedIsa(x_local, x_local, x_local, None, None, world, chunk_heads=chunk_heads, compute=compute,
+                           mode=mode)
         ok = True
         for step in range(2):  # the layer is reusable step after step
             out_full = torch.full((1, H, S, D), float("nan"))
             layer(out_full)
             ok &= bool(torch.equal(out_full, _per_head(full, list(range(H)))))
-        expect = [(r.start, r.stop) for r in chunk_ranges(len(mine), chunk_heads)] * 2
+        ranges = chunk_ranges(len(mine), chunk_heads) if mode == "chunks" else [range(len(mine))]
+        expect = [(r.start, r.stop) for r in ranges] * 2
         q.put((rank, ok and calls == expect))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,chunk_heads", [(2, 1), (4, 1), (8, 1), (4, 3), (8, 2)])
-def test_chunked_schedule_matches_single_process(world, chunk_heads):
-    """H = 40 (Wan-14B) over P = 2 / 4 / 8 ranks: 20 / 10 / 5 local heads in
-    chunks of 1-3, each chunk's slab all-gathers landing in the contiguous
-    [c*P, (c+1)*P) head slabs; bit-identical to the single-process layer."""
+@pytest.mark.parametrize("world,chunk_heads,mode", [(2, 1, "chunks"), (4, 1, "chunks"), (8, 1, "chunks"),
+                                                   (4, 3, "chunks"), (8, 2, "chunks"), (2, 1, "signal"),
+                                                   (4, 1, "signal"), (8, 1, "signal")])
+def test_chunked_schedule_matches_single_process(world, chunk_heads, mode):
+    """H = 40 (Wan-14B) over P = 2 / 4 / 8 ranks: 20 / 10 / 5 local heads,
+    computed in chunks of 1-3 ("chunks") or in one call with per-head slab
+    gathers ("signal"), each all-gather landing in the contiguous
+    [c*P, (c+1)*P) head slab; bit-identical to the single-process layer."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_chunk_worker, args=(r, world, port, 40, 8, 8, chunk_heads, q))
+    procs = [ctx.Process(target=_chunk_worker, args=(r, world, port, 40, 8, 8, chunk_heads, q, mode))
              for r in range(world)]
     for p in procs:
         p.start()
