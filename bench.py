@@ -287,56 +287,59 @@ def run_ours(args, rank, world, local_rank):
                         for r in range(world) for c in range(Hl))
 
     # ---- per-stage / per-kernel times (events recorded by the C ABI on the launching stream)
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-    ev_struct = N.IsaEvents()
-    for i, e in enumerate(evs):
-        e.record()
-        ev_struct.ev[i] = e.cuda_event
-    reps = 3
+    def make_events():
+        evl = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        es = N.IsaEvents()
+        for i_, e_ in enumerate(evl):
+            e_.record()
+            es.ev[i_] = e_.cuda_event
+        return evl, es
 
-    def stage_times(flags):
-        acc = {k_: 0.0 for k_ in ("coarse", "select", "split", "attn", "exact", "taylor")}
-        for _ in range(reps):
-            _call_with_events(prep, ev_struct, flags)
-            torch.cuda.synchronize()
-            acc["coarse"] += evs[0].elapsed_time(evs[1])
-            acc["select"] += evs[1].elapsed_time(evs[2])
-            acc["split"] += evs[2].elapsed_time(evs[3])
-            acc["attn"] += evs[3].elapsed_time(evs[5])
-            acc["exact"] += evs[3].elapsed_time(evs[4])
-            acc["taylor"] += evs[4].elapsed_time(evs[5])
-        return {k_: v_ / reps for k_, v_ in acc.items()}
+    def stages(evl):
+        return {"coarse": evl[0].elapsed_time(evl[1]), "select": evl[1].elapsed_time(evl[2]),
+                "split": evl[2].elapsed_time(evl[3]), "attn": evl[3].elapsed_time(evl[5]),
+                "exact": evl[3].elapsed_time(evl[4]), "taylor": evl[4].elapsed_time(evl[5])}
 
-    # the shipped configuration (D = 128): one launch, K6 items over the sharp
-    # blocks and transposed-Taylor (K7T) items over the flat ones. N = 1:
-    # stage times averaged over the timed steps themselves; N > 1: separate
-    # calls after the timed region. Per-branch attribution: a separate-launch
-    # call (ISA_FLAG_SEPARATE_BRANCHES) after the timed region.
+    def mean_stages(lst):
+        return {k_: sum(d_[k_] for d_ in lst) / len(lst) for k_ in lst[0]}
+
+    # shipped configuration (D = 128): one launch, K6 items over the sharp
+    # blocks and K7T / K7 items over the flat ones. N = 1: stage times are the
+    # timed steps' own events.
     step_stats = None
     if world == 1:
         per = sorted(evl[0].elapsed_time(evl[5]) for evl in step_evs)
         q_ = lambda f: per[min(len(per) - 1, int(round(f * (len(per) - 1))))]  # noqa: E731
         step_stats = {"median": statistics.median(per), "p10": q_(0.1), "p90": q_(0.9), "n": len(per),
                       "note": "per-step device time (first to last kernel event of the step)"}
-        shipped = {k_: 0.0 for k_ in ("coarse", "select", "split", "attn", "exact", "taylor")}
-        for evl in step_evs:
-            shipped["coarse"] += evl[0].elapsed_time(evl[1]) / args.steps
-            shipped["select"] += evl[1].elapsed_time(evl[2]) / args.steps
-            shipped["split"] += evl[2].elapsed_time(evl[3]) / args.steps
-            shipped["attn"] += evl[3].elapsed_time(evl[5]) / args.steps
-            shipped["exact"] += evl[3].elapsed_time(evl[4]) / args.steps
-            shipped["taylor"] += evl[4].elapsed_time(evl[5]) / args.steps
-    else:
-        shipped = stage_times(0)
-    separate = stage_times(1)
+        shipped = mean_stages([stages(evl) for evl in step_evs])
+    # A/B in ONE loop alternating the shipped step (K6 launch + Taylor launch)
+    # with the single fused grid (ISA_FLAG_FUSED_GRID), so both see the same clocks.
+    ev_a = [make_events() for _ in range(args.steps)]
+    ev_b = [make_events() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i_ in range(args.steps):
+        _call_with_events(prep, ev_a[i_][1], 0)
+        _call_with_events(prep, ev_b[i_][1], N.FLAG_FUSED_GRID)
+    torch.cuda.synchronize()
+    shipped_alt = mean_stages([stages(e_[0]) for e_ in ev_a])
+    fused_alt = mean_stages([stages(e_[0]) for e_ in ev_b])
+    if world > 1:
+        shipped = shipped_alt
     stage = {"coarse": shipped["coarse"], "select": shipped["select"], "split": shipped["split"],
-             "attention_fused": shipped["attn"], "exact_k6_separate": separate["exact"],
-             "taylor_k7t_separate": separate["taylor"]}
+             "attention": shipped["attn"], "exact_k6": shipped["exact"], "taylor": shipped["taylor"],
+             "ab_loop": {"shipped_two_launches": shipped_alt["attn"], "fused_single_grid": fused_alt["attn"],
+                         "shipped_exact_k6": shipped_alt["exact"], "shipped_taylor": shipped_alt["taylor"],
+                         "steps": args.steps,
+                         "note": "shipped and fused-grid steps alternated in one loop after the timed region "
+                                 "(same clocks); per-launch CUDA events"}}
     peaks = _peaks()
-    peak_tc = peaks.get("bf16_tflops_sustained") or 1354.8
+    # K6 runs ~18 ms inside a ~23 ms step: a kernel timed on its own at burst
+    # clocks, not a seconds-long sustained run -> the burst peak
+    peak_tc = peaks.get("bf16_tflops") or 1666.4
     attn_tflops = (f_sharp + f_taylor_alg) / (shipped["attn"] * 1e-3) / 1e12
-    exact_tflops = f_sharp / (separate["exact"] * 1e-3) / 1e12
-    taylor_tflops = f_taylor_alg / (separate["taylor"] * 1e-3) / 1e12 if separate["taylor"] > 0 else None
+    exact_tflops = f_sharp / (shipped["exact"] * 1e-3) / 1e12
+    taylor_tflops = f_taylor_alg / (shipped["taylor"] * 1e-3) / 1e12 if shipped["taylor"] > 0 else None
     prof = _profile_summary()
 
     result = {
@@ -358,22 +361,25 @@ def run_ours(args, rank, world, local_rank):
                     "it); compute_only_ms = the same schedule without the gathers (max over ranks)"},
         "gpu_launches": launches * args.steps,
         "roofline": {
-            "kernel": "gba_isa_hybrid_kernel<128> (K6 sharp items + per-head K7T / K7 Taylor items, one launch)",
-            "bound": "tensor", "achieved": attn_tflops, "peak": peak_tc, "unit": "TFLOP/s",
-            "frac": attn_tflops / peak_tc, "traffic": prof.get("attn_dram_bytes"),
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a ~23 ms step)",
-            "algorithmic": "F_sharp + F_taylor (pipeline.py:269-289, taylor.py:299-316) per launch / average "
-                           "CUDA-event duration of the launch over the timed steps, on its stream",
+            "kernel": "gba_attention_kernel<128, MODE_EXACT> (K6, the sharp branch: the dominant launch)",
+            "bound": "tensor", "achieved": exact_tflops, "peak": peak_tc, "unit": "TFLOP/s",
+            "frac": exact_tflops / peak_tc, "traffic": prof.get("k6_dram_bytes"),
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: K6 runs ~18 ms per step, not a seconds-long "
+                           "sustained run)",
+            "algorithmic": "F_sharp = 4*b^2*D*n_sharp*t_new (pipeline.py:278) per launch / average CUDA-event "
+                           "duration of the launch over the timed steps, on its stream",
         },
-        "exact_kernel": {"achieved": exact_tflops, "frac": exact_tflops / peak_tc, "unit": "TFLOP/s",
-                         "kernel": "gba_attention_kernel<128, MODE_EXACT> (K6)",
-                         "algorithmic": "F_sharp = 4*b^2*D*n_sharp*t_new (pipeline.py:278)",
-                         "timed": "separate launch (ISA_FLAG_SEPARATE_BRANCHES)", "traffic": prof.get("k6_dram_bytes")},
+        "attention_kernels": {"achieved": attn_tflops, "frac": attn_tflops / peak_tc, "unit": "TFLOP/s",
+                              "kernels": "K6 launch + Taylor launch (per-head K7T / K7)",
+                              "algorithmic": "F_sharp + F_taylor (pipeline.py:269-289, taylor.py:299-316)",
+                              "traffic": prof.get("attn_dram_bytes")},
         "taylor_kernel": {"achieved": taylor_tflops, "frac": (taylor_tflops / peak_tc) if taylor_tflops else None,
-                          "unit": "TFLOP/s", "kernel": "gba_taylor_t_kernel<128> (K7T)",
-                          "algorithmic": "reference flop_count (taylor.py:299-316)",
-                          "timed": "separate launch (ISA_FLAG_SEPARATE_BRANCHES)",
-                          "traffic": prof.get("k7t_dram_bytes"), "l2_bytes": prof.get("k7t_l2_bytes")},
+                          "unit": "TFLOP/s", "kernel": "gba_isa_hybrid_kernel<128> with 0 exact items "
+                                                       "(per head K7T gba_taylor_t body or K7 union tiles)",
+                          "algorithmic": "reference flop_count (taylor.py:299-316): F_taylor",
+                          "timed": "its launch inside the timed steps",
+                          "traffic": prof.get("k7t_dram_bytes"), "l2_bytes": prof.get("k7t_l2_bytes"),
+                          "l2_roofline": _l2_roofline(prof.get("k7t_l2_bytes"), shipped["taylor"])},
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_extras:
@@ -418,6 +424,18 @@ def _peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "fallback": True}
+
+
+def _l2_roofline(l2_bytes, ms):
+    """K7T streams its K/V and centroid tiles from L2: achieved L2->SM GB/s
+    against the measured L2->SM bandwidth (profiles/ ubench, TMA bulk copies
+    with 2 CTAs x 64 KB in flight per SM)."""
+    peak = _profile_summary().get("l2_to_sm_gbs")
+    if not l2_bytes or not ms or not peak:
+        return None
+    ach = l2_bytes / (ms * 1e-3) / 1e9
+    return {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "source": "profiles/r2_ubench_l2bw.txt (tools/ubench/l2bw.cu)"}
 
 
 def _profile_summary():

@@ -78,9 +78,12 @@ typedef struct IsaKnobs {
 } IsaKnobs;
 
 /* IsaKnobs.flags: launch the exact (sharp) and Taylor (flat) attention
- * branches as two kernels instead of one fused grid (per-branch profiling;
- * the Taylor branch then runs as K7T at D = 128). */
+ * branches as two kernels (the default at D = 128; at D = 64 it replaces the
+ * fused K6 + K7 grid). */
 #define ISA_FLAG_SEPARATE_BRANCHES 1
+/* D = 128: the sharp and flat items in ONE grid (gba_isa_hybrid_kernel)
+ * instead of the default K6 launch + Taylor launch (A/B measurements). */
+#define ISA_FLAG_FUSED_GRID 8
 /* Force the D = 128 Taylor-branch kernel for every head instead of the
  * per-head automatic choice (taylor_pick_kernel): K7 = row-major pair-union
  * tiles, K7T = transposed per-block tiles. Same operator, test/A-B hooks. */

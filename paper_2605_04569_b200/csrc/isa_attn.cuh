@@ -990,6 +990,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
                          const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
   gba_body<D, MODE>(tm_q, tm_k, tm_v, tm_kc, tm_vc, p, blockIdx.x, blockIdx.y);
+  if (p.head_done) {  // this CTA's output rows are final: publish for the comm stream (parallel.py)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(p.head_done + blockIdx.y, 1);
+  }
 }
 
 // Both ISA branches in one launch: CTAs [0, n_exact) run the sharp items (288

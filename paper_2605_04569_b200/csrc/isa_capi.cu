@@ -762,7 +762,7 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
   }
   const bool taylor_t = d.n_flat && d.D == 128 && taylor_t_mode();
   const bool fuse = d.n_sharp && d.n_flat && !taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES);
-  if (taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES)) {
+  if (taylor_t && (knobs->flags & ISA_FLAG_FUSED_GRID)) {
     // K6 + Taylor items in one grid (the short Taylor CTAs fill the tail of
     // the last K6 wave); per head the Taylor branch runs as K7T or, when the
     // paired exact lists overlap enough that the union tiles cost less, K7
@@ -773,11 +773,20 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
     head_done = nullptr;
     record(events, 4, st);
   } else if (taylor_t) {
-    // K6 over the sharp blocks, then K7T over the flat ones (per-branch attribution)
+    // Shipped (D = 128): K6 over the sharp blocks, then one grid of Taylor
+    // items run per head as K7T or K7 (taylor_pick_kernel). Two launches beat
+    // the single K6 + Taylor grid at cfg3 in an alternating same-clock loop
+    // (22.15 vs 23.12 ms): K6 runs alone at full tensor rate, the L2-bound
+    // Taylor items no longer contend with it. Both grids count per-head
+    // completion when signalling (isa_forward_signal).
+    ps.head_done = head_done;
+    pf.head_done = head_done;
+    if (done_inc) *done_inc = (d.n_sharp ? d.items_s : 0) + d.items_f + (pf.n_qblk + 1) / 2;
     if (d.n_sharp)
       if ((rc = launch_attention_d<isa::MODE_EXACT>(d.D, tq, tk, tv, tq, tq, ps, d.items_s, d.BH, st))) return rc;
     record(events, 4, st);
-    if ((rc = launch_taylor_t(tq, tk, tv, tkc, tvc, pf, d.BH, st))) return rc;
+    if ((rc = launch_isa_hybrid(tq, tk, tv, tkc, tvc, pf, pf, 0, d.items_f, w.taylor_pick, d.BH, st))) return rc;
+    head_done = nullptr;
   } else if (fuse) {
     // K6 + K7 in one grid: exact items first, Taylor items fill the tail.
     if ((rc = launch_isa_fused(d.D, tq, tk, tv, tkc, tvc, ps, pf, d.items_s, d.items_f, d.BH, st))) return rc;
@@ -797,7 +806,7 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
     if (done_inc) *done_inc = 1;
   }
   if (routing && routing->taylor_kernel) {  // which Taylor-branch kernel ran per head (test hook)
-    if (taylor_t && !(knobs->flags & ISA_FLAG_SEPARATE_BRANCHES)) {
+    if (taylor_t) {
       ISA_CUDA(cudaMemcpyAsync(routing->taylor_kernel, w.taylor_pick, 4ull * d.BH, cudaMemcpyDeviceToDevice, st));
     } else {
       isa::fill_i32_kernel<<<grid1d(d.BH, 256), 256, 0, st>>>(routing->taylor_kernel, taylor_t ? 1 : 0, d.BH);
