@@ -81,8 +81,24 @@ struct TTileSrc {
   int tok0, tok1, centroid;
 };
 
-// Tile i of stage (flat position) pos: exact pair (mask[2i], mask[2i+1]) or centroid tile i - n_ex.
-__device__ __forceinline__ TTileSrc tt_tile(const AttnParams& p, int bh, int pos, int i, int n_ex) {
+constexpr int kTTokRegs = 3;  // exact blocks resolved up front: k <= 32 * kTTokRegs (larger k: lookups per tile)
+
+// Token row of exact block j of a stage from the producer warp's registers
+// (lane j % 32 holds entry j in tok[j / 32]); every lane must participate.
+__device__ __forceinline__ int tt_tok(const int (&tok)[kTTokRegs], int j) {
+  int v = tok[0];
+#pragma unroll
+  for (int r = 1; r < kTTokRegs; ++r)
+    if ((j >> 5) == r) v = tok[r];
+  return __shfl_sync(0xffffffffu, v, j & 31);
+}
+
+// Tile i of stage (flat position) pos: exact pair (mask[2i], mask[2i+1]) or
+// centroid tile i - n_ex. With `tok` the stage's exact blocks were resolved
+// once before the loop (mask -> K_new block table -> token row), so the
+// producer issues loads without dependent global lookups.
+__device__ __forceinline__ TTileSrc tt_tile(const AttnParams& p, int bh, int pos, int i, int n_ex, bool table,
+                                            const int (&tok)[kTTokRegs]) {
   TTileSrc t;
   if (i >= n_ex) {
     t.centroid = 1;
@@ -91,6 +107,11 @@ __device__ __forceinline__ TTileSrc tt_tile(const AttnParams& p, int bh, int pos
     return t;
   }
   t.centroid = 0;
+  if (table) {
+    t.tok0 = tt_tok(tok, 2 * i);
+    t.tok1 = tt_tok(tok, 2 * i + 1 < p.kmask ? 2 * i + 1 : 2 * i);
+    return t;
+  }
   const int* mrow = p.mask + ((long long)bh * p.n_qblk + pos) * p.kmask;
   const int* tab = p.kv_blk + (long long)bh * p.t_new;
   const int j0 = __ldg(mrow + 2 * i);
@@ -182,6 +203,18 @@ __device__ __forceinline__ void taylor_t_body(const CUtensorMap& tm_q, const CUt
             tma_load_4d(sQ + s * L::kQStage + pl * 8192, &tm_q, &q_full[s], pl * 64, tok, hh, bb, pol_q);
         }
       }
+      int tokr[2][kTTokRegs];
+      const bool table = p.kmask <= 32 * kTTokRegs;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int* mrow = p.mask + ((long long)bh * p.n_qblk + pos[s]) * p.kmask;
+        const int* tab = p.kv_blk + (long long)bh * p.t_new;
+#pragma unroll
+        for (int r = 0; r < kTTokRegs; ++r) {
+          const int j = 32 * r + lane;
+          tokr[s][r] = (table && j < p.kmask) ? blk_tok0(p, __ldg(tab + __ldg(mrow + j))) : 0;
+        }
+      }
       int c = 0;
       auto push = [&](const TTileSrc& t, int is_v) {
         const int slot = c % kTKvStages;
@@ -208,12 +241,12 @@ __device__ __forceinline__ void taylor_t_body(const CUtensorMap& tm_q, const CUt
       for (int i = 0; i < 2 && i < n_kv; ++i)
 #pragma unroll
         for (int s = 0; s < 2; ++s)
-          if (own(i, s)) push(tt_tile(p, bh, pos[s], i, n_ex), 0);
+          if (own(i, s)) push(tt_tile(p, bh, pos[s], i, n_ex, table, tokr[s]), 0);
       for (int i = 0; i < n_kv; ++i) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-          if (own(i, s)) push(tt_tile(p, bh, pos[s], i, n_ex), 1);
-          if (i + 2 < n_kv && own(i + 2, s)) push(tt_tile(p, bh, pos[s], i + 2, n_ex), 0);
+          if (own(i, s)) push(tt_tile(p, bh, pos[s], i, n_ex, table, tokr[s]), 1);
+          if (i + 2 < n_kv && own(i + 2, s)) push(tt_tile(p, bh, pos[s], i + 2, n_ex, table, tokr[s]), 0);
         }
       }
     } else if (warp == 8) {

@@ -66,6 +66,24 @@ def run(args):
     torch.cuda.synchronize()
     buf = np.zeros((96, 2, 8), dtype=np.int64)
     N.check(lib.isa_debug_trace_copy(buf.ctypes.data, buf.nbytes))
+    if args.k7t:  # one query block per CTA (isa_taylor_t.cuh): stage 0 only
+        t = buf[:, 0] - buf[0, 0, 0]
+        print("tile |  S_rdy  ld  chk  exp+st  arrive | mma_see(P_i) V_taken QK(i+2)_issued | tile_dt")
+        n = int((buf[:, 0, 0] != 0).sum())
+        for i in range(n):
+            a = t[i]
+            m = t[i + 1] if i + 1 < 96 else np.zeros(8, dtype=np.int64)
+            dt = t[i + 1, 0] - a[0] if i + 1 < n else 0
+            print(f"{i:4d} | {a[0]:7d} {a[1]-a[0]:4d} {a[2]-a[1]:4d} {a[3]-a[2]:6d} {a[4]-a[3]:6d} |"
+                  f" {m[6]-a[4]:8d} {m[5]-m[6]:7d} {m[7]-m[5]:8d} | {dt:6d}")
+        print(f"CTA span: {t[n - 1, 4]} clk for {n} tiles ({t[n - 1, 4] / max(n, 1):.0f} clk/tile)")
+        u = buf[:, 1] - buf[0, 0, 0]
+        print("tile | prodK_issue prodV_issue | PV_issued K_taken  (MMA warp, relative to V_taken of tile i)")
+        for i in range(n):
+            m = t[i + 1] if i + 1 < 96 else np.zeros(8, dtype=np.int64)
+            w = u[i + 1] if i + 1 < 96 else np.zeros(8, dtype=np.int64)
+            print(f"{i:4d} | {u[i, 4]:9d} {u[i, 5]:9d} | {w[0] - m[5]:8d} {w[1] - m[5]:8d}   Ktile(i+2) issued at {u[i + 2, 4] if i + 2 < 96 else 0}")
+        return
     t = buf - buf[1, 0, 0]
     print("step st |  S_rdy   ld  exps st_wait  S->P(arrive) | mma_see issue | S_rdy(i+1)-issue | step_dt")
     for i in range(args.first, min(args.first + args.n, 95)):
@@ -106,6 +124,7 @@ if __name__ == "__main__":
     ap.add_argument("--first", type=int, default=20)
     ap.add_argument("--isa", action="store_true", help="trace an isa_forward (separate branches) instead of dense")
     ap.add_argument("--n", type=int, default=24)
+    ap.add_argument("--k7t", action="store_true", help="print the one-block-per-CTA K7T layout (use with --isa)")
     a = ap.parse_args()
     if a.build:
         build(a.cta, a.variant)
