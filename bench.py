@@ -37,7 +37,23 @@ WORKLOAD = dict(workload="cfg3: ISA attention layer, Wan-14B shape, 32K source +
                 batch=1, heads=40, head_dim=128, l_src=32768, l_ctx=32768, block=64,
                 alpha_s=0.125, alpha_ns=0.0625, alpha_f=0.5,
                 inputs="iid N(0,1) bf16 drawn per head h on the GPU (torch.Generator seed 1000 + h; Q, K, V "
-                       "in that order: bench.synth_qkv); 2 GB of Q/K/V > 126 MB L2 (no flush needed)")
+                       "in that order: bench.synth_qkv)")
+
+
+# BASELINE.json configs: the metric is quoted on cfg3 (the default); the others
+# run through the same harness with --config (cfg4-grid adds the knob sweep).
+CONFIGS = {
+    "cfg1": dict(workload="cfg1: the reference's CPU-runnable case (B=1, H=2, d=64, 1024 + 1024 tokens)",
+                 heads=2, head_dim=64, l_src=1024, l_ctx=1024),
+    "cfg2": dict(workload="cfg2: single ISA layer, Wan-14B shape, 8K source + 8K context",
+                 heads=40, head_dim=128, l_src=8192, l_ctx=8192),
+    "cfg3": dict(workload=WORKLOAD["workload"], heads=40, head_dim=128, l_src=32768, l_ctx=32768),
+    "cfg4": dict(workload="cfg4: ISA layer at 16K source + 16K context (default knobs; cfg4-grid sweeps "
+                          "alpha_s x alpha_f against dense)", heads=40, head_dim=128, l_src=16384, l_ctx=16384),
+    "cfg5": dict(workload="cfg5: one LIVEditor-14B-shaped layer, 50,000 + 50,000 tokens (ragged segments)",
+                 heads=40, head_dim=128, l_src=50000, l_ctx=50000),
+}
+CFG4_GRID = dict(alpha_s=(0.0625, 0.125, 0.25, 0.5, 1.0), alpha_f=(0.0, 0.25, 0.5, 0.75))
 
 
 def synth_qkv(heads, S, D, dev):
@@ -63,34 +79,59 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--heads", type=int, default=WORKLOAD["heads"])
-    ap.add_argument("--l-src", type=int, default=WORKLOAD["l_src"])
-    ap.add_argument("--l-ctx", type=int, default=WORKLOAD["l_ctx"])
+    ap.add_argument("--config", choices=sorted(CONFIGS) + ["cfg4-grid"], default="cfg3")
+    ap.add_argument("--heads", type=int, default=None)
+    ap.add_argument("--l-src", type=int, default=None)
+    ap.add_argument("--l-ctx", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true", help="reference arm: every head, every query block")
     ap.add_argument("--no-extras", action="store_true", help="skip dense/SDPA/e2e side measurements")
-    return ap.parse_args()
+    args = ap.parse_args()
+    c = CONFIGS["cfg4" if args.config == "cfg4-grid" else args.config]
+    args.heads = args.heads or c["heads"]
+    args.l_src = args.l_src if args.l_src is not None else c["l_src"]
+    args.l_ctx = args.l_ctx if args.l_ctx is not None else c["l_ctx"]
+    args.head_dim = c["head_dim"]
+    args.workload = dict(WORKLOAD, workload=c["workload"], heads=args.heads, head_dim=args.head_dim,
+                         l_src=args.l_src, l_ctx=args.l_ctx)
+    return args
 
 
 # --------------------------------------------------------------------------- CPU (reference algorithm)
-def cpu_sample(l_src, l_ctx, heads, D=128, fraction=1 / 16, seed=0):
+def cpu_sample(l_src, l_ctx, heads, D=128, fraction=1 / 16, seed=0, heads_run=1):
     """Time the reference algorithm (oracle port, numpy/BLAS on all host cores)
-    on one head of the workload: routing (stages 1-3) in full, attention on a
-    `fraction` of the query blocks; extrapolate to all heads (the reference runs
-    heads serially: reference.py:159-160, taylor.py:176-177)."""
+    on `heads_run` heads of the workload: routing (stages 1-3) in full,
+    attention on a `fraction` of the query blocks; extrapolate to all heads
+    (the reference runs heads serially: reference.py:159-160, taylor.py:176-177).
+    heads_run = heads and fraction = 1 is the full workload, no extrapolation."""
     import numpy as np
 
     from oracle import isa_oracle as O
 
     rng = np.random.default_rng(seed)
     S = l_src + l_ctx
-    q, k, v = (O.round_bf16(rng.standard_normal((1, 1, S, D), dtype=np.float32)) for _ in range(3))
-    t0 = time.perf_counter()
-    asm = O.OracleAssembly(q, k, v, l_src, l_ctx)
-    t1 = time.perf_counter()
-    asm.forward(block_fraction=fraction)
-    t2 = time.perf_counter()
-    per_head = (t1 - t0) + (t2 - t1) / fraction
-    return per_head * heads * 1e3, dict(route_s=t1 - t0, attn_sample_s=t2 - t1)
+    route = attn = 0.0
+    for _ in range(heads_run):
+        q, k, v = (O.round_bf16(rng.standard_normal((1, 1, S, D), dtype=np.float32)) for _ in range(3))
+        t0 = time.perf_counter()
+        asm = O.OracleAssembly(q, k, v, l_src, l_ctx)
+        t1 = time.perf_counter()
+        asm.forward(block_fraction=fraction)
+        t2 = time.perf_counter()
+        route += t1 - t0
+        attn += t2 - t1
+    per_head = (route + attn / fraction) / heads_run
+    return per_head * heads * 1e3, dict(route_s=route, attn_sample_s=attn, heads_run=heads_run, fraction=fraction)
+
+
+def cpu_plan(args):
+    """Bounded CPU sample per config: (heads_run, fraction). cfg1 runs in full;
+    --cpu-full runs every head and every query block of any config."""
+    if args.cpu_full or args.config == "cfg1":
+        return args.heads, 1.0
+    if args.config == "cfg2":
+        return 2, 1.0
+    return 1, 1 / 16
 
 
 def cpu_cores():
@@ -107,25 +148,34 @@ def cpu_cores():
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    fraction = 1 / 16
+    heads_run, fraction = cpu_plan(args)
     vals = []
     for i in range(args.warmup + args.steps):
-        ms, detail = cpu_sample(args.l_src, args.l_ctx, args.heads, fraction=fraction)
+        ms, detail = cpu_sample(args.l_src, args.l_ctx, args.heads, D=args.head_dim, fraction=fraction,
+                                heads_run=heads_run)
         if i >= args.warmup:
             vals.append(ms)
     value = statistics.median(vals)
     cores, apis = cpu_cores()
-    sample = (f"1 of {args.heads} heads: routing (stages 1-3) in full + attention on 1/16 of the query blocks, "
-              f"extrapolated x{args.heads} heads (oracle port of the pure-Python reference; numpy fp64 over {apis})")
+    sample = _sample_text(args, heads_run, fraction, apis)
     line = {
         "metric": METRIC, "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": dict(WORKLOAD, parallelism="cpu"),
+        "config": dict(args.workload, parallelism="cpu",
+                       inputs="iid N(0,1) rounded to bf16 values (numpy default_rng, fp32 -> fp64 arithmetic)"),
         "cpu_baseline": {"value": value, "unit": "ms", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _sample_text(args, heads_run, fraction, apis):
+    full = heads_run == args.heads and fraction == 1.0
+    what = (f"{heads_run} of {args.heads} heads: routing (stages 1-3) in full + attention on "
+            f"{'all' if fraction == 1.0 else f'1/{round(1 / fraction)} of the'} query blocks")
+    return (what + ("" if full else f", extrapolated to {args.heads} heads")
+            + f" (oracle port of the pure-Python reference; numpy fp64 over {apis})")
 
 
 # --------------------------------------------------------------------------- clocks
@@ -189,7 +239,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    H, D = args.heads, WORKLOAD["head_dim"]
+    H, D = args.heads, args.head_dim
     S = args.l_src + args.l_ctx
     icl = P.IclLayout(args.l_src, args.l_ctx)
     cfg = P.IsaConfig(strict=(args.l_src % 64 == 0 and args.l_ctx % 64 == 0))  # ragged segments (cfg5) allowed
@@ -346,9 +396,9 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": dict(WORKLOAD, heads=H, l_src=args.l_src, l_ctx=args.l_ctx,
-                       parallelism=f"head-sharded x{world}" if world > 1 else "single GPU",
-                       l2="inputs larger than L2"),
+        "config": dict(args.workload, parallelism=f"head-sharded x{world}" if world > 1 else "single GPU",
+                       l2="inputs larger than L2" if 3 * H * S * D * 2 > 126e6 else
+                          "inputs fit in L2: steps back to back (no flush); routing reads are warm"),
         "tflops_isa_alg": f_isa / (ms * 1e-3) / 1e12,
         "tflops_dense_equiv": f_dense / (ms * 1e-3) / 1e12,
         "flops": {"isa": f_isa, "dense": f_dense, "sharp": f_sharp * world, "taylor_alg": f_taylor_alg * world},
@@ -384,6 +434,8 @@ def run_ours(args, rank, world, local_rank):
     }
     if rank == 0 and world == 1 and not args.no_extras:
         result.update(_extras(args, P, q, k, v, icl, cfg, ms, dev))
+    if args.config == "cfg4-grid":
+        result["grid"] = _cfg4_grid(P, q, k, v, icl, result.get("dense_ms"), result.get("cudnn_sdpa_ms"))
     if world > 1 and not args.no_extras:
         e = _e2e(args, P, q, k, v, icl, cfg, world)
         t = torch.tensor([e["value"]], device=dev)
@@ -391,13 +443,13 @@ def run_ours(args, rank, world, local_rank):
         e["value"] = float(t.item())
         result["e2e"] = e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cms, detail = cpu_sample(args.l_src, args.l_ctx, H)
+        heads_run, fraction = cpu_plan(args)
+        cms, detail = cpu_sample(args.l_src, args.l_ctx, H, D=D, fraction=fraction, heads_run=heads_run)
         cores, apis = cpu_cores()
         result["cpu_baseline"] = {
             "value": cms, "unit": "ms", "cores": cores, "kind": "port",
-            "sample": f"1 head (routing full + 1/16 of query blocks for attention) x{H} heads extrapolated; "
-                      f"oracle port of the pure-Python reference (numpy fp64, BLAS {apis}); "
-                      f"route {detail['route_s']:.2f}s, attention sample {detail['attn_sample_s']:.2f}s",
+            "sample": _sample_text(args, heads_run, fraction, apis)
+                      + f"; route {detail['route_s']:.2f}s, attention sample {detail['attn_sample_s']:.2f}s",
         }
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -482,6 +534,39 @@ def _extras(args, P, q, k, v, icl, cfg, ms, dev):
 
     res["e2e"] = _e2e(args, P, q, k, v, icl, cfg, 1)
     return res
+
+
+def _cfg4_grid(P, q, k, v, icl, dense_ms, sdpa_ms, reps=3):
+    """BASELINE configs[3]: the ISA layer over alpha_s x alpha_f (alpha_ns =
+    0.0625; alpha_f is the sharpness threshold as a rank cut, coarse.py:197)
+    against dense attention on the same tensors. CUDA events around `reps`
+    calls after one warm-up, per point."""
+    import torch
+
+    st = torch.cuda.current_stream()
+    rows = []
+    for a_s in CFG4_GRID["alpha_s"]:
+        for a_f in CFG4_GRID["alpha_f"]:
+            cfg = P.IsaConfig(alpha_s=a_s, alpha_f=a_f, alpha_ns=0.0625)
+            prep = P.prepare(q, k, v, icl, cfg)
+            prep()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(reps):
+                prep()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            d = P.IsaDims.derive(q.shape, icl, cfg)
+            f = d.flops()
+            rows.append({"alpha_s": a_s, "alpha_f": a_f, "ms": ms, "isa_alg_tflops": f.total() / ms / 1e9,
+                         "flop_ratio_dense_over_isa": f.dense_equivalent_mas / f.total(),
+                         "speedup_vs_dense_sm100a": dense_ms / ms if dense_ms else None,
+                         "speedup_vs_cudnn_sdpa": sdpa_ms / ms if sdpa_ms else None,
+                         "k_ctx": d.k_ctx, "n_flat": d.n_flat, "k": d.k})
+            del prep
+    return rows
 
 
 def _e2e(args, P, q, k, v, icl, cfg, world):
