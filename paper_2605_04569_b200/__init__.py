@@ -22,6 +22,7 @@ from .errors import (
     NumericError,
 )
 from .types import (
+    DTYPES,
     BlockLayout,
     BlockMask,
     FlopCount,
@@ -33,6 +34,7 @@ from .types import (
     IsaTrace,
     SelectionIndex,
     SharpnessSplit,
+    Tensor4,
 )
 
 from .blocks import concat_seq, ensure_tensor4, gather_blocks, pad_to_blocks, scatter_blocks
@@ -56,7 +58,7 @@ def __getattr__(name):
         from . import coarse
 
         return getattr(coarse, name)
-    if name in ("full_attention", "online_softmax_attention", "full_attention_backward"):
+    if name in ("full_attention", "online_softmax_attention", "full_attention_backward", "OnlineState"):
         from . import exact
 
         return getattr(exact, name)

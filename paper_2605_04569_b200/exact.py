@@ -7,9 +7,14 @@ S_q == S_k runs `isa_dense_attention`; S_q != S_k runs `isa_cross_attention`
 on query rows zero-padded to a multiple of 64, except a ragged key length with
 no more key blocks than query blocks, which runs `isa_dense_attention` on
 query slabs of S_k rows.
-Key masks: an all-valid mask is accepted; a mask that drops keys is not
-implemented on the GPU path and raises ConfigError (a row with every key
-masked raises DegenerateRowError first, like reference.py:116-117).
+Key masks (reference.py:67-76, 113-119, 160-162): masked keys get zero
+weight, i.e. the softmax runs over the valid keys only — so the valid K/V
+rows are compacted on the device (one index_select when every (b, h) shares
+the mask, per (b, h) otherwise) and the same kernel runs on them. A row with
+every key masked raises DegenerateRowError (reference.py:116-117).
+
+`OnlineState` (reference.py:28-60) is the blockwise softmax accumulator with
+the reference's update/finalize contract, on device fp64 tensors.
 """
 
 from __future__ import annotations
@@ -60,6 +65,50 @@ def _device_bf16(x, dev):
     return x
 
 
+class OnlineState:
+    """Running (max, normalizer, output accumulator) for blockwise softmax
+    attention (reference.py:28-60): update() folds in one block of scores and
+    values, rescaling the accumulators by exp(m - m_new) when the running max
+    moves; `weights` multiplies the exponentials per score column (the Taylor
+    branch's block weights). float64 on the CUDA device (numpy inputs are
+    uploaded; finalize returns a numpy array when update was fed numpy)."""
+
+    def __init__(self, rows: int, dim: int, device=None):
+        if not torch.cuda.is_available() and device is None:
+            raise LayoutError("OnlineState runs on a CUDA device and none is available (there is no CPU path)")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.m = torch.full((rows,), -math.inf, dtype=torch.float64, device=dev)
+        self.ell = torch.zeros(rows, dtype=torch.float64, device=dev)
+        self.o_acc = torch.zeros((rows, dim), dtype=torch.float64, device=dev)
+        self._numpy = False
+
+    def _t(self, x):
+        if isinstance(x, np.ndarray):
+            self._numpy = True
+            return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(self.m.device)
+        return torch.as_tensor(x, dtype=torch.float64, device=self.m.device)
+
+    def update(self, scores, values, weights=None) -> None:
+        s = self._t(scores)
+        m_new = torch.maximum(self.m, s.max(dim=1).values if s.shape[1] else self.m)
+        p = torch.where(torch.isfinite(s), torch.exp(s - m_new[:, None]), torch.zeros((), dtype=s.dtype,
+                                                                                      device=s.device))
+        if weights is not None:
+            p = p * self._t(weights)
+        delta = self.m - m_new
+        delta = torch.where(torch.isfinite(delta), delta, torch.zeros_like(delta))  # both -inf: nothing yet
+        alpha = torch.exp(delta)
+        self.ell = self.ell * alpha + p.sum(dim=1)
+        self.o_acc = self.o_acc * alpha[:, None] + p @ self._t(values)
+        self.m = m_new
+
+    def finalize(self):
+        if bool((self.ell <= 0.0).any()):
+            raise DegenerateRowError("row with empty key set: normalizer is zero")
+        out = self.o_acc / self.ell[:, None]
+        return out.cpu().numpy() if self._numpy else out
+
+
 def _exact(q, k, v, scale, mask):
     (B, H, S_q, D), (Bk, Hk, S_k, Dk), (Bv, Hv, S_v, Dv) = (_shape4(x, n) for x, n in ((q, "Q"), (k, "K"), (v, "V")))
     if (Bk, Hk) != (B, H) or (Bv, Hv) != (B, H) or Dk != D:
@@ -73,10 +122,10 @@ def _exact(q, k, v, scale, mask):
     if scale <= 0:
         raise ConfigError(f"scale must be > 0, got {scale}")
     km = _key_mask(mask, B, H, S_k)
-    if km is not None and not km.all():
-        if not km.any(axis=2).all():
-            raise DegenerateRowError("query row with all keys masked")
-        raise ConfigError("key masks that drop keys are not supported by the sm_100a kernel")
+    if km is not None and km.all():
+        km = None
+    if km is not None and not km.any(axis=2).all():
+        raise DegenerateRowError("query row with all keys masked")
     if D > max(SUPPORTED_HEAD_DIMS):
         raise ConfigError(f"head dim {D} not supported by the sm_100a kernels (<= {max(SUPPORTED_HEAD_DIMS)})")
     numpy_io = isinstance(q, np.ndarray)
@@ -92,16 +141,31 @@ def _exact(q, k, v, scale, mask):
     width = 64 if D <= 64 else 128
     if width != D:  # zero columns: exact zeros in every score, dropped output columns
         qd, kd, vd = (torch.nn.functional.pad(x, (0, width - D)) for x in (qd, kd, vd))
-    if S_q == S_k:
-        from .pipeline import dense_attention
-
-        res = dense_attention(qd, kd, vd, scale)
+    if km is None:
+        res = _run(qd, kd, vd, scale)
+    elif (km == km[:1, :1]).all():  # one mask for every (b, h): compact the valid keys once
+        idx = torch.from_numpy(np.nonzero(km[0, 0])[0]).to(dev)
+        res = _run(qd, kd.index_select(2, idx), vd.index_select(2, idx), scale)
     else:
-        res = _cross(qd, kd, vd, scale)
+        res = torch.empty((B, H, S_q, width), dtype=torch.bfloat16, device=dev)
+        for bi in range(B):
+            for hi in range(H):
+                idx = torch.from_numpy(np.nonzero(km[bi, hi])[0]).to(dev)
+                sl = (slice(bi, bi + 1), slice(hi, hi + 1))
+                res[sl] = _run(qd[sl], kd[sl].index_select(2, idx), vd[sl].index_select(2, idx), scale)
     res = res[..., :D]
     if numpy_io:
         return res.float().cpu().numpy().astype(out_dtype)
     return res.to(out_dtype).contiguous()
+
+
+def _run(q, k, v, scale):
+    """Dense softmax attention of bf16 device tensors on the sm_100a kernels."""
+    if q.shape[2] == k.shape[2]:
+        from .pipeline import dense_attention
+
+        return dense_attention(q, k, v, scale)
+    return _cross(q, k, v, scale)
 
 
 def _cross(q, k, v, scale):

@@ -21,7 +21,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass, field
-from typing import Optional
+from typing import Union, Optional
 
 import numpy as np
 
@@ -35,6 +35,14 @@ PRECISIONS = ("double", "single")
 SUPPORTED_BLOCK = 64
 SUPPORTED_HEAD_DIMS = (64, 128)
 
+
+
+# tensor.py:17-19: the reference's tensor alias and storage dtypes. The B200
+# operator takes numpy arrays or torch tensors; "double" is accepted by
+# IsaConfig.validate (pipeline.py:73-88) and rejected by the sm_100a kernels
+# (validate_b200), which compute in bf16 with fp32 accumulation.
+Tensor4 = Union[np.ndarray, "torch.Tensor"]
+DTYPES = {"single": np.float32, "double": np.float64}
 
 @dataclass
 class GradBundle:
