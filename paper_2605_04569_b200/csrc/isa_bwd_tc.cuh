@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
   uint64_t* d_full = bars + 7;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
   int* s_count = reinterpret_cast<int*>(bars + 9);
+  uint64_t* st_free = bars + 10;  // [2]: every softmax thread has read the slot's lse/rho rows
   int* sList = reinterpret_cast<int*>(smem + L::kList);     // query-block position (x < n_sharp: sharp)
   int* sVis = sList + tp.n_list_max;                          // bit0: lists j0, bit1: lists j1
   // per-query statistics [2 slots][lse 128 | rho 128]: a static __shared__
@@ -82,8 +83,9 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
     *s_count = 0;
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&qo_full[s], 1);
+      mbar_init(&qo_full[s], 32);  // every producer lane arrives after its own smem writes
       mbar_init(&qo_empty[s], 1);
+      mbar_init(&st_free[s], 256);
     }
     mbar_init(s_full, 1);
     mbar_init(p_full, 8);
@@ -167,7 +169,10 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
       const int slot = t & 1;
       cur = nxt;
       fetch(t + 1, nxt);  // loads in flight during the wait below
-      if (t >= 2) mbar_wait(&qo_empty[slot], ((t >> 1) - 1) & 1);
+      if (t >= 2) {
+        mbar_wait(&qo_empty[slot], ((t >> 1) - 1) & 1);
+        mbar_wait(&st_free[slot], ((t >> 1) - 1) & 1);  // tile t-2's stats read by every softmax thread
+      }
       __syncwarp();
       float* st = sStats + slot * 256;
 #pragma unroll
@@ -176,7 +181,8 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
         st[128 + lane + 32 * k4] = cur.rh[k4];
       }
       __syncwarp();
-      __threadfence_block();
+      // each lane releases its own stats writes (the leader also arms the TMA bytes)
+      if (!leader) mbar_arrive(&qo_full[slot]);
       if (leader) {
         mbar_arrive_expect_tx(&qo_full[slot], 2 * L::kTile);
         uint8_t* dq_ = smem + L::kQO + slot * 2 * L::kTile;
@@ -315,6 +321,7 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
         tmem_st16(t_s + 64 + ch * 16, pk);
         tmem_st16(t_dp + 64 + ch * 16, dk);
       }
+      mbar_arrive(&st_free[slot]);  // this thread's reads of the slot's stats are done
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -405,6 +412,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
   uint64_t* p_full = bars + 6;
   uint64_t* d_full = bars + 7;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* meta_free = bars + 9;  // [2]: every softmax thread has read the slot's sMeta / sCol
   __shared__ float sCol[2 * 128];  // [2 slots][128] column bias (centroid tiles)
   __shared__ int sMeta[2 * 4];     // [2 slots]: centroid flag, tile index, meta0, meta1
 
@@ -432,8 +440,9 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
   if (threadIdx.x == 0) {
     mbar_init(qo_full, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_full[s], 32);  // every producer lane arrives after its own smem writes
       mbar_init(&kv_empty[s], 1);
+      mbar_init(&meta_free[s], 128);
     }
     mbar_init(s_full, 1);
     mbar_init(p_full, 4);
@@ -463,7 +472,10 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
     const int4* tl = flat ? tiles + (((long long)bh * n_items + item) * 2 + stg) * max_tiles : nullptr;
     for (int i = 0; i < n_kv; ++i) {
       const int slot = i & 1;
-      if (i >= 2) mbar_wait(&kv_empty[slot], ((i >> 1) - 1) & 1);
+      if (i >= 2) {
+        mbar_wait(&kv_empty[slot], ((i >> 1) - 1) & 1);
+        mbar_wait(&meta_free[slot], ((i >> 1) - 1) & 1);  // tile i-2's metadata read by every softmax thread
+      }
       __syncwarp();
       int tok0, tok1, cent = 0, meta0 = 0xF | (64 << 8), meta1 = 0xF | (64 << 8);
       if (i < n_exact) {
@@ -504,7 +516,8 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
         sMeta[slot * 4 + 3] = meta1;
       }
       __syncwarp();
-      __threadfence_block();
+      // each lane releases its own metadata writes (the leader also arms the TMA bytes)
+      if (!leader) mbar_arrive(&kv_full[slot]);
       if (leader) {
         mbar_arrive_expect_tx(&kv_full[slot], 2 * L::kTile);
         uint8_t* dst = smem + L::kKV + slot * 2 * L::kTile;
@@ -635,6 +648,7 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
 #pragma unroll 1
         for (int ch = 3; ch >= 0; --ch) chunk(ch, std::false_type{});
       }
+      mbar_arrive(&meta_free[slot]);  // this thread's reads of the slot's metadata are done
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();

@@ -501,6 +501,10 @@ __device__ __forceinline__ void taylor_t_body(const CUtensorMap& tm_q, const CUt
     mbar_wait(&o_full[s], 0);  // every PV of this stage complete: both P^T buffers are free
     __syncwarp();
     tc_fence_after();
+    // the P^T buffer is reused as scratch: order every warp's last P^T row
+    // stores before any warp's scratch stores (the o_full chain runs through
+    // the async proxy, which racecheck does not see)
+    named_bar_sync(bar_id, 128);
     float* sRed = reinterpret_cast<float*>(sPs);
     {
       float v[64];
