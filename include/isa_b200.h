@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define ISA_ABI_VERSION 3
+#define ISA_ABI_VERSION 4
 
 typedef enum IsaStatus {
   ISA_OK = 0,
@@ -75,6 +75,8 @@ typedef struct IsaKnobs {
   double gamma;          /* coarse residual weight, 0 = off (pipeline.py:354-356) */
   int32_t residual_softmax; /* residual weights: 1 softmax(S_coarse), 0 raw Qc.Kc (pipeline.py:261-267) */
   int32_t reserved;      /* 0 */
+  double rope_base;      /* > 0: apply decoupled RoPE (pipeline.py:469-490) to Q and K inside the pooling
+                            pass (bf16 inputs; same bits as isa_decoupled_rope then isa_forward); 0 = off */
 } IsaKnobs;
 
 /* IsaKnobs.flags: launch the exact (sharp) and Taylor (flat) attention

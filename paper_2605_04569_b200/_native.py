@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # ISA_B200_LIB points at an alternative build of the same C ABI (A/B kernel measurements)
 LIB_PATH = os.environ.get("ISA_B200_LIB") or os.path.join(HERE, "libisa_b200.so")
 
-ISA_ABI_VERSION = 3
+ISA_ABI_VERSION = 4
 ISA_DTYPE_BF16 = 0
 ISA_DTYPE_F32 = 1
 
@@ -93,6 +93,7 @@ class IsaKnobs(ctypes.Structure):
         ("gamma", ctypes.c_double),
         ("residual_softmax", ctypes.c_int32),
         ("_pad", ctypes.c_int32),
+        ("rope_base", ctypes.c_double),
     ]
 
 

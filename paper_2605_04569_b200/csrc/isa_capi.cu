@@ -122,6 +122,7 @@ struct Dims {
   double scale;
   double gamma;       // coarse residual weight (0 = off)
   int resid_softmax;  // residual weights softmax(S_coarse) (1) or raw Qc.Kc (0)
+  double rope_base;   // > 0: decoupled RoPE fused into the pooling pass
 };
 
 int derive(const IsaShape* sh, const IsaKnobs* kn, Dims* d) {
@@ -168,13 +169,18 @@ int derive(const IsaShape* sh, const IsaKnobs* kn, Dims* d) {
   if (!(kn->gamma >= 0.0)) return fail(ISA_ERR_CONFIG, "gamma must be >= 0, got %g", kn->gamma);
   d->gamma = kn->gamma;
   d->resid_softmax = kn->residual_softmax != 0;
+  d->rope_base = kn->rope_base;
+  if (d->rope_base < 0.0 || d->rope_base != d->rope_base) return fail(ISA_ERR_CONFIG, "rope base must be > 0");
+  if (d->rope_base > 0.0 && sh->dtype != ISA_DTYPE_BF16)
+    return fail(ISA_ERR_CONFIG, "fused decoupled RoPE takes bf16 Q/K/V");
   return ISA_OK;
 }
 
 struct Workspace {
   int32_t* err;
   float* means;  // [3][BH][T][D]
-  __nv_bfloat16* bf;  // [3][BH][S][D] (fp32 inputs only)
+  __nv_bfloat16* bf;  // [3][BH][S][D] (fp32 inputs; [2] rotated Q, K with fused RoPE)
+  float2* rope_tab;   // [S][D/2] (cos, sin) with fused RoPE
   double* s_new;      // [BH][T][t_new]  fp64 coarse scores vs K_new blocks
   double* s_ctx;      // [BH][t_src][t_ctx] fp64 source-row x context-column scores
   uint8_t* flags;     // [BH][max(T, t_ctx)]
@@ -209,7 +215,10 @@ Workspace carve(const Dims& d, int dtype, uint8_t* base) {
   const long long BH = d.BH;
   w.err = reinterpret_cast<int32_t*>(take(16));
   w.means = reinterpret_cast<float*>(take(3ull * BH * d.T * d.D * 4));
-  w.bf = dtype == ISA_DTYPE_F32 ? reinterpret_cast<__nv_bfloat16*>(take(3ull * BH * d.S * d.D * 2)) : nullptr;
+  w.bf = dtype == ISA_DTYPE_F32 ? reinterpret_cast<__nv_bfloat16*>(take(3ull * BH * d.S * d.D * 2))
+         : d.rope_base > 0.0     ? reinterpret_cast<__nv_bfloat16*>(take(2ull * BH * d.S * d.D * 2))
+                                 : nullptr;
+  w.rope_tab = d.rope_base > 0.0 ? reinterpret_cast<float2*>(take(8ull * d.S * (d.D / 2))) : nullptr;
   w.s_new = reinterpret_cast<double*>(take(8ull * BH * d.T * d.t_new));
   w.s_ctx = reinterpret_cast<double*>(take(8ull * BH * d.t_src * d.t_ctx));
   w.flags = reinterpret_cast<uint8_t*>(take((size_t)BH * (d.T > d.t_ctx ? d.T : d.t_ctx)));
@@ -339,9 +348,9 @@ int qkv_maps(const IsaShape* sh, const Dims& d, const void* q, const void* k, co
   CUtensorMap* maps[3] = {tq, tk, tv};
   for (int i = 0; i < 3; ++i) {
     int rc;
-    if (sh->dtype == ISA_DTYPE_BF16) {
+    if (sh->dtype == ISA_DTYPE_BF16 && !(d.rope_base > 0.0 && i < 2)) {
       rc = make_map(maps[i], ptr[i], d.D, d.S, d.H, d.B, sh->stride_s * 2, sh->stride_h * 2, sh->stride_b * 2);
-    } else {
+    } else {  // the workspace bf16 copy: fp32 inputs, or Q / K rotated by the fused RoPE
       const __nv_bfloat16* base = w.bf + (long long)i * d.BH * d.S * d.D;
       rc = make_map(maps[i], base, d.D, d.S, d.H, d.B, (long long)d.D * 2, (long long)d.S * d.D * 2,
                     (long long)d.H * d.S * d.D * 2);
@@ -389,21 +398,28 @@ void record(const IsaEvents* ev, int i, cudaStream_t st) {
 }
 
 int run_pool(const IsaShape* sh, const Dims& d, const void* q, const void* k, const void* v, float* means,
-             __nv_bfloat16* bf, int32_t* err, cudaStream_t st) {
+             __nv_bfloat16* bf, int32_t* err, cudaStream_t st, float2* rope_tab = nullptr) {
   isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};
   dim3 grid((d.T + 3) / 4, d.BH, 3);
   if (sh->dtype == ISA_DTYPE_BF16) {
     auto* qq = static_cast<const __nv_bfloat16*>(q);
     auto* kk = static_cast<const __nv_bfloat16*>(k);
     auto* vv = static_cast<const __nv_bfloat16*>(v);
+    const float2* tab = nullptr;
+    if (d.rope_base > 0.0) {  // fused decoupled RoPE: angle table, then rotate + pool Q / K
+      const long long n = (long long)d.S * (d.D / 2);
+      isa::rope_table_kernel<<<grid1d(n, 256), 256, 0, st>>>(rope_tab, d.S, d.D, d.l_src, std::log2(d.rope_base));
+      ISA_LAUNCHED("rope_table_kernel");
+      tab = rope_tab;
+    }
     if (d.D == 128)
       isa::pool_means_kernel<__nv_bfloat16, 128><<<grid, 128, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h,
-                                                                       sh->stride_s, d.H, seg, d.T, means, nullptr,
-                                                                       d.S, err);
+                                                                       sh->stride_s, d.H, seg, d.T, means, bf,
+                                                                       d.S, err, tab);
     else
       isa::pool_means_kernel<__nv_bfloat16, 64><<<grid, 128, 0, st>>>(qq, kk, vv, sh->stride_b, sh->stride_h,
-                                                                      sh->stride_s, d.H, seg, d.T, means, nullptr,
-                                                                      d.S, err);
+                                                                      sh->stride_s, d.H, seg, d.T, means, bf,
+                                                                      d.S, err, tab);
   } else {
     auto* qq = static_cast<const float*>(q);
     auto* kk = static_cast<const float*>(k);
@@ -484,7 +500,7 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   float* kc = w.means + BH * d.T * d.D;
   float* vc = w.means + 2 * BH * d.T * d.D;
   // ---- stage 1: coarse (pooled means, context saliency)
-  if ((rc = run_pool(sh, d, q, k, v, w.means, w.bf, err, st))) return rc;
+  if ((rc = run_pool(sh, d, q, k, v, w.means, w.bf, err, st, w.rope_tab))) return rc;
   const bool need_scores = !pinned;
   if (need_scores && d.t_ctx) {
     // context saliency in the reference's order: fp64 scores of the source

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/isa_b200.h"
+#include "isa_ptx.cuh"
 
 namespace isa {
 
@@ -34,6 +35,29 @@ __device__ __forceinline__ bool ranks_before(double a, int ia, double b, int ib)
   return a > b || (a == b && ia < ib);
 }
 
+// Decoupled RoPE rotation of one pair (pipeline.py:469-490): fp32 with the
+// operation order pinned (no contraction differences between the standalone
+// kernel and the one fused into the pooling pass: same bits either way).
+__device__ __forceinline__ void rope_pair(float e, float o, float c, float s, float& r0, float& r1) {
+  r0 = __fsub_rn(__fmul_rn(e, c), __fmul_rn(o, s));
+  r1 = __fadd_rn(__fmul_rn(e, s), __fmul_rn(o, c));
+}
+
+// cos / sin of pos * base^(-2i/D) for every token and pair, computed in fp64
+// and rounded to fp32 (the values decoupled_rope_kernel forms per token);
+// positions restart at 0 for the context segment. tab[tok][i] = (cos, sin).
+__global__ void rope_table_kernel(float2* __restrict__ tab, int S, int D, int l_src, double log2_base) {
+  const int half = D / 2;
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= (long long)S * half) return;
+  const int tok = static_cast<int>(gid / half), i = static_cast<int>(gid % half);
+  const double pos = tok < l_src ? tok : tok - l_src;
+  const double theta = pos * exp2(-log2_base * (2.0 * i) / D);  // pos * base^(-2i/D)
+  double sd, cd;
+  sincos(theta, &sd, &cd);
+  tab[gid] = make_float2(static_cast<float>(cd), static_cast<float>(sd));
+}
+
 // ----------------------------------------------------------------------------
 // K1: block means of Q, K, V (fp64 sums over valid rows -> fp32; bit-identical
 // to tensor.py:115-119 whenever the 64-term fp64 sum is exact, always for bf16
@@ -48,7 +72,8 @@ __global__ void __launch_bounds__(128) pool_means_kernel(const Tin* __restrict__
                                                          long long ss, int H, SegInfo seg, int T,
                                                          float* __restrict__ means,  // [3][BH][T][D]
                                                          __nv_bfloat16* __restrict__ bf_copy,  // [3][BH][S][D] or null
-                                                         int S, int* __restrict__ err) {
+                                                         int S, int* __restrict__ err,
+                                                         const float2* __restrict__ rope_tab = nullptr) {
   constexpr int VEC = 8;
   constexpr int LPR = D / VEC;     // lanes per row
   constexpr int RPW = 32 / LPR;    // rows per warp wave
@@ -82,6 +107,25 @@ __global__ void __launch_bounds__(128) pool_means_kernel(const Tin* __restrict__
         const float2 t = __bfloat1622float2(hw[e]);
         f[2 * e] = t.x;
         f[2 * e + 1] = t.y;
+      }
+      if (rope_tab && which < 2) {
+        // fused decoupled RoPE (bf16 inputs): rotate Q / K rows, round to bf16
+        // like the standalone kernel, write the copy the attention kernels
+        // load, and pool the rounded rotated values (== RoPE then isa_forward)
+        const float4* tr = reinterpret_cast<const float4*>(rope_tab + (long long)(tok0 + r) * (D / 2) + col / 2);
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float4 cs2 = __ldg(tr + e / 2);
+          const float cc = (e & 1) ? cs2.z : cs2.x, sn = (e & 1) ? cs2.w : cs2.y;
+          float r0, r1;
+          rope_pair(f[2 * e], f[2 * e + 1], cc, sn, r0, r1);
+          pk[e] = pack_bf16x2(r0, r1);
+          f[2 * e] = __uint_as_float(pk[e] << 16);
+          f[2 * e + 1] = __uint_as_float(pk[e] & 0xffff0000u);
+        }
+        *reinterpret_cast<uint4*>(bf_copy + (((long long)which * gridDim.y + bh) * S + tok0 + r) * D + col) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
     } else {
       const float4 a = __ldg(reinterpret_cast<const float4*>(rowp));
@@ -906,11 +950,7 @@ __global__ void __launch_bounds__(256) decoupled_rope_kernel(const T* __restrict
       }
       float r[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float e = v[2 * j], o = v[2 * j + 1];
-        r[2 * j] = e * cs[j] - o * sn[j];
-        r[2 * j + 1] = e * sn[j] + o * cs[j];
-      }
+      for (int j = 0; j < 4; ++j) rope_pair(v[2 * j], v[2 * j + 1], cs[j], sn[j], r[2 * j], r[2 * j + 1]);
       if constexpr (sizeof(T) == 2) {
         uint4 w;
         w.x = pack_bf16x2(r[0], r[1]);

@@ -421,7 +421,7 @@ _TAYLOR_FLAGS = {None: 0, "auto": 0, "k7": 2, "k7t": 4}
 
 
 def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = True, *, out=None, validate=True,
-                heads_per_chunk: int = 0, taylor_kernel: Optional[str] = None):
+                heads_per_chunk: int = 0, taylor_kernel: Optional[str] = None, rope_base: Optional[float] = None):
     """Run the full pipeline; returns (output, IsaTrace or None) (pipeline.py:307-316).
 
     The output has the input dtype (bf16 in -> bf16 out; fp32 in -> fp32 out,
@@ -432,6 +432,10 @@ def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = T
     Head dims other than 64/128 (up to 128) run zero-padded (`_pad_head_dim`).
     `taylor_kernel` ("k7" | "k7t" | None = per-head automatic choice) forces
     the D = 128 Taylor-branch kernel (test / A-B hook; same operator).
+    `rope_base` (bf16 inputs) applies the decoupled RoPE of
+    `apply_decoupled_rope(., icl, rope_base)` (pipeline.py:469-490) to Q and K
+    inside the pooling pass: the result equals RoPE followed by isa_forward
+    bit for bit, without the separate read + write of Q and K.
     """
     if taylor_kernel not in _TAYLOR_FLAGS:
         raise ConfigError(f"taylor_kernel must be one of {sorted(k for k in _TAYLOR_FLAGS if k)} or None")
@@ -439,6 +443,8 @@ def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = T
     if padded is not None:
         D = int(q.shape[-1])
         pcfg, pq, pk, pv = padded
+        if rope_base is not None:
+            raise ConfigError("fused RoPE needs a kernel head dim (64 or 128)")
         res, trace = isa_forward(pq, pk, pv, icl, pcfg, collect_trace, validate=validate,
                                  heads_per_chunk=heads_per_chunk, taylor_kernel=taylor_kernel)
         res = _unpad(res, D)
@@ -450,6 +456,10 @@ def isa_forward(q, k, v, icl: IclLayout, cfg: IsaConfig, collect_trace: bool = T
         return res, trace
     inp = _Inputs(q, k, v, icl, cfg)
     inp.knobs.flags |= _TAYLOR_FLAGS[taylor_kernel]
+    if rope_base is not None:
+        if not rope_base > 0:
+            raise ConfigError(f"rope base must be > 0, got {rope_base}")
+        inp.knobs.rope_base = float(rope_base)
     res, trace, _ = _run(inp, collect_trace, out=out, validate=validate, heads_per_chunk=heads_per_chunk)
     return res, trace
 
@@ -601,7 +611,8 @@ def apply_decoupled_rope(x, icl: IclLayout, base: float = 10000.0, *, out: Optio
     return out
 
 
-def prepare(q, k, v, icl, cfg, separate_branches: bool = False, signal: bool = False):
+def prepare(q, k, v, icl, cfg, separate_branches: bool = False, signal: bool = False,
+            rope_base: Optional[float] = None):
     """Validated inputs + a reusable workspace for repeated calls (bench/CUDA graphs).
 
     separate_branches launches the exact and Taylor attention branches as two
@@ -610,6 +621,8 @@ def prepare(q, k, v, icl, cfg, separate_branches: bool = False, signal: bool = F
     inp = _Inputs(q, k, v, icl, cfg)
     if separate_branches:
         inp.knobs.flags |= N.FLAG_SEPARATE_BRANCHES
+    if rope_base is not None:
+        inp.knobs.rope_base = float(rope_base)
     ws, nbytes = inp.workspace()
     return _Prepared(inp, ws, nbytes, signal=signal)
 

@@ -133,3 +133,42 @@ def test_head_shard_round_robin():
     assert sorted(h for r in range(3) for h in head_shard(10, r, 3)) == list(range(10))
     with pytest.raises(ValueError):
         head_shard(4, 2, 2)
+
+
+def _stack_worker(rank, world, port, q):
+    """Head-sharded DiT attention layers (column-parallel QKV, row-parallel O
+    with the chunked all-reduce) on CPU fp32 with a per-head stand-in attention;
+    every rank must reproduce the single-process stack."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_04569_b200.stack import DiTAttentionStack
+
+        def attend(qh, kh, vh, out):  # per-head softmax attention (the ISA layer is per head too)
+            s = torch.softmax(qh @ kh.transpose(-1, -2) / 4.0, dim=-1)
+            out.copy_(s @ vh)
+
+        H, D, S = 8, 16, 24
+        x = torch.randn(1, S, H * D, generator=torch.Generator().manual_seed(2))
+        kw = dict(layers=2, heads=H, head_dim=D, device="cpu", dtype=torch.float32, seed=4)
+        ref = DiTAttentionStack(**kw)(x, None, None, attend=attend)
+        got = DiTAttentionStack(**kw, world=world, rank=rank)(x, None, None, attend=attend)
+        q.put((rank, bool(torch.allclose(got, ref, rtol=1e-5, atol=1e-5)), float((got - ref).abs().max())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_dit_stack_matches_single_process(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stack_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res), res

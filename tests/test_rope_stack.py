@@ -117,3 +117,63 @@ def test_stack_layer_matches_composition(l_src, l_ctx):
     yd = layer(x, icl, cfg, attention="dense") if (l_src % 64 == 0 and l_ctx % 64 == 0) else None
     if yd is not None:
         assert torch.isfinite(yd.float()).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("l_src,l_ctx", [(2048, 2048), (1000, 1100)])
+def test_fused_rope_equals_rope_then_isa(l_src, l_ctx):
+    """isa_forward(..., rope_base) rotates Q/K inside the pooling pass; output
+    and routing equal apply_decoupled_rope followed by isa_forward bit for bit
+    (pipeline.py:469-490 then :307-316), on strided (B,S,3,H,D) views too."""
+    import torch
+
+    import paper_2605_04569_b200 as P
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    H, D, S = 3, 128, l_src + l_ctx
+    qkv = torch.randn(1, S, 3, H, D, device="cuda", generator=g).to(torch.bfloat16)
+    q, k, v = (qkv[:, :, i].permute(0, 2, 1, 3) for i in range(3))
+    icl, cfg = P.IclLayout(l_src, l_ctx), P.IsaConfig(strict=(l_src % 64 == 0 and l_ctx % 64 == 0))
+    out, tr = P.isa_forward(q, k, v, icl, cfg, rope_base=10000.0)
+    qr, kr = P.apply_decoupled_rope(q, icl), P.apply_decoupled_rope(k, icl)
+    ref, tr_ref = P.isa_forward(qr, kr, v, icl, cfg)
+    assert torch.equal(out, ref)
+    assert torch.equal(tr.selection.indices, tr_ref.selection.indices)
+    assert torch.equal(tr.mask.indices, tr_ref.mask.indices)
+    with pytest.raises(P.ConfigError):
+        P.isa_forward(q.float(), k.float(), v.float(), icl, cfg, rope_base=10000.0)
+
+
+@pytest.mark.gpu
+def test_stack_layer_vs_oracle():
+    """One DiT attention layer against the numpy oracle: the layer's own q/k/v
+    projection (cuBLAS), then oracle.apply_decoupled_rope + OracleAssembly
+    (pipeline.py:469-490, 133-370) in fp64 on the bf16 values and the output
+    projection in fp64; max-abs and cosine within the north-star tolerance."""
+    import numpy as np
+    import torch
+
+    import paper_2605_04569_b200 as P
+    from oracle import isa_oracle as O
+    from paper_2605_04569_b200.stack import DiTAttentionLayer
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    H, D, ls, lc = 4, 128, 2048, 2048
+    E, S = H * D, ls + lc
+    layer = DiTAttentionLayer(H, D, generator=g)
+    x = torch.randn(1, S, E, device="cuda", generator=g).to(torch.bfloat16)
+    icl = P.IclLayout(ls, lc)
+    y = layer(x, icl, P.IsaConfig())
+    qkv = layer.attention_inputs(x).float().cpu().numpy()  # bf16 values
+    q, k, v = (np.ascontiguousarray(qkv[:, :, i].transpose(0, 2, 1, 3)) for i in range(3))
+    qr = O.round_bf16(O.apply_decoupled_rope(q, ls, lc).astype(np.float32))
+    kr = O.round_bf16(O.apply_decoupled_rope(k, ls, lc).astype(np.float32))
+    o = O.OracleAssembly(qr, kr, v, ls, lc).forward()          # (1, H, S, D)
+    o = O.round_bf16(o.astype(np.float32)).transpose(0, 2, 1, 3).reshape(S, E).astype(np.float64)
+    xs = x.float().cpu().numpy().reshape(S, E).astype(np.float64)
+    ref = o @ layer.w_o.float().cpu().numpy().astype(np.float64)  # the attention branch's contribution
+    a = y.float().cpu().numpy().reshape(S, E).astype(np.float64) - xs
+    err = float(np.abs(a - ref).max())
+    cos = float((a * ref).sum() / (np.linalg.norm(a) * np.linalg.norm(ref)))
+    # y is stored in bf16 (|x| ~ 4 => ulp 2^-6): the tolerance is that rounding plus the attention's
+    assert err <= 2e-2 + 2 ** -6 * max(1.0, float(np.abs(xs).max())) and cos >= 0.999, (err, cos)
