@@ -2,7 +2,7 @@
 //
 // isa_forward runs the five reference stages (pipeline.py:133-370) as one
 // stream-ordered sequence of kernels with no host synchronisation:
-//   stage 1 "coarse"  K1 pool_means, K2 coarse_np (fp64 S of the source rows
+//   stage 1 "coarse"  K1 pool_means, K2 coarse_dmma (fp64 S of the source rows
 //                     vs the context columns), K2b ctx_mean  pipeline.py:176-184
 //   stage 2 "select"  K3 topk_rank (context), K_new block table, bf16 K_new
 //                     centroids + log2 weights              pipeline.py:186-212
@@ -397,6 +397,15 @@ void record(const IsaEvents* ev, int i, cudaStream_t st) {
   if (ev && ev->ev[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev->ev[i]), st);
 }
 
+// fp64 coarse scores, numpy einsum bits (coarse_dmma_kernel)
+int launch_coarse(const float* qc, long long q_hs, const float* kc, long long k_hs, const int* kv_blk, int col0,
+                  int rows, int n, int D, double scale, double* out, int BH, cudaStream_t st) {
+  dim3 g((n + 63) / 64, (rows + 63) / 64, BH);
+  isa::coarse_dmma_kernel<<<g, 256, 0, st>>>(qc, q_hs, kc, k_hs, kv_blk, col0, rows, n, D, scale, out);
+  ISA_LAUNCHED("coarse_dmma_kernel");
+  return ISA_OK;
+}
+
 int run_pool(const IsaShape* sh, const Dims& d, const void* q, const void* k, const void* v, float* means,
              __nv_bfloat16* bf, int32_t* err, cudaStream_t st, float2* rope_tab = nullptr) {
   isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};
@@ -505,10 +514,9 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
   if (need_scores && d.t_ctx) {
     // context saliency in the reference's order: fp64 scores of the source
     // rows against the context columns (numpy einsum bits), sequential mean
-    dim3 g((d.t_ctx + 63) / 64, (d.t_src + 63) / 64, d.BH);
-    isa::coarse_np_kernel<<<g, 128, 0, st>>>(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, nullptr, d.t_src,
-                                             d.t_src, d.t_ctx, d.D, d.scale, w.s_ctx);
-    ISA_LAUNCHED("coarse_np_kernel");
+    if ((rc = launch_coarse(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, nullptr, d.t_src, d.t_src, d.t_ctx,
+                            d.D, d.scale, w.s_ctx, d.BH, st)))
+      return rc;
     isa::ctx_mean_kernel<<<dim3((d.t_ctx + 127) / 128, d.BH), 128, 0, st>>>(w.s_ctx, (long long)d.t_src * d.t_ctx,
                                                                           d.t_ctx, d.t_src, d.t_ctx, w.ctx);
     ISA_LAUNCHED("ctx_mean_kernel");
@@ -549,10 +557,9 @@ int run_routing(const IsaShape* sh, const Dims& d, const IsaKnobs* kn, const voi
                                                    w.ctx_short);
   ISA_LAUNCHED("kvblk_from_sel_kernel");
   if (need_scores) {
-    dim3 g((d.t_new + 63) / 64, (d.T + 63) / 64, d.BH);
-    isa::coarse_np_kernel<<<g, 128, 0, st>>>(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, w.kv_blk, 0, d.T,
-                                             d.t_new, d.D, d.scale, w.s_new);
-    ISA_LAUNCHED("coarse_np_kernel");
+    if ((rc = launch_coarse(qc, (long long)d.T * d.D, kc, (long long)d.T * d.D, w.kv_blk, 0, d.T, d.t_new, d.D,
+                            d.scale, w.s_new, d.BH, st)))
+      return rc;
   }
   if (d.n_flat) {
     isa::SegInfo seg{d.l_src, d.l_ctx, d.t_src, d.t_ctx};
@@ -1450,12 +1457,8 @@ int isa_coarse_scores(int32_t bh, int32_t t_q, int32_t t_k, int32_t d, double sc
   if (!bh || !t_q || !t_k) return ISA_OK;
   if (!qc || !kc || !s || (reinterpret_cast<uintptr_t>(qc) & 15) || (reinterpret_cast<uintptr_t>(kc) & 15))
     return fail(ISA_ERR_LAYOUT, "qc/kc must be 16-byte aligned");
-  dim3 g((t_k + 63) / 64, (t_q + 63) / 64, bh);
-  isa::coarse_np_kernel<<<g, 128, 0, static_cast<cudaStream_t>(stream)>>>(qc, (long long)t_q * d, kc,
-                                                                          (long long)t_k * d, nullptr, 0, t_q, t_k, d,
-                                                                          scale, s);
-  ISA_LAUNCHED("coarse_np_kernel");
-  return ISA_OK;
+  return launch_coarse(qc, (long long)t_q * d, kc, (long long)t_k * d, nullptr, 0, t_q, t_k, d, scale, s, bh,
+                       static_cast<cudaStream_t>(stream));
 }
 
 int isa_ctx_saliency_f64(const double* s, int32_t bh, int64_t head_stride, int64_t row_stride, int32_t n_src,

@@ -180,33 +180,42 @@ __global__ void __launch_bounds__(128) pool_means_kernel(const Tin* __restrict__
 // lanes. So lane 0 accumulates d = 8g+6, 8g+4, 8g+2, 8g in that order, lane 1
 // d = 8g+7, 8g+5, 8g+3, 8g+1, and the dot is 0 + (lane0 + lane1). qc/kc are
 // fp32, so every product is exact in fp64 and numpy's separate mul + add equals
-// one fp64 FMA: the two-lane FMA chains below reproduce numpy's bits exactly
-// (tests/test_gpu_parity.py pins it against np.einsum; verified 100% equal for
-// D = 64 and 128, the head dims divisible by 8 the kernels take).
+// one fp64 FMA: two-lane FMA chains reproduce numpy's bits exactly
+// (tests/test_coarse_api.py pins s_coarse against the reference's np.einsum
+// output bit for bit, D = 64 and 128).
 //
 // s_out[bh][i][j] = scale * <qc[bh][i], kc[bh][col(j)]> for i < rows, j < n,
-// col(j) = kv_blk ? kv_blk[bh * n + j] : col0 + j. 64 x 64 output tile per
-// CTA, 128 threads = 64 thread PAIRS: the two threads of a pair own the same
-// 8 x 8 outputs, the even one numpy's lane 0 (even d), the odd one lane 1
-// (odd d), each a sequential FMA chain; the pair adds its lanes through one
-// shuffle at the end. 64 accumulators per thread and 16 operand loads per 64
-// DFMA (2 B/DFMA of shared-memory traffic: the SM's LDS bandwidth at the DFMA
-// rate); 2 CTAs (8 warps) per SM at 206 registers (3 CTAs spill: 384 vs
-// 342 us at cfg3; 4 CTAs: 1618 us). d is staged 8 at a time (= one numpy
-// group) in two alternating shared stages (one barrier per group); row strides
-// padded so a pair's two d rows sit in disjoint banks.
-// grid (ceil(n/64), ceil(rows/64), BH).
-// ----------------------------------------------------------------------------
-constexpr int kCnS = 72;  // stage row stride (doubles): +16 banks per d row
-#ifndef ISA_COARSE_MINB
-#define ISA_COARSE_MINB 2
-#endif
-__global__ void __launch_bounds__(128, ISA_COARSE_MINB) coarse_np_kernel(const float* __restrict__ qc, long long q_hstride,
-                                                           const float* __restrict__ kc, long long k_hstride,
-                                                           const int* __restrict__ kv_blk, int col0, int rows, int n,
-                                                           int D, double scale, double* __restrict__ s_out) {
-  __shared__ __align__(16) double As[2][8][kCnS];
-  __shared__ __align__(16) double Bs[2][8][kCnS];
+// col(j) = kv_blk ? kv_blk[bh * n + j] : col0 + j, on the fp64 tensor cores
+// (DMMA, mma.sync.m8n8k4 .f64).
+// Measured on B200 (tools/ubench/dmma_order.cu): an m8n8k4 DMMA accumulates
+// its k = 4 products as the sequential FMA chain k = 0, 1, 2, 3 into C, bit
+// for bit (0 mismatches in 262,144 outputs with fp32-valued operands). So one
+// DMMA per (numpy group, lane) with k ordered (6, 4, 2, 0) resp. (7, 5, 3, 1)
+// continues numpy's lane chains exactly, with C = the running lane
+// accumulator. Fragments come from shared memory once per 8 DMMAs of a warp
+// (0.75 B per FMA; an FMA-pipe kernel with 8 x 8 register tiles needs 2 B
+// and ran 330 vs 247 us at cfg3).
+// CTA: 64 x 64 outputs, 8 warps (2 x 4), warp tile 32 rows x 16 columns =
+// 4 x 2 m8n8 tiles x 2 lanes. d staged 16 at a time (two numpy groups), k-major
+// in shared memory with a 66-double row stride (conflict-free fragment
+// loads: 2 wavefronts, the minimum for 256 bytes), two stages.
+// grid (ceil(n/64), ceil(rows/64), BH), 256 threads.
+// k-row stride in doubles: 66 = 132 words = 4 banks mod 32, so the k rows
+// (6, 4, 2, 0) resp. (7, 5, 3, 1) a half-warp's fragment load touches start 8
+// banks apart and each half-warp's 16 doubles cover all 32 banks once
+constexpr int kDmS = 66;
+__device__ __forceinline__ void dmma_m8n8k4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+constexpr int kDmG = 2;  // numpy groups (of 8 d) staged per barrier
+__global__ void __launch_bounds__(256, 2) coarse_dmma_kernel(const float* __restrict__ qc, long long q_hstride,
+                                                             const float* __restrict__ kc, long long k_hstride,
+                                                             const int* __restrict__ kv_blk, int col0, int rows,
+                                                             int n, int D, double scale, double* __restrict__ s_out) {
+  __shared__ __align__(16) double As[2][8 * kDmG][kDmS];  // [stage][d within the staged groups][row]
+  __shared__ __align__(16) double Bs[2][8 * kDmG][kDmS];  // [stage][d within the staged groups][col]
   __shared__ int colrow[64];
   const int bh = blockIdx.z;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
@@ -217,63 +226,80 @@ __global__ void __launch_bounds__(128, ISA_COARSE_MINB) coarse_np_kernel(const f
     colrow[threadIdx.x] = j < n ? (kv_blk ? kv_blk[(long long)bh * n + j] : col0 + j) : -1;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 1, pair = threadIdx.x >> 1;
-  const int ty = pair >> 3, tx = pair & 7;  // rows ty + 8 r, cols tx + 8 c
-  double acc[8][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp >> 2) * 32, wc = (warp & 3) * 16;  // warp tile origin (rows, cols)
+  const int fr = lane >> 2, fk = lane & 3;                 // fragment row/col and k slot
+  double acc[2][4][2][2];  // [numpy lane][m tile][n tile][2 values]
 #pragma unroll
-  for (int r = 0; r < 8; ++r)
+  for (int l = 0; l < 2; ++l)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
-  // loaders: thread -> row tid/2 (of 64), 4 consecutive d, for both operands;
-  // group g+1 is fetched into registers before group g's FMAs
-  const int lr = threadIdx.x >> 1, ld = (threadIdx.x & 1) * 4;
-  const int gi = i0 + lr, gj = colrow[lr];
-  const float* arow = gi < rows ? qb + (long long)gi * D + ld : nullptr;
-  const float* brow = gj >= 0 ? kb + (long long)gj * D + ld : nullptr;
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int t = 0; t < 2; ++t) acc[l][m][t][0] = acc[l][m][t][1] = 0.0;
+  // loaders: threads 0-127 stage A (row tid/2), 128-255 stage B (col (tid-128)/2); 4 d of each group
+  const int lt = threadIdx.x & 127, lr = lt >> 1, ld = (lt & 1) * 4;
+  const bool loads_a = threadIdx.x < 128;
+  const float* src;
+  if (loads_a) {
+    const int gi = i0 + lr;
+    src = gi < rows ? qb + (long long)gi * D + ld : nullptr;
+  } else {
+    const int gj = colrow[lr];
+    src = gj >= 0 ? kb + (long long)gj * D + ld : nullptr;
+  }
   const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow)) : zero4;
-  float4 b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow)) : zero4;
-  auto stage_in = [&](int buf) {
-    As[buf][ld + 0][lr] = a4.x; As[buf][ld + 1][lr] = a4.y; As[buf][ld + 2][lr] = a4.z; As[buf][ld + 3][lr] = a4.w;
-    Bs[buf][ld + 0][lr] = b4.x; Bs[buf][ld + 1][lr] = b4.y; Bs[buf][ld + 2][lr] = b4.z; Bs[buf][ld + 3][lr] = b4.w;
+  float4 x4[kDmG];
+  auto fetch = [&](int st) {  // st-th stage: groups kDmG * st ...
+#pragma unroll
+    for (int h = 0; h < kDmG; ++h) x4[h] = src ? __ldg(reinterpret_cast<const float4*>(src + 8 * (kDmG * st + h))) : zero4;
   };
+  auto stage_in = [&](int buf) {
+    double(*dst)[kDmS] = loads_a ? As[buf] : Bs[buf];
+#pragma unroll
+    for (int h = 0; h < kDmG; ++h) {
+      dst[8 * h + ld + 0][lr] = x4[h].x; dst[8 * h + ld + 1][lr] = x4[h].y;
+      dst[8 * h + ld + 2][lr] = x4[h].z; dst[8 * h + ld + 3][lr] = x4[h].w;
+    }
+  };
+  fetch(0);
   stage_in(0);
   __syncthreads();
-  const int G = D / 8;
-  for (int g = 0; g < G; ++g) {
-    const int buf = g & 1;
-    if (g + 1 < G) {
-      a4 = arow ? __ldg(reinterpret_cast<const float4*>(arow + 8 * (g + 1))) : zero4;
-      b4 = brow ? __ldg(reinterpret_cast<const float4*>(brow + 8 * (g + 1))) : zero4;
-    }
+  const int NS = D / (8 * kDmG);
+  for (int st = 0; st < NS; ++st) {
+    const int buf = st & 1;
+    if (st + 1 < NS) fetch(st + 1);
 #pragma unroll
-    for (int m = 3; m >= 0; --m) {  // numpy's chain order a3, a2, a1, a0 within the group
-      const int dd = 2 * m + lane;
-      double bv[8];
+    for (int h = 0; h < kDmG; ++h)
 #pragma unroll
-      for (int t = 0; t < 8; ++t) bv[t] = Bs[buf][dd][tx + 8 * t];
+      for (int l = 0; l < 2; ++l) {
+        const int kd = 8 * h + 6 - 2 * fk + l;  // k slot fk: d = 6, 4, 2, 0 (lane 0) / 7, 5, 3, 1 (lane 1)
+        double af[4], bf[2];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const double a = As[buf][dd][ty + 8 * r];
+        for (int m = 0; m < 4; ++m) af[m] = As[buf][kd][wr + 8 * m + fr];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[r][c] = fma(a, bv[c], acc[r][c]);
+        for (int t = 0; t < 2; ++t) bf[t] = Bs[buf][kd][wc + 8 * t + fr];
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int t = 0; t < 2; ++t) dmma_m8n8k4(acc[l][m][t], af[m], bf[t]);
       }
-    }
-    if (g + 1 < G) stage_in(buf ^ 1);
+    if (st + 1 < NS) stage_in(buf ^ 1);
     __syncthreads();
   }
-  // dot = 0 + (lane0 + lane1); the even thread stores columns c < 4, the odd one c >= 4
+  // C fragment: row 8m + lane/4, cols 8t + 2 (lane % 4) + {0, 1}; dot = 0 + (lane0 + lane1)
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int i = i0 + ty + 8 * r;
+  for (int m = 0; m < 4; ++m) {
+    const int i = i0 + wr + 8 * m + fr;
+    if (i >= rows) continue;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const double other = __shfl_xor_sync(0xffffffffu, acc[r][c], 1);
-      const double dot = lane ? __dadd_rn(other, acc[r][c]) : __dadd_rn(acc[r][c], other);
-      const int j = j0 + tx + 8 * c;
-      if ((c >> 2) == lane && i < rows && j < n)
-        s_out[((long long)bh * rows + i) * n + j] = scale * __dadd_rn(0.0, dot);
-    }
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = j0 + wc + 8 * t + 2 * fk + e;
+        if (j < n)
+          s_out[((long long)bh * rows + i) * n + j] =
+              scale * __dadd_rn(0.0, __dadd_rn(acc[0][m][t][e], acc[1][m][t][e]));
+      }
   }
 }
 
@@ -281,7 +307,7 @@ __global__ void __launch_bounds__(128, ISA_COARSE_MINB) coarse_np_kernel(const f
 // K2b: context saliency = s_coarse[:, :, :t_src, t_src:].mean(axis=2)
 // (coarse.py:155) in numpy's order: the reduction over the (outer) query-block
 // axis adds rows sequentially, ((s_0 + s_1) + s_2) + ..., then divides by
-// t_src. `s_ctx` holds the t_src x t_ctx scores from coarse_np_kernel (same
+// t_src. `s_ctx` holds the t_src x t_ctx scores from coarse_dmma_kernel (same
 // bits as the reference's s_coarse), so the means are bit-identical too.
 // Element (bh, i, c) at s + bh * head_stride + i * row_stride + c. Thread per
 // context column. grid (ceil(t_ctx/128), BH).
