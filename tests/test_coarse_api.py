@@ -93,7 +93,7 @@ def test_matches_reference_golden(name):
     for key, t in (("qc", cs.qc), ("kc", cs.kc), ("vc", cs.vc)):
         assert isinstance(t, np.ndarray)
         np.testing.assert_array_equal(t, g[key], err_msg=key)
-    # the fp64 scores are numpy einsum's own bits (coarse_np_kernel)
+    # the fp64 scores are numpy einsum's own bits (coarse_dmma_kernel)
     np.testing.assert_array_equal(cs.s_coarse, g["s_coarse"])
     icl = P.IclLayout(ls, lc)
     sel = rank_context(cs, icl, a_s)
@@ -115,7 +115,7 @@ def test_matches_reference_golden(name):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", CASES)
 def test_pipeline_saliency_bits_and_selection(name):
-    """The fused pipeline's context saliency (coarse_np_kernel over the source
+    """The fused pipeline's context saliency (coarse_dmma_kernel over the source
     rows x context columns, then ctx_mean_kernel) equals the reference's
     s_coarse[:, :, :T_src, T_src:].mean(axis=2) bit for bit (coarse.py:155),
     so duplicated and near-tied context blocks at the top-k boundary select

@@ -132,7 +132,7 @@ def test_bench_inputs_cfg3_all_heads():
     for h in range(H):
         qh, kh, vh = (t[:, h:h + 1].float().cpu().numpy() for t in (q, k, v))
         r = O.isa_routing(qh, kh, vh, L, L)
-        # the saliency scores themselves: numpy's bits (coarse_np_kernel + ctx_mean_kernel)
+        # the saliency scores themselves: numpy's bits (coarse_dmma_kernel + ctx_mean_kernel)
         np.testing.assert_array_equal(ctx[:, h:h + 1], r.ctx_scores, err_msg=f"head {h}")
         np.testing.assert_array_equal(sel[:, h:h + 1], r.selection, err_msg=f"head {h}")
         np.testing.assert_array_equal(sharp[:, h:h + 1], r.sharp, err_msg=f"head {h}")
