@@ -367,22 +367,26 @@ def run_ours(args, rank, world, local_rank):
     # with the single fused grid (ISA_FLAG_FUSED_GRID), so both see the same clocks.
     ev_a = [make_events() for _ in range(args.steps)]
     ev_b = [make_events() for _ in range(args.steps)]
+    ev_c = [make_events() for _ in range(args.steps)]
     torch.cuda.synchronize()
     for i_ in range(args.steps):
         _call_with_events(prep, ev_a[i_][1], 0)
         _call_with_events(prep, ev_b[i_][1], N.FLAG_FUSED_GRID)
+        _call_with_events(prep, ev_c[i_][1], N.FLAG_SINGLE_CTA)
     torch.cuda.synchronize()
     shipped_alt = mean_stages([stages(e_[0]) for e_ in ev_a])
     fused_alt = mean_stages([stages(e_[0]) for e_ in ev_b])
+    single_alt = mean_stages([stages(e_[0]) for e_ in ev_c])
     if world > 1:
         shipped = shipped_alt
     stage = {"coarse": shipped["coarse"], "select": shipped["select"], "split": shipped["split"],
              "attention": shipped["attn"], "exact_k6": shipped["exact"], "taylor": shipped["taylor"],
              "ab_loop": {"shipped_two_launches": shipped_alt["attn"], "fused_single_grid": fused_alt["attn"],
                          "shipped_exact_k6": shipped_alt["exact"], "shipped_taylor": shipped_alt["taylor"],
+                         "single_cta_exact_k6": single_alt["exact"],
                          "steps": args.steps,
-                         "note": "shipped and fused-grid steps alternated in one loop after the timed region "
-                                 "(same clocks); per-launch CUDA events"}}
+                         "note": "shipped, fused-grid and single-CTA-K6 steps alternated in one loop after the "
+                                 "timed region (same clocks); per-launch CUDA events"}}
     peaks = _peaks()
     # K6 runs ~18 ms inside a ~23 ms step: a kernel timed on its own at burst
     # clocks, not a seconds-long sustained run -> the burst peak
@@ -411,7 +415,8 @@ def run_ours(args, rank, world, local_rank):
                     "it); compute_only_ms = the same schedule without the gathers (max over ranks)"},
         "gpu_launches": launches * args.steps,
         "roofline": {
-            "kernel": "gba_attention_kernel<128, MODE_EXACT> (K6, the sharp branch: the dominant launch)",
+            "kernel": "gba_attention_pair_kernel<128, MODE_EXACT> (K6 on CTA pairs, cta_group::2: the sharp "
+                      "branch, the dominant launch)",
             "bound": "tensor", "achieved": exact_tflops, "peak": peak_tc, "unit": "TFLOP/s",
             "frac": exact_tflops / peak_tc, "traffic": prof.get("k6_dram_bytes"),
             "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: K6 runs ~18 ms per step, not a seconds-long "

@@ -86,6 +86,8 @@ typedef struct IsaKnobs {
 /* D = 128: the sharp and flat items in ONE grid (gba_isa_hybrid_kernel)
  * instead of the default K6 launch + Taylor launch (A/B measurements). */
 #define ISA_FLAG_FUSED_GRID 8
+/* D = 128: run K6 on single CTAs instead of CTA pairs (cta_group::2; A/B). */
+#define ISA_FLAG_SINGLE_CTA 16
 /* Force the D = 128 Taylor-branch kernel for every head instead of the
  * per-head automatic choice (taylor_pick_kernel): K7 = row-major pair-union
  * tiles, K7T = transposed per-block tiles. Same operator, test/A-B hooks. */

@@ -52,6 +52,7 @@ FLAG_SEPARATE_BRANCHES = 1
 FLAG_TAYLOR_K7 = 2
 FLAG_TAYLOR_K7T = 4
 FLAG_FUSED_GRID = 8
+FLAG_SINGLE_CTA = 16
 
 # err_word bits (include/isa_b200.h ISA_ERRBIT_*)
 ERRBIT_INPUT = 1

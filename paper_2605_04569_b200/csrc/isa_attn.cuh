@@ -218,7 +218,7 @@ __device__ __forceinline__ int query_block(const AttnParams& p, int bh, int item
   return p.qlist[(long long)bh * p.n_qblk + pos];
 }
 
-template <int D, int MODE>
+template <int D, int MODE, bool kPair = false>
 __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensorMap& tm_k, const CUtensorMap& tm_v,
                                          const CUtensorMap& tm_kc, const CUtensorMap& tm_vc, const AttnParams& p,
                                          const int item, const int bh) {
@@ -227,14 +227,22 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + L::kQOff;
   uint8_t* sKV = smem + L::kKvOff;
+  // kPair (cta_group::2, K6/K8 at D = 128): every K/V ring entry is a half
+  // tile in each CTA of the pair (K: one 64-key block; V: one 64-column d
+  // plane of both blocks), so the same ring bytes hold twice the slots.
+  static_assert(!kPair || (MODE != MODE_TAYLOR && D == 128), "CTA pairs run the exact/dense branch at D = 128");
+  constexpr int kSlots = kPair ? 2 * kKvStages : kKvStages;
+  constexpr int kSlotBytes = kPair ? L::kTileBytes / 2 : L::kTileBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* q_full = bars + 0;           // [2]
-  uint64_t* kv_full = bars + 2;          // [kKvStages]
-  uint64_t* kv_empty = bars + 2 + kKvStages;  // [kKvStages]
-  uint64_t* s_full = bars + 2 + 2 * kKvStages;     // [2]
-  uint64_t* p_full = bars + 4 + 2 * kKvStages;     // [2]
-  uint64_t* o_full = bars + 6 + 2 * kKvStages;     // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kKvStages);
+  uint64_t* kv_full = bars + 2;          // [kSlots]
+  uint64_t* kv_empty = bars + 2 + kSlots;  // [kSlots]
+  uint64_t* s_full = bars + 2 + 2 * kSlots;     // [2]
+  uint64_t* p_full = bars + 4 + 2 * kSlots;     // [2]
+  uint64_t* o_full = bars + 6 + 2 * kSlots;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kSlots);
+  static_assert((8 + 2 * kSlots) * 8 + 4 <= 256, "barrier area");
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -243,20 +251,28 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
   if (threadIdx.x == 0) {
     mbar_init(&q_full[0], 1);
     mbar_init(&q_full[1], 1);
-    for (int s = 0; s < kKvStages; ++s) {
+    for (int s = 0; s < kSlots; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 4);
+      mbar_init(&p_full[s], kPair ? 8 : 4);  // pair: the leader's copy counts both CTAs' softmax warps
       mbar_init(&o_full[s], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 8) tmem_alloc<512>(tmem_slot);
+  if (warp == 8) {
+    if constexpr (kPair)
+      tmem_alloc2<512>(tmem_slot);
+    else
+      tmem_alloc<512>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA signal
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -278,17 +294,22 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
       const int hh = bh % p.H, bb = bh / p.H;
-      const int first_u = query_block<MODE>(p, bh, item, 0);
+      int first_u = query_block<MODE>(p, bh, item, 0);
+      if (first_u < 0) first_u = query_block<MODE>(p, bh, 0, 0);  // pair padding CTA: load any valid rows
       if (leader) {
         for (int s = 0; s < 2; ++s) {
-          mbar_arrive_expect_tx(&q_full[s], L::kTileBytes);
+          if (!kPair || rank == 0) mbar_arrive_expect_tx(&q_full[s], kPair ? 2 * L::kTileBytes : L::kTileBytes);
           for (int half = 0; half < 2; ++half) {
             int u = query_block<MODE>(p, bh, item, 2 * s + half);
             if (u < 0) u = first_u;
             const int tok = blk_tok0(p, u);
-            for (int pl = 0; pl < L::kPlanes; ++pl)
-              tma_load_4d(sQ + s * L::kTileBytes + pl * 16384 + half * 8192, &tm_q, &q_full[s], pl * 64, tok, hh,
-                          bb, pol_q);
+            for (int pl = 0; pl < L::kPlanes; ++pl) {
+              uint8_t* dst = sQ + s * L::kTileBytes + pl * 16384 + half * 8192;
+              if constexpr (kPair)
+                tma_load_4d_pair(dst, &tm_q, &q_full[s], pl * 64, tok, hh, bb, pol_q);
+              else
+                tma_load_4d(dst, &tm_q, &q_full[s], pl * 64, tok, hh, bb, pol_q);
+            }
           }
         }
       }
@@ -298,13 +319,12 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       constexpr int kStages = (MODE == MODE_TAYLOR) ? 2 : 1;
       int c = 0;
       auto push = [&](const TileSrc& t, int is_v) {
-        const int slot = c % kKvStages;
-        const int use = c / kKvStages;
+        const int slot = c % kSlots;
+        const int use = c / kSlots;
         if (use > 0) mbar_wait(&kv_empty[slot], (use - 1) & 1);
         __syncwarp();
         if (leader) {
-          mbar_arrive_expect_tx(&kv_full[slot], L::kTileBytes);
-          uint8_t* dst = sKV + slot * L::kTileBytes;
+          uint8_t* dst = sKV + slot * kSlotBytes;
           const CUtensorMap* tm;
           int c2, c3;
           if (t.centroid) {
@@ -316,10 +336,26 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
             c2 = hh;
             c3 = bb;
           }
-          for (int half = 0; half < 2; ++half) {
-            const int tok = half ? t.tok1 : t.tok0;
-            for (int pl = 0; pl < L::kPlanes; ++pl)
-              tma_load_4d(dst + pl * 16384 + half * 8192, tm, &kv_full[slot], pl * 64, tok, c2, c3, pol_kv);
+          if constexpr (kPair) {
+            // K: this CTA's 64-key block, both d planes ([plane][64 keys][64 d]);
+            // V: this CTA's d plane of both blocks ([128 keys][64 d])
+            if (rank == 0) mbar_arrive_expect_tx(&kv_full[slot], 2 * kSlotBytes);
+            if (!is_v) {
+              const int tok = rank ? t.tok1 : t.tok0;
+              for (int pl = 0; pl < L::kPlanes; ++pl)
+                tma_load_4d_pair(dst + pl * 8192, tm, &kv_full[slot], pl * 64, tok, c2, c3, pol_kv);
+            } else {
+              for (int half = 0; half < 2; ++half)
+                tma_load_4d_pair(dst + half * 8192, tm, &kv_full[slot], static_cast<int>(rank) * 64,
+                                 half ? t.tok1 : t.tok0, c2, c3, pol_kv);
+            }
+          } else {
+            mbar_arrive_expect_tx(&kv_full[slot], L::kTileBytes);
+            for (int half = 0; half < 2; ++half) {
+              const int tok = half ? t.tok1 : t.tok0;
+              for (int pl = 0; pl < L::kPlanes; ++pl)
+                tma_load_4d(dst + pl * 16384 + half * 8192, tm, &kv_full[slot], pl * 64, tok, c2, c3, pol_kv);
+            }
           }
           progress(0, c + 1);
         }
@@ -355,11 +391,14 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           }
         }
       }
-    } else if (warp == 8) {
+      if constexpr (kPair) {  // drain: the leader's multicast releases of our slots have all landed
+        for (int e = c > kSlots ? c - kSlots : 0; e < c; ++e) mbar_wait(&kv_empty[e % kSlots], (e / kSlots) & 1);
+      }
+    } else if (warp == 8 && (!kPair || rank == 0)) {
       // ------------------------------------------------------------ MMA issuer
       // Whole warp waits; one elected lane issues tcgen05.mma / commit.
-      constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D, 0, 1);
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(kPair ? 256 : 128, 128, 0, 0);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(kPair ? 256 : 128, D, 0, 1);
       const uint32_t sq = smem_u32(sQ);
       const uint32_t skv = smem_u32(sKV);
       const bool leader = elect_one();
@@ -369,35 +408,51 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       const uint64_t dq_base = sdesc_sw128_base(sq, 16, 1024);
       const uint64_t dk_base = sdesc_sw128_base(skv, 16, 1024);
       const uint64_t dv_base = sdesc_sw128_base(skv, 16384, 1024);
+      constexpr int kKPlane = kPair ? 8192 : 16384;  // K tile d-plane stride (pair: 64-key half tiles)
       auto issue_qk = [&](int s, int slot) {
         if (leader) {
           const uint64_t da = dq_base + static_cast<uint64_t>((s * L::kTileBytes) >> 4);
-          const uint64_t db = dk_base + static_cast<uint64_t>((slot * L::kTileBytes) >> 4);
+          const uint64_t db = dk_base + static_cast<uint64_t>((slot * kSlotBytes) >> 4);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-            mma_ss(tmem + s * 128, da + off, db + off, idesc_qk, kk > 0);
+            const uint64_t oa = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+            const uint64_t ob = ((kk >> 2) * kKPlane + (kk & 3) * 32) >> 4;
+            if constexpr (kPair)
+              mma_ss2(tmem + s * 128, da + oa, db + ob, idesc_qk, kk > 0);
+            else
+              mma_ss(tmem + s * 128, da + oa, db + ob, idesc_qk, kk > 0);
           }
         }
         __syncwarp();
       };
       auto issue_pv = [&](int s, int slot, uint32_t acc) {
         if (leader) {
-          const uint64_t db = dv_base + static_cast<uint64_t>((slot * L::kTileBytes) >> 4);
+          const uint64_t db = dv_base + static_cast<uint64_t>((slot * kSlotBytes) >> 4);
           const uint32_t ta = tmem + s * 128 + 64;
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma_ts(tmem + 256 + s * 128, ta + kk * 8, db + static_cast<uint64_t>((kk * 2048) >> 4), idesc_pv,
-                   (acc | kk) != 0);
+          for (int kk = 0; kk < 8; ++kk) {
+            if constexpr (kPair)
+              mma_ts2(tmem + 256 + s * 128, ta + kk * 8, db + static_cast<uint64_t>((kk * 2048) >> 4), idesc_pv,
+                      (acc | kk) != 0);
+            else
+              mma_ts(tmem + 256 + s * 128, ta + kk * 8, db + static_cast<uint64_t>((kk * 2048) >> 4), idesc_pv,
+                     (acc | kk) != 0);
+          }
         }
         __syncwarp();
       };
       auto commit = [&](uint64_t* bar) {
-        if (leader) mma_commit(bar);
+        if (leader) {
+          if constexpr (kPair)
+            mma_commit_pair(bar);
+          else
+            mma_commit(bar);
+        }
         __syncwarp();
       };
-      auto wait_entry = [&](int e) { mbar_wait(&kv_full[e % kKvStages], (e / kKvStages) & 1); };
-      auto release = [&](int e) { commit(&kv_empty[e % kKvStages]); };
+      auto wait_p = [&](int s, uint32_t parity) { mbar_wait(&p_full[s], parity); };
+      auto wait_entry = [&](int e) { mbar_wait(&kv_full[e % kSlots], (e / kSlots) & 1); };
+      auto release = [&](int e) { commit(&kv_empty[e % kSlots]); };
       mbar_wait(&q_full[0], 0);
       mbar_wait(&q_full[1], 0);
       if (MODE == MODE_TAYLOR) {
@@ -405,7 +460,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           wait_entry(s);
           __syncwarp();
           tc_fence_after();
-          issue_qk(s, s % kKvStages);
+          issue_qk(s, s % kSlots);
           commit(&s_full[s]);
           release(s);
         }
@@ -413,18 +468,18 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           const int base = 2 + 4 * (i - 1);
           for (int s = 0; s < 2; ++s) {
             const int ev = base + 2 * s, ek = ev + 1;
-            mbar_wait(&p_full[s], (i - 1) & 1);
+            wait_p(s, (i - 1) & 1);
             if (leader && ISA_TRACE_MODE == 2) ISA_TSTAMP(i, s, 6);
             wait_entry(ev);
             if (leader && ISA_TRACE_MODE == 2) ISA_TSTAMP(i, s, 5);
             __syncwarp();
             tc_fence_after();
-            issue_pv(s, ev % kKvStages, i > 1);
+            issue_pv(s, ev % kSlots, i > 1);
             release(ev);
             wait_entry(ek);
             __syncwarp();
             tc_fence_after();
-            issue_qk(s, ek % kKvStages);
+            issue_qk(s, ek % kSlots);
             commit(&s_full[s]);
             if (leader && ISA_TRACE_MODE == 2) ISA_TSTAMP(i, s, 7);
             release(ek);
@@ -433,11 +488,11 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         }
         for (int s = 0; s < 2; ++s) {
           const int ev = 4 * n_kv - 2 + s;
-          mbar_wait(&p_full[s], (n_kv - 1) & 1);
+          wait_p(s, (n_kv - 1) & 1);
           wait_entry(ev);
           __syncwarp();
           tc_fence_after();
-          issue_pv(s, ev % kKvStages, n_kv > 1);
+          issue_pv(s, ev % kSlots, n_kv > 1);
           commit(&o_full[s]);
           release(ev);
         }
@@ -457,12 +512,12 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           if (leader && ISA_TRACE_MODE != 2) ISA_TSTAMP(i, 0, 5);
           if (leader) progress(1, 1000 * i + 1);
           for (int s = 0; s < 2; ++s) {
-            mbar_wait(&p_full[s], (i - 1) & 1);
+            wait_p(s, (i - 1) & 1);
             if (leader && ISA_TRACE_MODE != 2) ISA_TSTAMP(i, s, 6);
             __syncwarp();
             tc_fence_after();
-            issue_pv(s, ev % kKvStages, i > 1);
-            issue_qk(s, ek % kKvStages);
+            issue_pv(s, ev % kSlots, i > 1);
+            issue_qk(s, ek % kSlots);
             commit(&s_full[s]);
             if (leader && ISA_TRACE_MODE != 2) ISA_TSTAMP(i, s, 7);
           }
@@ -472,10 +527,10 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         const int ev = 2 * n_kv - 1;
         wait_entry(ev);
         for (int s = 0; s < 2; ++s) {
-          mbar_wait(&p_full[s], (n_kv - 1) & 1);
+          wait_p(s, (n_kv - 1) & 1);
           __syncwarp();
           tc_fence_after();
-          issue_pv(s, ev % kKvStages, n_kv > 1);
+          issue_pv(s, ev % kSlots, n_kv > 1);
           commit(&o_full[s]);
         }
         release(ev);
@@ -485,6 +540,15 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
   } else {
     // -------------------------------------------------------------- softmax
     setmaxnreg_inc<kSoftmaxRegs>();
+    auto arrive_p = [&](int st) {  // P(i) of stage st written to TMEM
+      if constexpr (kPair) {
+        if (rank) {
+          mbar_arrive_leader(&p_full[st]);
+          return;
+        }
+      }
+      mbar_arrive(&p_full[st]);
+    };
     const int s = warp >> 2;                  // Q tile (stage)
     const int row = (warp & 3) * 32 + lane;   // row in the 128-row tile == TMEM lane
     const int qb = 2 * s + (row >> 6);        // query block 0..3 of this CTA
@@ -572,7 +636,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[s]);
+        if (lane == 0) arrive_p(s);
         if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 4);
         l += 1.f;
         continue;
@@ -605,7 +669,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[s]);
+        if (lane == 0) arrive_p(s);
         if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 4);
         l += 1.f;
         continue;
@@ -689,7 +753,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[s]);
+        if (lane == 0) arrive_p(s);
         ISA_COUNT(MODE, 3);
         continue;
       }
@@ -781,7 +845,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
           ISA_COUNT(MODE, 0);
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[s]);
+          if (lane == 0) arrive_p(s);
           if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 4);
           const float2 s2 = fadd2(fadd2(sp2[0], sp2[1]), fadd2(sp2[2], sp2[3]));
           l += s2.x + s2.y;
@@ -922,7 +986,7 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[s]);
+      if (lane == 0) arrive_p(s);
       if ((warp & 3) == ISA_TRACE_Q && lane == 0 && (MODE == MODE_TAYLOR) == (ISA_TRACE_MODE == 2)) ISA_TSTAMP(i, s, 4);
       const float2 s2 = fadd2(fadd2(sm2[0], sm2[1]), fadd2(sm2[2], sm2[3]));
       l += ((sm[0] + sm[1]) + (sm[2] + sm[3])) + (s2.x + s2.y);
@@ -977,9 +1041,29 @@ __device__ __forceinline__ void gba_body(const CUtensorMap& tm_q, const CUtensor
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // the peer's MMAs / signals into this CTA are complete
   if (warp == 8) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    if constexpr (kPair)
+      tmem_dealloc2<512>(tmem);
+    else
+      tmem_dealloc<512>(tmem);
+  }
+}
+
+// K6 / K8 on CTA pairs (cta_group::2, cluster of 2 along x): items 2c and
+// 2c+1 of a head run as one M = 256 MMA stream; each SM loads half of every
+// K/V tile and feeds half of each MMA's B operand.
+template <int D, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gba_attention_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kc,
+                              const __grid_constant__ CUtensorMap tm_vc, const AttnParams p) {
+  gba_body<D, MODE, true>(tm_q, tm_k, tm_v, tm_kc, tm_vc, p, blockIdx.x, blockIdx.y);
+  if (p.head_done) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(p.head_done + blockIdx.y, 1);
   }
 }
 

@@ -255,12 +255,32 @@ int launch_resid_tiled(dim3 g, const float* qc, const float* kc, const float* vc
   return ISA_OK;
 }
 
+// K6 / K8 at D = 128 run on CTA pairs (cta_group::2, isa_attn.cuh) unless
+// the call sets ISA_FLAG_SINGLE_CTA (or the process sets ISA_PAIR=0): A/B.
+thread_local bool g_single_cta = false;
+bool pair_mode() {
+  static bool env_off = [] {
+    const char* e = getenv("ISA_PAIR");
+    return e && e[0] == '0';
+  }();
+  return !env_off && !g_single_cta;
+}
+
 template <int D, int MODE>
 int launch_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tkc,
                      const CUtensorMap& tvc, const isa::AttnParams& p, int items, int BH, cudaStream_t st) {
   using L = isa::AttnSmem<D>;
-  if (int rc_ = ensure_smem((const void*)isa::gba_attention_kernel<D, MODE>, L::kAlloc)) return rc_;
   if (items < 1) return ISA_OK;
+  if constexpr (D == 128 && MODE != isa::MODE_TAYLOR) {
+    if (pair_mode()) {
+      if (int rc_ = ensure_smem((const void*)isa::gba_attention_pair_kernel<D, MODE>, L::kAlloc)) return rc_;
+      isa::gba_attention_pair_kernel<D, MODE><<<dim3((items + 1) & ~1, BH), isa::kThreads, L::kAlloc, st>>>(
+          tq, tk, tv, tkc, tvc, p);
+      ISA_LAUNCHED("gba_attention_pair_kernel");
+      return ISA_OK;
+    }
+  }
+  if (int rc_ = ensure_smem((const void*)isa::gba_attention_kernel<D, MODE>, L::kAlloc)) return rc_;
   dim3 grid(items, BH);
   isa::gba_attention_kernel<D, MODE><<<grid, isa::kThreads, L::kAlloc, st>>>(tq, tk, tv, tkc, tvc, p);
   ISA_LAUNCHED("gba_attention_kernel");
@@ -735,6 +755,7 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
                  int32_t* err_word, const IsaEvents* events, float* lse, cudaStream_t st,
                  int32_t* head_done = nullptr, int32_t* done_inc = nullptr) {
   int rc;
+  g_single_cta = (knobs->flags & ISA_FLAG_SINGLE_CTA) != 0;
   record(events, 0, st);
   if ((rc = run_routing(shape, d, knobs, q, k, v, w, pinned, routing, err_word, events, st))) return rc;
   // ---- stage 4 (+ fused stage 5)
@@ -804,7 +825,8 @@ int forward_impl(const IsaShape* shape, const IsaKnobs* knobs, const Dims& d, co
     // completion when signalling (isa_forward_signal).
     ps.head_done = head_done;
     pf.head_done = head_done;
-    if (done_inc) *done_inc = (d.n_sharp ? d.items_s : 0) + d.items_f + (pf.n_qblk + 1) / 2;
+    const int k6_ctas = d.n_sharp ? (pair_mode() ? (d.items_s + 1) & ~1 : d.items_s) : 0;  // CTAs of the K6 grid
+    if (done_inc) *done_inc = k6_ctas + d.items_f + (pf.n_qblk + 1) / 2;
     if (d.n_sharp)
       if ((rc = launch_attention_d<isa::MODE_EXACT>(d.D, tq, tk, tv, tq, tq, ps, d.items_s, d.BH, st))) return rc;
     record(events, 4, st);

@@ -51,3 +51,34 @@ def test_sharded_schedule_world1_matches_plain(mode, chunk):
         layer(out_full)
         torch.cuda.synchronize()
         assert torch.equal(out_full, ref)
+
+
+def test_cta_pair_k6_matches_single_cta():
+    """K6 / K8 on CTA pairs (cta_group::2, the default at D = 128) against the
+    single-CTA kernel (ISA_FLAG_SINGLE_CTA): same routing, same outputs to the
+    last bf16 bit or within one bf16 ulp (the pair MMA accumulates each output
+    over the same k order; only the issue differs), odd item counts included
+    (a padding CTA completes the last pair)."""
+    import ctypes
+
+    import paper_2605_04569_b200 as P
+    from paper_2605_04569_b200 import _native as N
+    from paper_2605_04569_b200.pipeline import _ptr
+
+    for S, ls in ((8192, 4096), (4096 + 640, 4096)):  # T = 128 (items even) / 74 (n_sharp 37: odd items)
+        q, k, v = _inputs(3, S, seed=S)
+        icl, cfg = P.IclLayout(ls, S - ls), P.IsaConfig(strict=(S - ls) % 64 == 0)
+        outs = []
+        for flags in (0, N.FLAG_SINGLE_CTA):
+            prep = P.prepare(q, k, v, icl, cfg)
+            inp = prep.inp
+            kn = N.IsaKnobs(inp.knobs.scale, inp.knobs.k_ctx, inp.knobs.n_flat, inp.knobs.k_mask,
+                            inp.knobs.softmax_first, flags, inp.knobs.gamma, inp.knobs.residual_softmax)
+            N.check(N.load().isa_forward(ctypes.byref(inp.shape), ctypes.byref(kn), _ptr(inp.q), _ptr(inp.k),
+                                         _ptr(inp.v), _ptr(prep.out), _ptr(prep.ws), prep.nbytes, None, None,
+                                         _ptr(prep.err), None, torch.cuda.current_stream().cuda_stream))
+            outs.append(prep.out.float().clone())
+        d = (outs[0] - outs[1]).abs().max().item()
+        assert d <= 8e-3, d
+    dq, dk, dv = _inputs(2, 4096, seed=9)
+    assert torch.isfinite(P.dense_attention(dq, dk, dv).float()).all()
