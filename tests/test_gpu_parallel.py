@@ -65,7 +65,7 @@ def test_cta_pair_k6_matches_single_cta():
     from paper_2605_04569_b200 import _native as N
     from paper_2605_04569_b200.pipeline import _ptr
 
-    for S, ls in ((8192, 4096), (4096 + 640, 4096)):  # T = 128 (items even) / 74 (n_sharp 37: odd items)
+    for S, ls in ((8192, 4096), (4096 + 512, 4096)):  # T = 128 (16 K6 items) / 72 (n_sharp 36: 9 items, odd)
         q, k, v = _inputs(3, S, seed=S)
         icl, cfg = P.IclLayout(ls, S - ls), P.IsaConfig(strict=(S - ls) % 64 == 0)
         outs = []
