@@ -372,27 +372,49 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
 }
 
 // ---------------------------------------------------------------- dQ (query-major, tcgen05)
+#ifdef ISA_TRACE_DQ  // tools/trace_dq.py: stamp the dQ kernel instead of dK/dV
+#define DQ_TSTAMP(step, stage, slot) ISA_TSTAMP(step, stage, slot)
+#else
+#define DQ_TSTAMP(step, stage, slot) \
+  do {                               \
+  } while (0)
+#endif
 // CTA = 128 query rows = a pair of query blocks: sharp pairs stream every
 // K_new block pair (reference.py:173-225); flat pairs (the Taylor plan's
 // (item, stage) streams) stream their exact-union tiles, then every centroid
-// tile (taylor.py:262-285). Q/dO resident, K/V double-buffered by TMA:
-//   S  = Q K^T   (SS, TMEM [0,128)),  dP = dO V^T (SS, TMEM [128,256))
-//   softmax (thread = query row): dS = P (dP - rho), bf16 over S's upper half
-//   dQ += dS K   (TS, TMEM [256,384); K tile read MN-major)
+// tile (taylor.py:262-285). Key tiles are 128 keys = two 64-key blocks.
+//
+// tcgen05.mma costs ~45 clk per instruction at N=64 whatever the operand
+// source (tools/ubench/mma.cu: 5.8 of 8.2 kFLOP/clk/SM), full rate only from
+// N=128 up, so S and dP are N=128 MMAs. TMEM (512 columns) holds two S
+// buffers, one dP buffer and dQ:
+//   S  = Q K^T   (SS, M=128 N=128, TMEM (i&1)*128 + [0,128))
+//   dP = dO V^T  (SS, TMEM [256,384)) -- rewritten for tile i+1 as soon as
+//                every softmax warp has pulled tile i's dP into registers
+//   softmax (8 warps: thread = query row x 64-key half, packed f32x2 math):
+//                dS = P (dP - rho), bf16 over the first 32 columns of its own S half
+//   dQ += dS K   (TS, K = 128 keys, TMEM [384, 384 + D); K tile read MN-major)
+// so the tensor pipe runs S(i+1), dP(i+1) and dQ(i-1)... while the softmax
+// warps work on tile i: per 128-key tile 3 x 512 clk of MMA (D=128) against
+// 64 exp2 per thread (1024 MUFU clk per SM sub-partition) -- MMA-bound.
+// Q/dO stay resident in shared memory; K streams through a 3-slot ring (it
+// is read again by dQ(i), issued a tile after S(i)), V through 2 slots.
 template <int D>
 struct BwdDqSmem {
-  static constexpr int kTile = 128 * D * 2;
+  static constexpr int kKSlots = 3, kVSlots = 2;
+  static constexpr int kTile = 128 * D * 2;  // 128 rows: [plane][128 rows][64 d]
   static constexpr int kQ = 0;
   static constexpr int kO = kTile;
-  static constexpr int kKV = 2 * kTile;                  // [2 slots][K, V]
-  static constexpr int kCol = kKV + 4 * kTile;          // [2 slots][128] column bias (centroid) floats
-  static constexpr int kMeta = kCol + 2 * 128 * 4;      // [2 slots][4] ints: centroid flag, tile index, meta0, meta1
+  static constexpr int kK = 2 * kTile;                     // [kKSlots]
+  static constexpr int kV = kK + kKSlots * kTile;          // [kVSlots]
+  static constexpr int kCol = kV + kVSlots * kTile;        // [kKSlots][128] column bias (centroid tiles) floats
+  static constexpr int kMeta = kCol + kKSlots * 128 * 4;   // [kKSlots][4] ints: centroid flag, tile, meta0, meta1
   static constexpr int kBar = kMeta + 64;
-  static constexpr int kBytes = kBar + 128 + 1024;
+  static constexpr int kBytes = kBar + 256 + 1024;
 };
 
 template <int D>
-__global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
+__global__ void __launch_bounds__(320, 1) bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                                                            const __grid_constant__ CUtensorMap tm_k,
                                                            const __grid_constant__ CUtensorMap tm_v,
                                                            const __grid_constant__ CUtensorMap tm_do,
@@ -402,19 +424,28 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
                                                            const int* __restrict__ n_tiles_f, int n_items,
                                                            int max_tiles) {
   using L = BwdDqSmem<D>;
+  constexpr int NK = L::kKSlots, NV = L::kVSlots;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the shared array, so metadata reads stay ld.shared
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* qo_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* d_full = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
-  uint64_t* meta_free = bars + 9;  // [2]: every softmax thread has read the slot's sMeta / sCol
-  __shared__ float sCol[2 * 128];  // [2 slots][128] column bias (centroid tiles)
-  __shared__ int sMeta[2 * 4];     // [2 slots]: centroid flag, tile index, meta0, meta1
+  uint64_t* d_full = bars + 1;
+  uint64_t* dp_full = bars + 2;              // dP of the current tile written
+  uint64_t* dp_free = bars + 3;              // every softmax warp holds the tile's dP in registers
+  // [2] dS of the S buffer's tile stored. Per buffer: a softmax warp may
+  // finish tile i+1 before a slower one finishes tile i (dP(i+1) only waits
+  // for tile i's dP loads), so one shared barrier would alias the two phases.
+  uint64_t* p_full = bars + 4;
+  uint64_t* s_full = bars + 6;               // [2] S buffer written
+  uint64_t* kf_full = bars + 8;              // [NK] K tile + metadata landed
+  uint64_t* kf_empty = bars + 8 + NK;        // [NK] dQ MMA of the slot's tile done
+  uint64_t* meta_free = bars + 8 + 2 * NK;   // [NK] every softmax thread has read the slot's metadata
+  uint64_t* vf_full = bars + 8 + 3 * NK;     // [NV]
+  uint64_t* vf_empty = bars + 8 + 3 * NK + NV;  // [NV] dP MMA of the slot's tile done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 3 * NK + 2 * NV);
+  float* sCol = reinterpret_cast<float*>(smem + L::kCol);
+  int* sMeta = reinterpret_cast<int*>(smem + L::kMeta);
 
   const int bh = blockIdx.y;
   const int hh = bh % p.H, bb = bh / p.H;
@@ -439,23 +470,31 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
 
   if (threadIdx.x == 0) {
     mbar_init(qo_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 32);  // every producer lane arrives after its own smem writes
-      mbar_init(&kv_empty[s], 1);
-      mbar_init(&meta_free[s], 128);
-    }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
     mbar_init(d_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(dp_free, 8);
+    for (int b2 = 0; b2 < 2; ++b2) {
+      mbar_init(&p_full[b2], 8);
+      mbar_init(&s_full[b2], 1);
+    }
+    for (int s2 = 0; s2 < NK; ++s2) {
+      mbar_init(&kf_full[s2], 32);  // every producer lane arrives after its own smem writes
+      mbar_init(&kf_empty[s2], 1);
+      mbar_init(&meta_free[s2], 256);
+    }
+    for (int s2 = 0; s2 < NV; ++s2) {
+      mbar_init(&vf_full[s2], 1);
+      mbar_init(&vf_empty[s2], 1);
+    }
     fence_barrier_init();
   }
-  if (warp == 4) tmem_alloc<512>(tmem_slot);
+  if (warp == 8) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 5) {
+  if (warp == 9) {
     // ---------------------------------------------------------------- TMA producer
     const bool leader = elect_one();
     const uint64_t pol = policy_evict_last();
@@ -471,11 +510,13 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
     }
     const int4* tl = flat ? tiles + (((long long)bh * n_items + item) * 2 + stg) * max_tiles : nullptr;
     for (int i = 0; i < n_kv; ++i) {
-      const int slot = i & 1;
-      if (i >= 2) {
-        mbar_wait(&kv_empty[slot], ((i >> 1) - 1) & 1);
-        mbar_wait(&meta_free[slot], ((i >> 1) - 1) & 1);  // tile i-2's metadata read by every softmax thread
+      const int ks = i % NK, vs = i % NV;
+      if (i >= NK) {
+        const uint32_t ph = ((i / NK) - 1) & 1;
+        mbar_wait(&kf_empty[ks], ph);
+        mbar_wait(&meta_free[ks], ph);  // the slot's previous metadata read by every softmax thread
       }
+      if (leader) DQ_TSTAMP(i, 1, 4);
       __syncwarp();
       int tok0, tok1, cent = 0, meta0 = 0xF | (64 << 8), meta1 = 0xF | (64 << 8);
       if (i < n_exact) {
@@ -483,15 +524,14 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
           const int4 e = tl[i];
           tok0 = e.x >= 0 ? e.x : 0;
           tok1 = e.y >= 0 ? e.y : tok0;
-          meta0 = e.z >> (2 * stg) & 3 | (e.z & ~0xFF);  // visibility bits of this pair's two blocks
+          meta0 = e.z >> (2 * stg) & 3 | (e.z & ~0xFF);  // visibility bits of this pair's two blocks | valid << 8
           meta1 = e.w >> (2 * stg) & 3 | (e.w & ~0xFF);
         } else {
-          const int kn0 = 2 * i, kn1 = 2 * i + 1;
-          const int u0 = tab[kn0];
+          const int u0 = tab[2 * i];
           tok0 = bw_tok0(p, u0);
           meta0 = 3 | (bw_valid(p, u0) << 8);
-          if (kn1 < p.t_new) {
-            const int u1 = tab[kn1];
+          if (2 * i + 1 < p.t_new) {
+            const int u1 = tab[2 * i + 1];
             tok1 = bw_tok0(p, u1);
             meta1 = 3 | (bw_valid(p, u1) << 8);
           } else {
@@ -506,82 +546,127 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
         // column weights log2(valid rows) of the 128 centroids (-inf past t_new), taylor.py:156
         for (int c = lane; c < 128; c += 32) {
           const int jj = tok0 + c;
-          sCol[slot * 128 + c] = jj < p.t_new ? __log2f((float)bw_valid(p, tab[jj])) : -INFINITY;
+          sCol[ks * 128 + c] = jj < p.t_new ? __log2f((float)bw_valid(p, tab[jj])) : -INFINITY;
         }
       }
       if (lane == 0) {
-        sMeta[slot * 4 + 0] = cent;
-        sMeta[slot * 4 + 1] = i - n_exact;
-        sMeta[slot * 4 + 2] = meta0;
-        sMeta[slot * 4 + 3] = meta1;
+        sMeta[ks * 4 + 0] = cent;
+        sMeta[ks * 4 + 1] = i - n_exact;
+        sMeta[ks * 4 + 2] = meta0;
+        sMeta[ks * 4 + 3] = meta1;
       }
       __syncwarp();
       // each lane releases its own metadata writes (the leader also arms the TMA bytes)
-      if (!leader) mbar_arrive(&kv_full[slot]);
+      if (!leader) mbar_arrive(&kf_full[ks]);
       if (leader) {
-        mbar_arrive_expect_tx(&kv_full[slot], 2 * L::kTile);
-        uint8_t* dst = smem + L::kKV + slot * 2 * L::kTile;
-        for (int h = 0; h < 2; ++h) {
-          const int tok = h ? tok1 : tok0;
+        mbar_arrive_expect_tx(&kf_full[ks], L::kTile);
+        uint8_t* dk = smem + L::kK + ks * L::kTile;
+        for (int h = 0; h < 2; ++h)
           for (int pl = 0; pl < D / 64; ++pl) {
-            if (cent) {
-              tma_load_4d(dst + pl * 16384 + h * 8192, &tm_kc, &kv_full[slot], pl * 64, tok, bh, 0, pol);
-              tma_load_4d(dst + L::kTile + pl * 16384 + h * 8192, &tm_vc, &kv_full[slot], pl * 64, tok, bh, 0, pol);
-            } else {
-              tma_load_4d(dst + pl * 16384 + h * 8192, &tm_k, &kv_full[slot], pl * 64, tok, hh, bb, pol);
-              tma_load_4d(dst + L::kTile + pl * 16384 + h * 8192, &tm_v, &kv_full[slot], pl * 64, tok, hh, bb, pol);
-            }
+            if (cent)
+              tma_load_4d(dk + pl * 16384 + h * 8192, &tm_kc, &kf_full[ks], pl * 64, h ? tok1 : tok0, bh, 0, pol);
+            else
+              tma_load_4d(dk + pl * 16384 + h * 8192, &tm_k, &kf_full[ks], pl * 64, h ? tok1 : tok0, hh, bb, pol);
           }
-        }
+        if (i >= NV) mbar_wait(&vf_empty[vs], ((i / NV) - 1) & 1);
+        mbar_arrive_expect_tx(&vf_full[vs], L::kTile);
+        uint8_t* dv = smem + L::kV + vs * L::kTile;
+        for (int h = 0; h < 2; ++h)
+          for (int pl = 0; pl < D / 64; ++pl) {
+            if (cent)
+              tma_load_4d(dv + pl * 16384 + h * 8192, &tm_vc, &vf_full[vs], pl * 64, h ? tok1 : tok0, bh, 0, pol);
+            else
+              tma_load_4d(dv + pl * 16384 + h * 8192, &tm_v, &vf_full[vs], pl * 64, h ? tok1 : tok0, hh, bb, pol);
+          }
+        DQ_TSTAMP(i, 1, 5);
       }
+      __syncwarp();
     }
-  } else if (warp == 4) {
+  } else if (warp == 8) {
     // ---------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128, 0, 0);
     constexpr uint32_t idesc_g = idesc_bf16_f32(128, D, 0, 1);
     const bool leader = elect_one();
-    const uint64_t dq_base = sdesc_sw128_base(smem_u32(smem + L::kQ), 16, 1024);
-    const uint64_t do_base = sdesc_sw128_base(smem_u32(smem + L::kO), 16, 1024);
-    mbar_wait(qo_full, 0);
-    for (int i = 0; i < n_kv; ++i) {
-      const int slot = i & 1;
-      mbar_wait(&kv_full[slot], (i >> 1) & 1);
+    const uint64_t q_desc = sdesc_sw128_base(smem_u32(smem + L::kQ), 16, 1024);
+    const uint64_t do_desc = sdesc_sw128_base(smem_u32(smem + L::kO), 16, 1024);
+    const uint32_t kb0 = smem_u32(smem + L::kK), vb0 = smem_u32(smem + L::kV);
+    auto issue_s = [&](int j) {  // S of tile j into buffer j & 1
+      const int ks = j % NK;
+      mbar_wait(&kf_full[ks], (j / NK) & 1);
       __syncwarp();
       tc_fence_after();
-      const uint32_t kb = smem_u32(smem + L::kKV + slot * 2 * L::kTile);
       if (leader) {
-        const uint64_t dk = sdesc_sw128_base(kb, 16, 1024), dv = sdesc_sw128_base(kb + L::kTile, 16, 1024);
+        const uint64_t dk = sdesc_sw128_base(kb0 + ks * L::kTile, 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-          mma_ss(tmem + 0, dq_base + off, dk + off, idesc_s, kk > 0);
+          const uint64_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + (j & 1) * 128, q_desc + o, dk + o, idesc_s, kk > 0);
         }
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-          mma_ss(tmem + 128, do_base + off, dv + off, idesc_s, kk > 0);
-        }
-        mma_commit(s_full);
+        mma_commit(&s_full[j & 1]);
       }
       __syncwarp();
-      mbar_wait(p_full, i & 1);
+    };
+    auto issue_dp = [&](int j) {  // dP of tile j
+      const int vs = j % NV;
+      mbar_wait(&vf_full[vs], (j / NV) & 1);
       __syncwarp();
       tc_fence_after();
       if (leader) {
-        const uint64_t dkm = sdesc_sw128_base(kb, 16384, 1024);
+        const uint64_t dv = sdesc_sw128_base(vb0 + vs * L::kTile, 16, 1024);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tmem + 256, tmem + 64 + kk * 8, dkm + (uint64_t)((kk * 2048) >> 4), idesc_g, (i > 0) || kk > 0);
-        mma_commit(&kv_empty[slot]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t o = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+          mma_ss(tmem + 256, do_desc + o, dv + o, idesc_s, kk > 0);
+        }
+        mma_commit(dp_full);
+        mma_commit(&vf_empty[vs]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(qo_full, 0);
+    if (leader) {
+      ISA_CTA_SPAN(0, global_ns());
+      ISA_CTA_SPAN(2, 2 * n_kv);
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      ISA_CTA_SPAN(3, sm);
+    }
+    if (n_kv > 0) {
+      issue_s(0);
+      issue_dp(0);
+    }
+    for (int i = 0; i < n_kv; ++i) {
+      // S buffer (i+1)&1 last held tile i-1: its softmax finished and its dQ
+      // MMA was issued (in order, before these writes) last iteration
+      if (i + 1 < n_kv) {
+        issue_s(i + 1);
+        mbar_wait(dp_free, i & 1);  // tile i's dP is in the softmax registers
+        issue_dp(i + 1);
+      }
+      if (leader) DQ_TSTAMP(i, 1, 2);
+      mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+      if (leader) DQ_TSTAMP(i, 1, 3);
+      __syncwarp();
+      tc_fence_after();
+      if (leader) {
+        const int ks = i % NK;
+        const uint64_t dkm = sdesc_sw128_base(kb0 + ks * L::kTile, 16384, 1024);  // K as the MN-major B
+        const uint32_t ts = tmem + (i & 1) * 128;  // dS (bf16): keys 0-63 at cols [0,32), 64-127 at [64,96)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // 128 keys = 8 x 16
+          mma_ts(tmem + 384, ts + (kk >> 2) * 64 + (kk & 3) * 8, dkm + (uint64_t)((kk * 2048) >> 4), idesc_g,
+                 (i > 0) || kk > 0);
+        mma_commit(&kf_empty[ks]);
       }
       __syncwarp();
     }
     if (leader) mma_commit(d_full);
     __syncwarp();
   } else {
-    // ---------------------------------------------------------------- softmax (thread = query row)
-    const int row = warp * 32 + lane;
-    const int qh = row >> 6;
+    // ---------------------------------------------------------------- softmax (thread = query row x key half)
+    const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant; keys [64 half, 64 half + 64) = one block
+    const int row = quad * 32 + lane;
+    const int qh = row >> 6;  // warp-uniform
     const int uq = u[qh];
     const int vq = uq >= 0 ? bw_valid(p, uq) : 0;
     const bool row_ok = (row & 63) < vq;
@@ -592,77 +677,108 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
     const float lse_eff = live ? lse : INFINITY;  // dead rows: exp2(-inf) = 0, no per-element predicate
     const uint32_t* mb = (flat && uq >= 0) ? p.bits + ((long long)bh * p.n_flat + 4 * item + 2 * stg + qh) * p.W
                                            : nullptr;
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-    const uint32_t t_s = tmem + lane_base, t_dp = tmem + lane_base + 128;
-    const float sl2 = p.sl2;
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    const uint64_t sl2x2 = f32x2(p.sl2, p.sl2), nlse2 = f32x2(-lse_eff, -lse_eff), nrho2 = f32x2(-rho, -rho);
+    const uint32_t t_dp = tmem + lane_base + 256 + half * 64;
     for (int i = 0; i < n_kv; ++i) {
-      const int slot = i & 1;
-      mbar_wait(&kv_full[slot], (i >> 1) & 1);  // the producer's per-tile metadata
-      const int cent = sMeta[slot * 4 + 0], cidx = sMeta[slot * 4 + 1];
-      const int m0 = sMeta[slot * 4 + 2], m1 = sMeta[slot * 4 + 3];
-      // exact tiles: per-half limit (valid rows if this row's block sees the half, else 0)
-      const int lim0 = ((m0 >> qh) & 1) ? (m0 >> 8) : 0;
-      const int lim1 = ((m1 >> qh) & 1) ? (m1 >> 8) : 0;
-      uint32_t mw[4] = {0u, 0u, 0u, 0u};
-      if (cent && mb) {
-#pragma unroll
-        for (int w = 0; w < 4; ++w) mw[w] = __ldg(mb + cidx * 4 + w);  // own exact members excluded
+      const int ks = i % NK;
+      mbar_wait(&kf_full[ks], (i / NK) & 1);  // the producer's per-tile metadata
+      if (threadIdx.x == 0) DQ_TSTAMP(i, 0, 2);
+      const int cent = sMeta[ks * 4 + 0], cidx = sMeta[ks * 4 + 1], m = sMeta[ks * 4 + 2 + half];
+      // exact tiles: valid keys of this half's block if this row's block sees it (warp-uniform)
+      const int lc = ((m >> qh) & 1) ? (m >> 8) : 0;
+      uint32_t cw[2] = {0u, 0u};
+      float colb[2] = {0.f, 0.f};  // lane c holds column 32 ch + c's weight
+      if (cent) {
+        if (mb) {
+          cw[0] = __ldg(mb + cidx * 4 + 2 * half);  // own exact members excluded
+          cw[1] = __ldg(mb + cidx * 4 + 2 * half + 1);
+        }
+        colb[0] = sCol[ks * 128 + half * 64 + lane];
+        colb[1] = sCol[ks * 128 + half * 64 + 32 + lane];
       }
-      mbar_wait(s_full, i & 1);
+      const uint32_t t_s = tmem + lane_base + (i & 1) * 128 + half * 64;
+      mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+      mbar_wait(dp_full, i & 1);
+      if (threadIdx.x == 0) DQ_TSTAMP(i, 0, 1);
       __syncwarp();
       tc_fence_after();
-      // one copy of the chunk code per tile kind (compile-time tag), so the
-      // exact tiles carry no centroid selects / shared-memory bias loads
-      auto chunk = [&](const int ch, auto cent_tag) {
-        constexpr bool kCent = decltype(cent_tag)::value;
-        uint32_t sr[32], dr[32];
-        tmem_ld32(t_s + ch * 32, sr);
-        tmem_ld32(t_dp + ch * 32, dr);
-        tmem_ld_wait();
-        // exact tiles: this chunk lies in one 64-key half with a row-uniform limit
-        const int lim = (ch < 2 ? lim0 : lim1) - 32 * (ch & 1);
-        const uint32_t cw = kCent ? mw[ch] : 0u;
-        uint32_t pk[16];
+      if (!cent && lc <= 0) {
+        // block invisible to this query block: dS = 0
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dp_free);
+        uint32_t z[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float dv[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int cc = 2 * c + e;  // column within the chunk
-            float bias;
-            if (kCent)
-              bias = ((cw >> cc) & 1u) ? -INFINITY : sCol[slot * 128 + ch * 32 + cc];
-            else
-              bias = cc < lim ? 0.f : -INFINITY;
-            const float pr = ex2_approx(fmaf(__uint_as_float(sr[cc]), sl2, bias - lse_eff));
-            dv[e] = pr * (__uint_as_float(dr[cc]) - rho);
-          }
-          pk[c] = pack_bf16x2(dv[0], dv[1]);
-        }
-        tmem_st16(t_s + 64 + ch * 16, pk);
-      };
-      if (cent) {
-#pragma unroll 1
-        for (int ch = 3; ch >= 0; --ch) chunk(ch, std::true_type{});
+        for (int c = 0; c < 16; ++c) z[c] = 0u;
+        tmem_st16(t_s, z);
+        tmem_st16(t_s + 16, z);
       } else {
-#pragma unroll 1
-        for (int ch = 3; ch >= 0; --ch) chunk(ch, std::false_type{});
+        uint32_t dr[2][32];
+        tmem_ld32(t_dp, dr[0]);
+        tmem_ld32(t_dp + 32, dr[1]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dp_free);  // the MMA warp may overwrite dP with tile i+1's
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t sr[32], pk[16];
+          tmem_ld32(t_s + ch * 32, sr);
+          tmem_ld_wait();
+          if (!cent && lc >= 64) {
+            // whole block visible: no masking, two columns per packed op
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const uint64_t x =
+                  fma_f32x2(f32x2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sl2x2, nlse2);
+              float x0, x1;
+              f32x2_split(x, x0, x1);
+              const uint64_t pr = f32x2(ex2_approx(x0), ex2_approx(x1));
+              const uint64_t dd =
+                  add_f32x2(f32x2(__uint_as_float(dr[ch][2 * c]), __uint_as_float(dr[ch][2 * c + 1])), nrho2);
+              float d0, d1;
+              f32x2_split(mul_f32x2(pr, dd), d0, d1);
+              pk[c] = pack_bf16x2(d0, d1);
+            }
+          } else {
+            const int lcc = lc - 32 * ch;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              float dvv[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int cc = 2 * c + e;  // column within the chunk
+                float bias;
+                if (cent)
+                  bias = ((cw[ch] >> cc) & 1u) ? -INFINITY : __shfl_sync(0xffffffffu, colb[ch], cc);
+                else
+                  bias = cc < lcc ? 0.f : -INFINITY;
+                const float pr = ex2_approx(fmaf(__uint_as_float(sr[cc]), p.sl2, bias - lse_eff));
+                dvv[e] = pr * (__uint_as_float(dr[ch][cc]) - rho);
+              }
+              pk[c] = pack_bf16x2(dvv[0], dvv[1]);
+            }
+          }
+          tmem_st16(t_s + ch * 16, pk);  // over S columns this thread has already read
+        }
       }
-      mbar_arrive(&meta_free[slot]);  // this thread's reads of the slot's metadata are done
+      mbar_arrive(&meta_free[ks]);  // this thread's reads of the tile's metadata are done
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (threadIdx.x == 0) DQ_TSTAMP(i, 0, 3);
+      if (lane == 0) mbar_arrive(&p_full[i & 1]);
     }
     // ---------------------------------------------------------------- epilogue
     mbar_wait(d_full, 0);
     __syncwarp();
     tc_fence_after();
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
       uint32_t qr[32];
       __syncwarp();
-      tmem_ld32(tmem + lane_base + 256 + c * 32, qr);
+      tmem_ld32(tmem + lane_base + 384 + c * 32, qr);
       tmem_ld_wait();
       if (row_ok) {
         float* dst = p.dq + grow * D + c * 32;
@@ -671,9 +787,10 @@ __global__ void __launch_bounds__(192, 1) bwd_dq_tc_kernel(const __grid_constant
       }
     }
   }
+  if (threadIdx.x == 0) ISA_CTA_SPAN(1, global_ns());
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }

@@ -953,7 +953,7 @@ int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps,
         return rc;
     }
     const int grid_x = (d.n_sharp + 1) / 2 + 2 * d.items_f;
-    isa::bwd_dq_tc_kernel<D><<<dim3(grid_x, d.BH), 192, QL::kBytes, st>>>(
+    isa::bwd_dq_tc_kernel<D><<<dim3(grid_x, d.BH), 320, QL::kBytes, st>>>(
         maps[0], maps[1], maps[2], maps[3], tkc, tvc, bp, w.tiles, w.n_tiles, d.items_f, d.max_tiles);
     ISA_LAUNCHED("bwd_dq_tc_kernel");
   }
@@ -1599,6 +1599,10 @@ int isa_debug_count_copy(void* host, int reset) {
 }
 int isa_debug_trace_copy(void* host, size_t bytes) {
   ISA_CUDA(cudaMemcpyFromSymbol(host, isa::g_isa_trace, bytes < sizeof(isa::g_isa_trace) ? bytes : sizeof(isa::g_isa_trace)));
+  return ISA_OK;
+}
+int isa_debug_cta_copy(void* host, size_t bytes) {
+  ISA_CUDA(cudaMemcpyFromSymbol(host, isa::g_isa_cta, bytes < sizeof(isa::g_isa_cta) ? bytes : sizeof(isa::g_isa_cta)));
   return ISA_OK;
 }
 #endif

@@ -108,6 +108,14 @@ __device__ __forceinline__ bool trace_cta() { return blockIdx.x == ISA_TRACE && 
   do {                                                                              \
     if (trace_cta() && (step) < kTraceSteps) g_isa_trace[(step)][(stage)][(slot)] = clock64(); \
   } while (0)
+// per-CTA spans of the traced kernel: [cta][0 start ns, 1 end ns, 2 work units, 3 smid]
+constexpr int kTraceCtas = 1 << 16;
+__device__ long long g_isa_cta[kTraceCtas][4];
+__device__ __forceinline__ int cta_linear() { return blockIdx.y * gridDim.x + blockIdx.x; }
+#define ISA_CTA_SPAN(k, v)                                                        \
+  do {                                                                            \
+    if (cta_linear() < kTraceCtas) g_isa_cta[cta_linear()][(k)] = (long long)(v);            \
+  } while (0)
 // softmax path counters (per warp-tile): [mode][0 spec, 1 redo, 2 general, 3 skip]
 __device__ unsigned long long g_isa_count[3][4];
 #define ISA_COUNT(mode, k)                                    \
@@ -120,6 +128,9 @@ __device__ unsigned long long g_isa_count[3][4];
   } while (0)
 #define ISA_TSTAMP(step, stage, slot) \
   do {                                \
+  } while (0)
+#define ISA_CTA_SPAN(k, v) \
+  do {                     \
   } while (0)
 #endif
 
@@ -390,6 +401,31 @@ __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// packed f32x2 arithmetic (sm_100: FFMA2 / FADD2 / FMUL2, two lanes per issue)
+__device__ __forceinline__ uint64_t f32x2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f32x2_split(uint64_t r, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma_f32x2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t add_f32x2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul_f32x2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

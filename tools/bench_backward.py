@@ -8,8 +8,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2605_04569_b200 as P
 
-H = int(sys.argv[1]) if len(sys.argv) > 1 else 40
-L = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+H = int(args[0]) if len(args) > 0 else 40
+L = int(args[1]) if len(args) > 1 else 32768
 q, k, v, do = (torch.randn(1, H, 2 * L, 128, device="cuda").to(torch.bfloat16) for _ in range(4))
 icl, cfg = P.IclLayout(L, L), P.IsaConfig()
 P.isa_backward(q, k, v, icl, cfg, do)
@@ -33,3 +34,16 @@ f = P.IsaDims.derive(q.shape, icl, cfg).flops()
 fl = 2.5 * (f.exact_mas + f.taylor_mas)
 print(json.dumps({"workload": f"isa_backward H={H} {L}+{L} D=128 bf16", "backward_total_ms": bwd, "forward_ms": fwd,
                   "gradient_kernels_ms": bwd - fwd, "alg_tflops_gradients": fl / (bwd - fwd) / 1e9}))
+if "--kernels" in sys.argv:  # per-kernel device times of one backward (CUPTI via torch.profiler)
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as pr:
+        P.isa_backward(q, k, v, icl, cfg, do)
+        torch.cuda.synchronize()
+    rows = {}
+    for e in pr.events():
+        if e.device_type.name == "CUDA":
+            r = rows.setdefault(e.name[:60], [0, 0.0])
+            r[0] += 1
+            r[1] += e.device_time_total / 1e3 if hasattr(e, "device_time_total") else e.cuda_time_total / 1e3
+    for name, (n, ms) in sorted(rows.items(), key=lambda x: -x[1][1])[:14]:
+        print(f"{ms:9.3f} ms  x{n:<3d} {name}")
