@@ -4,22 +4,25 @@
 // block-mean adjoint (taylor.py:290-292) and the K_new gather adjoint
 // (pipeline.py:423-433) fused into the epilogue.
 //
-// CTA = 128 keys = K_new blocks (2x, 2x+1); it streams 128-row query tiles
-// (pairs of query blocks: all sharp blocks, then the flat blocks whose exact
-// list holds either key block). Per query tile, with K/V resident in shared
-// memory and Q/dO double-buffered by TMA:
-//   S^T  = K Q^T     (SS, TMEM cols [0,128))
-//   dP^T = V dO^T    (SS, TMEM cols [128,256))
-//   softmax warps (thread = key row = TMEM lane): P^T = exp2(S^T*sl2 - lse),
-//     dS^T = P^T (dP^T - rho); bf16 P^T / dS^T over the upper halves of the
-//     S^T / dP^T regions (chunks in descending order: each write lands on
-//     columns already read)
-//   dV  += P^T dO    (TS, TMEM cols [256,384); dO tile read MN-major)
-//   dK  += dS^T Q    (TS, TMEM cols [384,512); Q tile read MN-major)
-// Warps: 0-7 softmax + epilogue (two warps per TMEM lane quadrant: warps 0-3
-// take query columns 64-127, warps 4-7 columns 0-63, so every SM
-// sub-partition runs two independent softmax streams), 8 TMEM alloc + MMA
-// issue, 9 TMA producer (+ per-query lse/rho rows into shared memory).
+// CTA = 128 keys = K_new blocks (2x, 2x+1); it streams 64-row query units
+// (query blocks: all sharp blocks, then the flat blocks whose exact list
+// holds either key block). K/V stay resident in shared memory, Q/dO units
+// stream through a kSlots TMA ring. TMEM holds two S^T/dP^T buffers, so the
+// MMA warp computes unit i+1's S^T and dP^T while the softmax warps turn
+// unit i into P^T / dS^T:
+//   S^T  = K Q^T     (SS, M=128 N=64, TMEM (i&1)*128 + [0,64))
+//   dP^T = V dO^T    (SS, TMEM (i&1)*128 + [64,128))
+//   softmax (8 warps: thread = key row x 32-query half, packed f32x2 math):
+//     P^T = exp2(S^T*sl2 - lse), dS^T = P^T (dP^T - rho), bf16 over the first
+//     16 columns of the warp's own S^T / dP^T half (no cross-warp overlap)
+//   dV  += P^T dO    (TS, TMEM [256,384); dO unit read MN-major)
+//   dK  += dS^T Q    (TS, TMEM [384,512); Q unit read MN-major)
+// The 128-query form (N=128, one buffer) ran MMA and softmax back to back
+// (~4400 clk per 128 queries); here per 64-query unit the tensor pipe does
+// 2 x 8 N=64 MMAs (~45 clk each, tools/ubench/mma.cu) + 2 x 4 N=D ones
+// (~1230 clk) under 32 exp2 per thread (512 MUFU clk per SM sub-partition).
+// Warps: 0-7 softmax + epilogue, 8 TMEM alloc + MMA issue, 9 TMA producer
+// (+ per-query lse/rho rows into shared memory).
 #pragma once
 #include <type_traits>
 
@@ -34,13 +37,15 @@ struct BwdTcParams {
 
 template <int D>
 struct BwdTcSmem {
-  static constexpr int kTile = 128 * D * 2;  // one 128-row bf16 tile
+  static constexpr int kSlots = 4;
+  static constexpr int kTile = 128 * D * 2;  // K / V: 128 key rows, [plane][128 rows][64 d]
+  static constexpr int kUnit = 64 * D * 2;   // Q / dO: 64 query rows, [plane][64 rows][64 d]
   static constexpr int kK = 0;
   static constexpr int kV = kTile;
-  static constexpr int kQO = 2 * kTile;          // [2 slots][Q, dO]
-  static constexpr int kStats = kQO + 4 * kTile;  // [2 slots][lse 128, rho 128] floats
-  static constexpr int kBar = kStats + 2 * 256 * 4;
-  static constexpr int kList = kBar + 256;       // int list (query-block positions) + vis flags
+  static constexpr int kQO = 2 * kTile;                       // [kSlots][Q, dO]
+  static constexpr int kStats = kQO + kSlots * 2 * kUnit;     // [kSlots][-lse 64 | -rho 64] floats
+  static constexpr int kBar = kStats + kSlots * 128 * 4;
+  static constexpr int kList = kBar + 256;                    // int list (query-block positions) + vis flags
   static constexpr int bytes(int n_list) { return kList + 8 * n_list + 1024; }
 };
 
@@ -51,25 +56,24 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
                                                             const __grid_constant__ CUtensorMap tm_do,
                                                             const BwdTcParams tp) {
   using L = BwdTcSmem<D>;
+  constexpr int NS = L::kSlots;
   const BwdParams& p = tp.b;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the shared array, so list / stats reads stay ld.shared
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t* kv_full = bars + 0;
-  uint64_t* qo_full = bars + 1;   // [2]
-  uint64_t* qo_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* d_full = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
-  int* s_count = reinterpret_cast<int*>(bars + 9);
-  uint64_t* st_free = bars + 10;  // [2]: every softmax thread has read the slot's lse/rho rows
-  int* sList = reinterpret_cast<int*>(smem + L::kList);     // query-block position (x < n_sharp: sharp)
-  int* sVis = sList + tp.n_list_max;                          // bit0: lists j0, bit1: lists j1
-  // per-query statistics [2 slots][lse 128 | rho 128]: a static __shared__
-  // array so the per-element reads compile to LDS (the aligned dynamic-smem
-  // pointer is generic to the compiler, which made them LD.E)
-  __shared__ float sStats[2 * 256];
+  uint64_t* d_full = bars + 1;
+  uint64_t* s_full = bars + 2;               // [2] S^T / dP^T buffer written
+  uint64_t* p_full = bars + 4;               // [2] P^T / dS^T of the buffer stored (per buffer: see bwd_dq)
+  uint64_t* qo_full = bars + 6;              // [NS] Q / dO unit + stats landed
+  uint64_t* qo_empty = bars + 6 + NS;        // [NS] dV / dK MMAs of the slot's unit done
+  uint64_t* st_free = bars + 6 + 2 * NS;     // [NS] every softmax thread has read the slot's stats
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 3 * NS);
+  int* s_count = reinterpret_cast<int*>(bars + 7 + 3 * NS);
+  float* sStats = reinterpret_cast<float*>(smem + L::kStats);
+  int* sList = reinterpret_cast<int*>(smem + L::kList);  // query-block position (x < n_sharp: sharp)
+  int* sVis = sList + tp.n_list_max;                       // bit0: lists j0, bit1: lists j1
 
   const int bh = blockIdx.y;
   const int hh = bh % p.H, bb = bh / p.H;
@@ -82,14 +86,16 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
   if (threadIdx.x == 0) {
     *s_count = 0;
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    mbar_init(d_full, 1);
+    for (int b2 = 0; b2 < 2; ++b2) {
+      mbar_init(&s_full[b2], 1);
+      mbar_init(&p_full[b2], 8);
+    }
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&qo_full[s], 32);  // every producer lane arrives after its own smem writes
       mbar_init(&qo_empty[s], 1);
       mbar_init(&st_free[s], 256);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 8);
-    mbar_init(d_full, 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -112,8 +118,7 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int n_list = p.n_sharp + *s_count;
-  const int n_tiles = (n_list + 1) >> 1;
+  const int n_units = p.n_sharp + *s_count;
 
   if (warp == 9) {
     // ---------------------------------------------------------------- TMA producer
@@ -131,201 +136,181 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
         }
       }
     }
-    // Per-tile query info (block ids, lse/rho rows: lane holds rows lane + 32k)
-    // is loaded one tile ahead into registers, so its dependent global loads
+    // Per-unit query info (block id, lse/rho rows: lane holds rows lane, lane + 32)
+    // is loaded one unit ahead into registers, so its dependent global loads
     // overlap the wait for the slot instead of delaying the TMA issue.
     struct Info {
-      int u[2];
-      float ls[4], rh[4];
+      int u;
+      float ls[2], rh[2];
     };
     auto fetch = [&](int t, Info& in) {
-      int vq[2];
-      for (int h = 0; h < 2; ++h) {
-        const int li = 2 * t + h;
-        if (t < n_tiles && li < n_list) {
-          const int x = sList[li];
-          in.u[h] = x < p.n_sharp ? p.sharp[bh * p.n_sharp + x] : p.flat[bh * p.n_flat + (x - p.n_sharp)];
-          vq[h] = bw_valid(p, in.u[h]);
-        } else {
-          in.u[h] = -1;
-          vq[h] = 0;
-        }
+      in.u = -1;
+      int vq = 0;
+      if (t < n_units) {
+        const int x = sList[t];
+        in.u = x < p.n_sharp ? p.sharp[bh * p.n_sharp + x] : p.flat[bh * p.n_flat + (x - p.n_sharp)];
+        vq = bw_valid(p, in.u);
       }
 #pragma unroll
-      for (int k4 = 0; k4 < 4; ++k4) {  // lse = -inf masks missing / padded rows
-        const int r = lane + 32 * k4, h = r >> 6, rr = r & 63;
-        in.ls[k4] = -INFINITY;
-        in.rh[k4] = 0.f;
-        if (in.u[h] >= 0 && rr < vq[h]) {
-          const long long row = (long long)bh * p.S + bw_tok0(p, in.u[h]) + rr;
-          in.ls[k4] = p.lse[row];
-          in.rh[k4] = p.rho[row];
+      for (int k2 = 0; k2 < 2; ++k2) {  // lse = -inf masks padded rows
+        const int r = lane + 32 * k2;
+        in.ls[k2] = -INFINITY;
+        in.rh[k2] = 0.f;
+        if (r < vq) {
+          const long long row = (long long)bh * p.S + bw_tok0(p, in.u) + r;
+          in.ls[k2] = p.lse[row];
+          in.rh[k2] = p.rho[row];
         }
       }
     };
     Info cur, nxt;
     fetch(0, nxt);
-    for (int t = 0; t < n_tiles; ++t) {
-      const int slot = t & 1;
+    for (int t = 0; t < n_units; ++t) {
+      const int slot = t % NS;
       cur = nxt;
       fetch(t + 1, nxt);  // loads in flight during the wait below
-      if (t >= 2) {
-        mbar_wait(&qo_empty[slot], ((t >> 1) - 1) & 1);
-        mbar_wait(&st_free[slot], ((t >> 1) - 1) & 1);  // tile t-2's stats read by every softmax thread
+      if (t >= NS) {
+        const uint32_t ph = ((t / NS) - 1) & 1;
+        mbar_wait(&qo_empty[slot], ph);
+        mbar_wait(&st_free[slot], ph);  // unit t-NS's stats read by every softmax thread
       }
       __syncwarp();
-      float* st = sStats + slot * 256;
+      float* st = sStats + slot * 128;
 #pragma unroll
-      for (int k4 = 0; k4 < 4; ++k4) {  // -lse (-inf for missing rows: p = 0 with no predicate)
-        st[lane + 32 * k4] = cur.ls[k4] > -INFINITY ? -cur.ls[k4] : -INFINITY;
-        st[128 + lane + 32 * k4] = cur.rh[k4];
+      for (int k2 = 0; k2 < 2; ++k2) {  // -lse (-inf for padded rows: p = 0 with no predicate), -rho
+        st[lane + 32 * k2] = cur.ls[k2] > -INFINITY ? -cur.ls[k2] : -INFINITY;
+        st[64 + lane + 32 * k2] = -cur.rh[k2];
       }
       __syncwarp();
       // each lane releases its own stats writes (the leader also arms the TMA bytes)
       if (!leader) mbar_arrive(&qo_full[slot]);
       if (leader) {
-        mbar_arrive_expect_tx(&qo_full[slot], 2 * L::kTile);
-        uint8_t* dq_ = smem + L::kQO + slot * 2 * L::kTile;
-        for (int h = 0; h < 2; ++h) {
-          const int uu = cur.u[h] >= 0 ? cur.u[h] : cur.u[0];
-          const int tok = bw_tok0(p, uu);
-          for (int pl = 0; pl < D / 64; ++pl) {
-            tma_load_4d(dq_ + pl * 16384 + h * 8192, &tm_q, &qo_full[slot], pl * 64, tok, hh, bb, pol);
-            tma_load_4d(dq_ + L::kTile + pl * 16384 + h * 8192, &tm_do, &qo_full[slot], pl * 64, tok, hh, bb,
-                        pol);
-          }
+        mbar_arrive_expect_tx(&qo_full[slot], 2 * L::kUnit);
+        uint8_t* dq_ = smem + L::kQO + slot * 2 * L::kUnit;
+        const int tok = bw_tok0(p, cur.u);
+        for (int pl = 0; pl < D / 64; ++pl) {
+          tma_load_4d(dq_ + pl * 8192, &tm_q, &qo_full[slot], pl * 64, tok, hh, bb, pol);
+          tma_load_4d(dq_ + L::kUnit + pl * 8192, &tm_do, &qo_full[slot], pl * 64, tok, hh, bb, pol);
         }
       }
     }
   } else if (warp == 8) {
     // ---------------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128, 0, 0);
+    constexpr uint32_t idesc_s = idesc_bf16_f32(128, 64, 0, 0);
     constexpr uint32_t idesc_g = idesc_bf16_f32(128, D, 0, 1);
     const bool leader = elect_one();
     const uint64_t dk_base = sdesc_sw128_base(smem_u32(smem + L::kK), 16, 1024);
     const uint64_t dv_base = sdesc_sw128_base(smem_u32(smem + L::kV), 16, 1024);
     auto qo_desc = [&](int slot, int which, bool mn) {
-      return sdesc_sw128_base(smem_u32(smem + L::kQO + (slot * 2 + which) * L::kTile), mn ? 16384 : 16, 1024);
+      return sdesc_sw128_base(smem_u32(smem + L::kQO + (slot * 2 + which) * L::kUnit), mn ? 8192 : 16, 1024);
     };
-    auto issue_sd = [&](int slot) {  // S^T = K Q^T, dP^T = V dO^T
+    auto issue_sd = [&](int j) {  // S^T = K Q^T, dP^T = V dO^T of unit j into buffer j & 1
+      const int slot = j % NS;
+      mbar_wait(&qo_full[slot], (j / NS) & 1);
+      if (leader) ISA_TSTAMP(j, 0, 5);
+      __syncwarp();
+      tc_fence_after();
       if (leader) {
+        const uint32_t tb = tmem + (j & 1) * 128;
         const uint64_t dq = qo_desc(slot, 0, false), dd = qo_desc(slot, 1, false);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-          mma_ss(tmem + 0, dk_base + off, dq + off, idesc_s, kk > 0);
+          const uint64_t oa = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;  // 128-row K / V planes
+          const uint64_t ob = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;   // 64-row Q / dO planes
+          mma_ss(tb, dk_base + oa, dq + ob, idesc_s, kk > 0);
+          mma_ss(tb + 64, dv_base + oa, dd + ob, idesc_s, kk > 0);
         }
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t off = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-          mma_ss(tmem + 128, dv_base + off, dd + off, idesc_s, kk > 0);
-        }
-        mma_commit(s_full);
-      }
-      __syncwarp();
-    };
-    auto issue_g = [&](int slot, bool acc) {  // dV += P^T dO, dK += dS^T Q
-      if (leader) {
-        const uint64_t dq = qo_desc(slot, 0, true), dd = qo_desc(slot, 1, true);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tmem + 256, tmem + 64 + kk * 8, dd + (uint64_t)((kk * 2048) >> 4), idesc_g, acc || kk > 0);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tmem + 384, tmem + 128 + 64 + kk * 8, dq + (uint64_t)((kk * 2048) >> 4), idesc_g, acc || kk > 0);
-        mma_commit(&qo_empty[slot]);
+        mma_commit(&s_full[j & 1]);
       }
       __syncwarp();
     };
     mbar_wait(kv_full, 0);
-    for (int t = 0; t < n_tiles; ++t) {
-      const int slot = t & 1;
-      mbar_wait(&qo_full[slot], (t >> 1) & 1);
-      if (leader) ISA_TSTAMP(t, 0, 5);
+    if (n_units > 0) issue_sd(0);
+    for (int i = 0; i < n_units; ++i) {
+      // buffer (i+1)&1 last held unit i-1, whose softmax finished and whose
+      // dV / dK MMAs were issued (in order, before these writes) last iteration
+      if (i + 1 < n_units) issue_sd(i + 1);
+      mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+      if (leader) ISA_TSTAMP(i, 0, 6);
       __syncwarp();
       tc_fence_after();
-      issue_sd(slot);
-      mbar_wait(p_full, t & 1);
-      if (leader) ISA_TSTAMP(t, 0, 6);
+      if (leader) {
+        const int slot = i % NS;
+        const uint32_t tb = tmem + (i & 1) * 128;
+        const uint64_t dq = qo_desc(slot, 0, true), dd = qo_desc(slot, 1, true);
+        // P^T / dS^T (bf16): queries 0-31 at cols [0,16), 32-63 at [32,48) of each region
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_ts(tmem + 256, tb + (kk >> 1) * 32 + (kk & 1) * 8, dd + (uint64_t)((kk * 2048) >> 4), idesc_g,
+                 (i > 0) || kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_ts(tmem + 384, tb + 64 + (kk >> 1) * 32 + (kk & 1) * 8, dq + (uint64_t)((kk * 2048) >> 4), idesc_g,
+                 (i > 0) || kk > 0);
+        mma_commit(&qo_empty[slot]);
+      }
       __syncwarp();
-      tc_fence_after();
-      issue_g(slot, t > 0);
-      if (leader) ISA_TSTAMP(t, 0, 7);
+      if (leader) ISA_TSTAMP(i, 0, 7);
     }
     if (leader) mma_commit(d_full);
     __syncwarp();
   } else {
-    // ---------------------------------------------------------------- softmax (thread = key row)
-    const int grp = warp >> 2;        // 0: query columns 64-127, 1: columns 0-63
-    const int row = (warp & 3) * 32 + lane;
-    const int kh = row >> 6;          // key half: 0 -> j0, 1 -> j1
+    // ---------------------------------------------------------------- softmax (thread = key row x query half)
+    const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant; query columns [32 half, 32 half + 32)
+    const int row = quad * 32 + lane;
+    const int kh = row >> 6;  // key half (warp-uniform): 0 -> j0, 1 -> j1
     const int j = kh ? j1 : j0;
     const bool key_exists = kh == 0 || has1;
     const int uk = key_exists ? tab[j] : tab[j0];
     const bool key_ok = key_exists && (row & 63) < bw_valid(p, uk);
-    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t t_s = tmem + lane_base, t_dp = tmem + lane_base + 128;
-    const float sl2 = p.sl2;
-    const int c_hi = grp == 0 ? 3 : 1;  // this group's chunks: c_hi, c_hi - 1
-    for (int t = 0; t < n_tiles; ++t) {
-      const int slot = t & 1;
-      const float* st = sStats + slot * 256;
-      // visibility of this key row for the two query halves of the tile
-      bool vis[2];
-      for (int h = 0; h < 2; ++h) {
-        const int li = 2 * t + h;
-        vis[h] = key_ok && li < n_list && ((sVis[li] >> kh) & 1);
-      }
-      mbar_wait(&qo_full[slot], (t >> 1) & 1);  // the producer's lse/rho rows of this tile
-      mbar_wait(s_full, t & 1);
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    const uint64_t sl2x2 = f32x2(p.sl2, p.sl2);
+    for (int t = 0; t < n_units; ++t) {
+      const int slot = t % NS;
+      // per lane (a partial key block has invalid rows); the TMEM loads below are
+      // warp-collective, so the branch is on the warp-wide OR
+      const bool vis = key_ok && ((sVis[t] >> kh) & 1);
+      const bool wvis = __any_sync(0xffffffffu, vis);
+      mbar_wait(&qo_full[slot], (t / NS) & 1);  // the producer's lse/rho rows of this unit
+      mbar_wait(&s_full[t & 1], (t >> 1) & 1);
       if (warp == 0 && lane == 0) ISA_TSTAMP(t, 0, 0);
       __syncwarp();
       tc_fence_after();
-      uint32_t sr[2][32], dr[2][32];
+      const uint32_t t_s = tmem + lane_base + (t & 1) * 128 + half * 32, t_dp = t_s + 64;
+      uint32_t pk[16], dk[16];
+      if (wvis) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(t_s, sr);
+        tmem_ld32(t_dp, dr);
+        tmem_ld_wait();
+        const float2* nl = reinterpret_cast<const float2*>(sStats + slot * 128 + half * 32);
+        const float2* nr = reinterpret_cast<const float2*>(sStats + slot * 128 + 64 + half * 32);
 #pragma unroll
-      for (int k2 = 0; k2 < 2; ++k2) {
-        tmem_ld32(t_s + (c_hi - k2) * 32, sr[k2]);
-        tmem_ld32(t_dp + (c_hi - k2) * 32, dr[k2]);
-      }
-      tmem_ld_wait();
-      // group 0's columns 64-95 are where group 1's packed P^T / dS^T land:
-      // group 0 signals once both its chunks are in registers, group 1 waits
-      // before its first store; each chunk is then computed and stored in turn
-      if (grp == 0)
-        named_bar_arrive(1, 256);
-      else
-        named_bar_sync(1, 256);
-      const bool v = vis[grp == 0 ? 1 : 0];  // uniform per warp (one key half, one query half)
-#pragma unroll
-      for (int k2 = 0; k2 < 2; ++k2) {
-        const int ch = c_hi - k2;
-        uint32_t pk[16], dk[16];
-        if (v) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const int q0 = ch * 32 + 2 * c;
-            float pv[2], dv[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const float pr = ex2_approx(fmaf(__uint_as_float(sr[k2][2 * c + e]), sl2, st[q0 + e]));
-              pv[e] = pr;
-              dv[e] = pr * (__uint_as_float(dr[k2][2 * c + e]) - st[128 + q0 + e]);
-            }
-            pk[c] = pack_bf16x2(pv[0], pv[1]);
-            dk[c] = pack_bf16x2(dv[0], dv[1]);
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) pk[c] = dk[c] = 0u;
+        for (int c = 0; c < 16; ++c) {
+          const float2 l2 = nl[c], r2 = nr[c];  // broadcast reads: -lse, -rho of queries 2c, 2c + 1
+          const uint64_t x = fma_f32x2(f32x2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sl2x2,
+                                       f32x2(l2.x, l2.y));
+          float x0, x1;
+          f32x2_split(x, x0, x1);
+          const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+          const uint64_t dd =
+              add_f32x2(f32x2(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])), f32x2(r2.x, r2.y));
+          float d0, d1;
+          f32x2_split(mul_f32x2(f32x2(p0, p1), dd), d0, d1);
+          pk[c] = vis ? pack_bf16x2(p0, p1) : 0u;
+          dk[c] = vis ? pack_bf16x2(d0, d1) : 0u;
         }
-        tmem_st16(t_s + 64 + ch * 16, pk);
-        tmem_st16(t_dp + 64 + ch * 16, dk);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) pk[c] = dk[c] = 0u;
       }
       mbar_arrive(&st_free[slot]);  // this thread's reads of the slot's stats are done
+      tmem_st16(t_s, pk);   // over this warp's own (already read) S^T columns
+      tmem_st16(t_dp, dk);  // and dP^T columns
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[t & 1]);
       if (warp == 0 && lane == 0) ISA_TSTAMP(t, 0, 4);
       if (warp == 4 && lane == 0) ISA_TSTAMP(t, 1, 4);
     }
@@ -337,13 +322,13 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
     const float invw = 1.f / (float)bw_valid(p, uk);
     const long long cb = ((long long)bh * p.t_new + j) * D;
 #pragma unroll 1
-    for (int c = grp * (D / 64); c < (grp + 1) * (D / 64); ++c) {  // each group stores half the columns
+    for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {  // each half stores half the columns
       uint32_t vr[32], kr[32];
       __syncwarp();
       tmem_ld32(tmem + lane_base + 256 + c * 32, vr);
       tmem_ld32(tmem + lane_base + 384 + c * 32, kr);
       tmem_ld_wait();
-      if (n_tiles == 0) {  // no query block sees these keys: only the centroid part
+      if (n_units == 0) {  // no query block sees these keys: only the centroid part
 #pragma unroll
         for (int e = 0; e < 32; ++e) vr[e] = kr[e] = 0u;
       }
