@@ -23,6 +23,13 @@
 // (~1230 clk) under 32 exp2 per thread (512 MUFU clk per SM sub-partition).
 // Warps: 0-7 softmax + epilogue, 8 TMEM alloc + MMA issue, 9 TMA producer
 // (+ per-query lse/rho rows into shared memory).
+//
+// CENT = true: the Taylor centroid adjoint (taylor.py:286-289) on the same
+// pipeline. CTA = 128 K_new centroids (kc/vc rows c0..c0+127); units = every
+// flat query block (a 1/gridDim.z share of them); key row c carries the bias
+// log2(valid rows of block c) (taylor.py:156) and is masked for the query
+// blocks that hold block c exactly (taylor.py:154, member bits). Writes
+// scale * dK_c / dV_c into the blockIdx.z partial slab of dkc / dvc.
 #pragma once
 #include <type_traits>
 
@@ -44,12 +51,13 @@ struct BwdTcSmem {
   static constexpr int kV = kTile;
   static constexpr int kQO = 2 * kTile;                       // [kSlots][Q, dO]
   static constexpr int kStats = kQO + kSlots * 2 * kUnit;     // [kSlots][-lse 64 | -rho 64] floats
-  static constexpr int kBar = kStats + kSlots * 128 * 4;
+  static constexpr int kMem = kStats + kSlots * 128 * 4;     // [kSlots][4] member words (CENT)
+  static constexpr int kBar = kMem + kSlots * 16;
   static constexpr int kList = kBar + 256;                    // int list (query-block positions) + vis flags
   static constexpr int bytes(int n_list) { return kList + 8 * n_list + 1024; }
 };
 
-template <int D>
+template <int D, bool CENT>
 __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tm_q,
                                                             const __grid_constant__ CUtensorMap tm_k,
                                                             const __grid_constant__ CUtensorMap tm_v,
@@ -72,13 +80,19 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 3 * NS);
   int* s_count = reinterpret_cast<int*>(bars + 7 + 3 * NS);
   float* sStats = reinterpret_cast<float*>(smem + L::kStats);
+  uint32_t* sMem = reinterpret_cast<uint32_t*>(smem + L::kMem);
   int* sList = reinterpret_cast<int*>(smem + L::kList);  // query-block position (x < n_sharp: sharp)
   int* sVis = sList + tp.n_list_max;                       // bit0: lists j0, bit1: lists j1
 
   const int bh = blockIdx.y;
   const int hh = bh % p.H, bb = bh / p.H;
   const int j0 = 2 * blockIdx.x, j1 = 2 * blockIdx.x + 1;
-  const bool has1 = j1 < p.t_new;
+  const bool has1 = CENT || j1 < p.t_new;
+  const int c0 = 128 * blockIdx.x;  // CENT: first centroid row
+  // CENT: this CTA's share [f0, f1) of the flat query blocks
+  const int f_per = CENT ? (p.n_flat + gridDim.z - 1) / gridDim.z : 0;
+  const int f0 = CENT ? min(p.n_flat, (int)blockIdx.z * f_per) : 0;
+  const int f1 = CENT ? min(p.n_flat, f0 + f_per) : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int* tab = p.kv_blk + (long long)bh * p.t_new;
 
@@ -89,16 +103,22 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
     mbar_init(d_full, 1);
     for (int b2 = 0; b2 < 2; ++b2) {
       mbar_init(&s_full[b2], 1);
-      mbar_init(&p_full[b2], 8);
+      mbar_init(&p_full[b2], 4);  // the four warps of unit parity b2
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&qo_full[s], 32);  // every producer lane arrives after its own smem writes
       mbar_init(&qo_empty[s], 1);
-      mbar_init(&st_free[s], 256);
+      mbar_init(&st_free[s], 128);  // the four warps of the unit's parity
     }
     fence_barrier_init();
   }
   __syncthreads();
+  if (CENT) {
+    for (int f = f0 + threadIdx.x; f < f1; f += blockDim.x) {
+      sList[f - f0] = p.n_sharp + f;
+      sVis[f - f0] = 3;
+    }
+  } else {
   for (int x = threadIdx.x; x < p.n_sharp; x += blockDim.x) {
     sList[x] = x;
     sVis[x] = 3;
@@ -113,12 +133,13 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
       sVis[at] = v0 | (v1 << 1);
     }
   }
+  }
   if (warp == 8) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int n_units = p.n_sharp + *s_count;
+  const int n_units = CENT ? f1 - f0 : p.n_sharp + *s_count;
 
   if (warp == 9) {
     // ---------------------------------------------------------------- TMA producer
@@ -127,6 +148,13 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
     if (leader) {
       mbar_arrive_expect_tx(kv_full, 2 * L::kTile);
       for (int half = 0; half < 2; ++half) {
+        if (CENT) {  // kc / vc maps: {D, tn_pad, BH, 1}
+          for (int pl = 0; pl < D / 64; ++pl) {
+            tma_load_4d(smem + L::kK + pl * 16384 + half * 8192, &tm_k, kv_full, pl * 64, c0 + 64 * half, bh, 0, pol);
+            tma_load_4d(smem + L::kV + pl * 16384 + half * 8192, &tm_v, kv_full, pl * 64, c0 + 64 * half, bh, 0, pol);
+          }
+          continue;
+        }
         const int j = half ? (has1 ? j1 : j0) : j0;
         const int u = tab[j];
         const int tok = bw_tok0(p, u);
@@ -180,6 +208,10 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
       for (int k2 = 0; k2 < 2; ++k2) {  // -lse (-inf for padded rows: p = 0 with no predicate), -rho
         st[lane + 32 * k2] = cur.ls[k2] > -INFINITY ? -cur.ls[k2] : -INFINITY;
         st[64 + lane + 32 * k2] = -cur.rh[k2];
+      }
+      if (CENT && lane < 4) {  // this query block's exact members among the 128 centroids
+        const uint32_t* mb = p.bits + ((long long)bh * p.n_flat + (sList[t] - p.n_sharp)) * p.W;
+        sMem[slot * 4 + lane] = (c0 >> 5) + lane < p.W ? mb[(c0 >> 5) + lane] : 0u;
       }
       __syncwarp();
       // each lane releases its own stats writes (the leader also arms the TMA bytes)
@@ -255,71 +287,79 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
     if (leader) mma_commit(d_full);
     __syncwarp();
   } else {
-    // ---------------------------------------------------------------- softmax (thread = key row x query half)
-    const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant; query columns [32 half, 32 half + 32)
+    // ---------------------------------------------------------------- softmax (thread = key row, unit parity = half)
+    // the two warps of a TMEM lane quadrant take alternate units (buffer
+    // half = unit & 1), all 64 query columns each, so both run at once on
+    // their SM sub-partition and each has two units of MMA time per unit
+    const int quad = warp & 3, half = warp >> 2;
     const int row = quad * 32 + lane;
     const int kh = row >> 6;  // key half (warp-uniform): 0 -> j0, 1 -> j1
     const int j = kh ? j1 : j0;
     const bool key_exists = kh == 0 || has1;
-    const int uk = key_exists ? tab[j] : tab[j0];
-    const bool key_ok = key_exists && (row & 63) < bw_valid(p, uk);
+    const int uk = CENT ? 0 : (key_exists ? tab[j] : tab[j0]);
+    // CENT: key row = centroid c0 + row, weighted by its block's valid rows
+    const bool key_ok = CENT ? c0 + row < p.t_new : key_exists && (row & 63) < bw_valid(p, uk);
+    const float cbias = (CENT && key_ok) ? __log2f((float)bw_valid(p, tab[c0 + row])) : 0.f;
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
     const uint64_t sl2x2 = f32x2(p.sl2, p.sl2);
-    for (int t = 0; t < n_units; ++t) {
+    for (int t = half; t < n_units; t += 2) {
       const int slot = t % NS;
       // per lane (a partial key block has invalid rows); the TMEM loads below are
       // warp-collective, so the branch is on the warp-wide OR
-      const bool vis = key_ok && ((sVis[t] >> kh) & 1);
+      mbar_wait(&qo_full[slot], (t / NS) & 1);  // the producer's lse/rho rows (+ member words) of this unit
+      const bool vis = CENT ? key_ok && !((sMem[slot * 4 + (row >> 5)] >> (row & 31)) & 1u)
+                            : key_ok && ((sVis[t] >> kh) & 1);
       const bool wvis = __any_sync(0xffffffffu, vis);
-      mbar_wait(&qo_full[slot], (t / NS) & 1);  // the producer's lse/rho rows of this unit
-      mbar_wait(&s_full[t & 1], (t >> 1) & 1);
-      if (warp == 0 && lane == 0) ISA_TSTAMP(t, 0, 0);
+      mbar_wait(&s_full[half], (t >> 1) & 1);
+      if ((warp & 3) == 0 && lane == 0) ISA_TSTAMP(t, 0, 0);
       __syncwarp();
       tc_fence_after();
-      const uint32_t t_s = tmem + lane_base + (t & 1) * 128 + half * 32, t_dp = t_s + 64;
-      uint32_t pk[16], dk[16];
-      if (wvis) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32(t_s, sr);
-        tmem_ld32(t_dp, dr);
-        tmem_ld_wait();
-        const float2* nl = reinterpret_cast<const float2*>(sStats + slot * 128 + half * 32);
-        const float2* nr = reinterpret_cast<const float2*>(sStats + slot * 128 + 64 + half * 32);
+      const uint32_t t_s = tmem + lane_base + half * 128, t_dp = t_s + 64;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const float2 l2 = nl[c], r2 = nr[c];  // broadcast reads: -lse, -rho of queries 2c, 2c + 1
-          const uint64_t x = fma_f32x2(f32x2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sl2x2,
-                                       f32x2(l2.x, l2.y));
-          float x0, x1;
-          f32x2_split(x, x0, x1);
-          const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
-          const uint64_t dd =
-              add_f32x2(f32x2(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])), f32x2(r2.x, r2.y));
-          float d0, d1;
-          f32x2_split(mul_f32x2(f32x2(p0, p1), dd), d0, d1);
-          pk[c] = vis ? pack_bf16x2(p0, p1) : 0u;
-          dk[c] = vis ? pack_bf16x2(d0, d1) : 0u;
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t pk[16], dk[16];
+        if (wvis) {
+          uint32_t sr[32], dr[32];
+          tmem_ld32(t_s + 32 * ch, sr);
+          tmem_ld32(t_dp + 32 * ch, dr);
+          tmem_ld_wait();
+          const float2* nl = reinterpret_cast<const float2*>(sStats + slot * 128 + ch * 32);
+          const float2* nr = reinterpret_cast<const float2*>(sStats + slot * 128 + 64 + ch * 32);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            const float2 l2 = nl[c], r2 = nr[c];  // broadcast reads: -lse, -rho of queries 2c, 2c + 1
+            const uint64_t x = fma_f32x2(f32x2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sl2x2,
+                                         CENT ? f32x2(l2.x + cbias, l2.y + cbias) : f32x2(l2.x, l2.y));
+            float x0, x1;
+            f32x2_split(x, x0, x1);
+            const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+            const uint64_t dd =
+                add_f32x2(f32x2(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])), f32x2(r2.x, r2.y));
+            float d0, d1;
+            f32x2_split(mul_f32x2(f32x2(p0, p1), dd), d0, d1);
+            pk[c] = vis ? pack_bf16x2(p0, p1) : 0u;
+            dk[c] = vis ? pack_bf16x2(d0, d1) : 0u;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk[c] = dk[c] = 0u;
         }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 16; ++c) pk[c] = dk[c] = 0u;
+        tmem_st16(t_s + 32 * ch, pk);   // over this chunk's own (already read) S^T columns
+        tmem_st16(t_dp + 32 * ch, dk);  // and dP^T columns
       }
       mbar_arrive(&st_free[slot]);  // this thread's reads of the slot's stats are done
-      tmem_st16(t_s, pk);   // over this warp's own (already read) S^T columns
-      tmem_st16(t_dp, dk);  // and dP^T columns
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t & 1]);
-      if (warp == 0 && lane == 0) ISA_TSTAMP(t, 0, 4);
-      if (warp == 4 && lane == 0) ISA_TSTAMP(t, 1, 4);
+      if (lane == 0) mbar_arrive(&p_full[half]);
+      if ((warp & 3) == 0 && lane == 0) ISA_TSTAMP(t, 0, 4);
     }
     // ---------------------------------------------------------------- epilogue
     mbar_wait(d_full, 0);
     __syncwarp();
     tc_fence_after();
-    const long long orow = (long long)bh * p.S + bw_tok0(p, uk) + (row & 63);
-    const float invw = 1.f / (float)bw_valid(p, uk);
+    const long long orow = CENT ? 0 : (long long)bh * p.S + bw_tok0(p, uk) + (row & 63);
+    const float invw = CENT ? 0.f : 1.f / (float)bw_valid(p, uk);
     const long long cb = ((long long)bh * p.t_new + j) * D;
 #pragma unroll 1
     for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {  // each half stores half the columns
@@ -332,7 +372,16 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
 #pragma unroll
         for (int e = 0; e < 32; ++e) vr[e] = kr[e] = 0u;
       }
-      if (key_ok) {
+      if (CENT) {  // partial slab blockIdx.z (reduced by bwd_centroid_reduce_kernel)
+        if (key_ok) {
+          const long long o = blockIdx.z * p.c_part + ((long long)bh * p.t_new + c0 + row) * D + c * 32;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            p.dkc[o + e] = p.scale * __uint_as_float(kr[e]);
+            p.dvc[o + e] = __uint_as_float(vr[e]);
+          }
+        }
+      } else if (key_ok) {
         float* dkp = p.dk + orow * D + c * 32;
         float* dvp = p.dv + orow * D + c * 32;
 #pragma unroll

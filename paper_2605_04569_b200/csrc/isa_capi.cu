@@ -879,7 +879,8 @@ int centroid_splits(const Dims& d) {
     const char* e = getenv("ISA_BWD_CSPLIT");
     return e ? atoi(e) : 0;
   }();
-  int s = forced > 0 ? forced : (4 * 148 + (d.tn_pad / 64) * d.BH - 1) / ((d.tn_pad / 64) * d.BH);
+  const int tiles = (d.tn_pad / 128) * d.BH;  // centroid CTAs per split (128 centroids each)
+  int s = forced > 0 ? forced : (4 * 148 + tiles - 1) / tiles;
   const int cap = d.n_flat / 16 > 1 ? d.n_flat / 16 : 1;
   if (s > cap) s = cap;
   if (s > 16) s = 16;
@@ -918,40 +919,37 @@ BwdWs carve_bwd(const Dims& d0, uint8_t* base) {
 template <int D>
 int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps, const Workspace& w,
                cudaStream_t st) {
-  const size_t tiles = 6ull * 64 * D * 2;  // 2 resident + 2 x 2 double-buffered tiles
-  const size_t sm_dkv = tiles + 4 * 64 * 4 + 16 + 4ull * (d.n_sharp + d.n_flat);
+  using TL = isa::BwdTcSmem<D>;
+  const int n_list = d.n_sharp + d.n_flat;
+  const size_t sm_tc = TL::bytes(n_list);
+  isa::BwdTcParams tp{bp, n_list};
   int rc;
-  if ((rc = ensure_smem((const void*)isa::bwd_dkv_kernel<D, 1>, sm_dkv))) return rc;
+  CUtensorMap tkc = maps[0], tvc = maps[0];  // centroid maps (unused without flat blocks)
   if (d.n_flat) {
+    if ((rc = make_map(&tkc, w.kc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
+                       (long long)d.BH * d.tn_pad * d.D * 2)))
+      return rc;
+    if ((rc = make_map(&tvc, w.vc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
+                       (long long)d.BH * d.tn_pad * d.D * 2)))
+      return rc;
+    // centroid adjoint (taylor.py:286-289): 128 centroids per CTA, flat list split over gridDim.z
     const int cs = bp.c_splits;
-    isa::bwd_dkv_kernel<D, 1><<<dim3(d.tn_pad / 64, d.BH, cs), 128, sm_dkv, st>>>(bp);
-    ISA_LAUNCHED("bwd_dkv_kernel<centroid>");
+    if ((rc = ensure_smem((const void*)isa::bwd_dkv_tc_kernel<D, true>, sm_tc))) return rc;
+    isa::bwd_dkv_tc_kernel<D, true><<<dim3(d.tn_pad / 128, d.BH, cs), 320, sm_tc, st>>>(maps[0], tkc, tvc, maps[3],
+                                                                                         tp);
+    ISA_LAUNCHED("bwd_dkv_tc_kernel<centroid>");
     if (cs > 1) {
       isa::bwd_centroid_reduce_kernel<<<grid1d(bp.c_part, 256), 256, 0, st>>>(bp.dkc, bp.dvc, bp.c_part, cs);
       ISA_LAUNCHED("bwd_centroid_reduce_kernel");
     }
   }
-  {
-    using TL = isa::BwdTcSmem<D>;
-    const int n_list = d.n_sharp + d.n_flat;
-    const size_t sm_tc = TL::bytes(n_list);
-    if ((rc = ensure_smem((const void*)isa::bwd_dkv_tc_kernel<D>, sm_tc))) return rc;
-    isa::BwdTcParams tp{bp, n_list};
-    isa::bwd_dkv_tc_kernel<D><<<dim3((d.t_new + 1) / 2, d.BH), 320, sm_tc, st>>>(maps[0], maps[1], maps[2], maps[3], tp);
-    ISA_LAUNCHED("bwd_dkv_tc_kernel");
-  }
+  if ((rc = ensure_smem((const void*)isa::bwd_dkv_tc_kernel<D, false>, sm_tc))) return rc;
+  isa::bwd_dkv_tc_kernel<D, false><<<dim3((d.t_new + 1) / 2, d.BH), 320, sm_tc, st>>>(maps[0], maps[1], maps[2],
+                                                                                        maps[3], tp);
+  ISA_LAUNCHED("bwd_dkv_tc_kernel");
   {
     using QL = isa::BwdDqSmem<D>;
     if ((rc = ensure_smem((const void*)isa::bwd_dq_tc_kernel<D>, QL::kBytes))) return rc;
-    CUtensorMap tkc = maps[0], tvc = maps[0];  // centroid maps (unused without flat blocks)
-    if (d.n_flat) {
-      if ((rc = make_map(&tkc, w.kc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
-                         (long long)d.BH * d.tn_pad * d.D * 2)))
-        return rc;
-      if ((rc = make_map(&tvc, w.vc_bf, d.D, d.tn_pad, d.BH, 1, (long long)d.D * 2, (long long)d.tn_pad * d.D * 2,
-                         (long long)d.BH * d.tn_pad * d.D * 2)))
-        return rc;
-    }
     const int grid_x = (d.n_sharp + 1) / 2 + 2 * d.items_f;
     isa::bwd_dq_tc_kernel<D><<<dim3(grid_x, d.BH), 320, QL::kBytes, st>>>(
         maps[0], maps[1], maps[2], maps[3], tkc, tvc, bp, w.tiles, w.n_tiles, d.items_f, d.max_tiles);
