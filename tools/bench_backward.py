@@ -60,3 +60,21 @@ if "--gaps" in sys.argv:  # idle device time between consecutive kernels of one 
         prev = e
     print(f"span {(ev[-1].time_range.end - ev[0].time_range.start) / 1e3:.3f} ms, busy "
           f"{sum(e.time_range.end - e.time_range.start for e in ev) / 1e3:.3f} ms")
+if "--host" in sys.argv:  # host-side cost of one call: wall clock vs CUDA events, synchronized on both sides
+    import time
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        a.record()
+        P.isa_backward(q, k, v, icl, cfg, do)
+        b.record()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        print(f"call wall {1e3 * (t1 - t0):.2f} ms, events {a.elapsed_time(b):.2f} ms")
+    import cProfile, pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    P.isa_backward(q, k, v, icl, cfg, do)
+    torch.cuda.synchronize()
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(12)

@@ -21,7 +21,24 @@ def qkv(H, S, D, seed):
     return tuple(torch.randn((1, H, S, D), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
 
 
+def backward_cases():
+    """Backward kernels (dK/dV exact + centroid modes, dQ) on ragged, D = 64 and odd-block shapes."""
+    q, k, v = qkv(2, 4096, 128, 1)
+    P.isa_backward(q, k, v, P.IclLayout(2048, 2048), P.IsaConfig(), torch.randn_like(q))
+    q2, k2, v2 = qkv(1, 1500, 128, 4)
+    P.isa_backward(q2, k2, v2, P.IclLayout(900, 600), P.IsaConfig(strict=False, gamma=0.05), torch.randn_like(q2))
+    q3, k3, v3 = qkv(2, 2048, 64, 5)
+    P.isa_backward(q3, k3, v3, P.IclLayout(1024, 1024), P.IsaConfig(alpha_f=0.75), torch.randn_like(q3))
+    q4, k4, v4 = qkv(1, 700, 64, 6)
+    P.full_attention_backward(q4, k4, v4, None, torch.randn_like(q4))
+    torch.cuda.synchronize()
+
+
 def main():
+    if "--backward" in sys.argv:
+        backward_cases()
+        print("sanitize backward cases done")
+        return
     q, k, v = qkv(2, 4096, 128, 1)
     icl = P.IclLayout(2048, 2048)
     out, tr = P.isa_forward(q, k, v, icl, P.IsaConfig())
@@ -39,9 +56,7 @@ def main():
     P.isa_forward(q3, k3, v3, icl, P.IsaConfig())
     P.dense_attention(q, k, v)
     P.apply_decoupled_rope(q, icl)
-    do = torch.randn_like(q)
-    P.isa_backward(q, k, v, icl, P.IsaConfig(), do)
-    torch.cuda.synchronize()
+    backward_cases()
     print("sanitize cases done")
 
 
