@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(320, 1) bwd_dq_tc_kernel(const __grid_constant
                                                            const __grid_constant__ CUtensorMap tm_vc,
                                                            const BwdParams p, const int4* __restrict__ tiles,
                                                            const int* __restrict__ n_tiles_f, int n_items,
-                                                           int max_tiles) {
+                                                           int max_tiles, int x0) {
   using L = BwdDqSmem<D>;
   constexpr int NK = L::kKSlots, NV = L::kVSlots;
   extern __shared__ uint8_t smem_raw[];
@@ -484,8 +484,9 @@ __global__ void __launch_bounds__(320, 1) bwd_dq_tc_kernel(const __grid_constant
   const int bh = blockIdx.y;
   const int hh = bh % p.H, bb = bh / p.H;
   const int n_sp = (p.n_sharp + 1) >> 1;  // sharp pairs
-  const bool flat = (int)blockIdx.x >= n_sp;
-  const int pair = flat ? blockIdx.x - n_sp : blockIdx.x;
+  const int bx = (int)blockIdx.x + x0;  // x0 = n_sp: a launch of the flat pairs only
+  const bool flat = bx >= n_sp;
+  const int pair = flat ? bx - n_sp : bx;
   const int item = pair >> 1, stg = pair & 1;  // flat: Taylor plan (item, stage)
   int u[2];
   for (int h = 0; h < 2; ++h) {
@@ -827,6 +828,356 @@ __global__ void __launch_bounds__(320, 1) bwd_dq_tc_kernel(const __grid_constant
   if (warp == 8) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------- dQ of the sharp blocks on CTA pairs
+#ifdef ISA_TRACE_DQP  // tools/trace_dq.py --pair: stamp the CTA-pair dQ kernel
+#define DQP_TSTAMP(step, stage, slot) ISA_TSTAMP(step, stage, slot)
+#else
+#define DQP_TSTAMP(step, stage, slot) \
+  do {                                \
+  } while (0)
+#endif
+// The sharp pairs all stream every K_new tile, so two of them (a 2-CTA
+// cluster, 256 query rows) share one tcgen05.mma.cta_group::2 stream: M = 256
+// (each CTA's 128 rows, its own Q/dO and TMEM), the B operand split between
+// the two CTAs' shared memory. Per 128-key tile, CTA r loads
+//   K block 2i+r, both d planes (16 KB): its half of S = Q K^T's B (N = keys)
+//   d plane r of both K blocks (16 KB):  its half of dQ += dS K's B (N = d)
+//   V block 2i+r, both d planes (16 KB): its half of dP = dO V^T's B
+// i.e. 48 KB of TMA and 48 + 48 + 16 KB of MMA operand reads per SM per tile
+// instead of 64 and 64 + 64 + 32 (the single-CTA kernel is bound by that
+// shared-memory traffic, ~1,750 clk per tile against 1,536 of MMA). The
+// leader (rank 0) issues every MMA; commits are multicast to both CTAs; the
+// full barriers of the TMA bytes and the softmax arrivals (dP pulled into
+// registers, dS stored) live in the leader. Softmax and epilogue are those of
+// bwd_dq_tc_kernel (sharp tiles only: no metadata slots, the valid rows come
+// from the block table).
+template <int D>
+struct BwdDqPairLayout {
+  static constexpr int kKSlots = 3, kVSlots = 2;
+  static constexpr int kTile = 128 * D * 2;   // Q / dO: 128 rows
+  static constexpr int kHalf = 64 * D * 2;    // 64 rows x D (two planes of 8 KB at D = 128)
+  static constexpr int kKSlot = 2 * kHalf;    // [S part: own block, planes 0..][dQ part: plane r of both blocks]
+  static constexpr int kVSlot = kHalf;        // own V block, planes 0..
+  static constexpr int kQ = 0;
+  static constexpr int kO = kTile;
+  static constexpr int kK = 2 * kTile;
+  static constexpr int kV = kK + kKSlots * kKSlot;
+  static constexpr int kBar = kV + kVSlots * kVSlot;
+  static constexpr int kValid = kBar + 256;  // [t_new] valid rows of each K_new block (softmax masks)
+  static constexpr int bytes(int t_new) { return kValid + 4 * t_new + 1024; }
+};
+
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+    bwd_dq_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                       const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                       const BwdParams p) {
+  static_assert(D == 128, "the pair dQ kernel splits the d planes between the two CTAs");
+  using L = BwdDqPairLayout<D>;
+  constexpr int NK = L::kKSlots, NV = L::kVSlots;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t* qo_full = bars + 0;               // leader: both CTAs' Q / dO bytes
+  uint64_t* d_full = bars + 1;                // multicast commit
+  uint64_t* dp_full = bars + 2;               // multicast commit
+  uint64_t* dp_free = bars + 3;               // leader: 16 softmax warps hold dP
+  uint64_t* p_full = bars + 4;                // [2] leader: 16 softmax warps stored dS
+  uint64_t* s_full = bars + 6;                // [2] multicast commit
+  uint64_t* kf_full = bars + 8;               // [NK] leader: both CTAs' K bytes
+  uint64_t* kf_empty = bars + 8 + NK;         // [NK] multicast commit after dQ(i)
+  uint64_t* vf_full = bars + 8 + 2 * NK;      // [NV] leader: both CTAs' V bytes
+  uint64_t* vf_empty = bars + 8 + 2 * NK + NV;  // [NV] multicast commit after dP(i)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * NK + 2 * NV);
+  int* sValid = reinterpret_cast<int*>(smem + L::kValid);
+  const uint32_t rank = cluster_ctarank();
+
+  const int bh = blockIdx.y;
+  const int hh = bh % p.H, bb = bh / p.H;
+  const int pair = blockIdx.x;  // sharp pair index (query blocks 2 pair, 2 pair + 1)
+  int u[2];
+  for (int h = 0; h < 2; ++h) {
+    const int x = 2 * pair + h;
+    u[h] = x < p.n_sharp ? p.sharp[bh * p.n_sharp + x] : -1;
+  }
+  const int n_kv = (p.t_new + 1) >> 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int* tab = p.kv_blk + (long long)bh * p.t_new;
+
+  if (threadIdx.x == 0) {
+    mbar_init(qo_full, 1);
+    mbar_init(d_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(dp_free, 16);
+    for (int b2 = 0; b2 < 2; ++b2) {
+      mbar_init(&p_full[b2], 16);
+      mbar_init(&s_full[b2], 1);
+    }
+    for (int s2 = 0; s2 < NK; ++s2) {
+      mbar_init(&kf_full[s2], 1);
+      mbar_init(&kf_empty[s2], 1);
+    }
+    for (int s2 = 0; s2 < NV; ++s2) {
+      mbar_init(&vf_full[s2], 1);
+      mbar_init(&vf_empty[s2], 1);
+    }
+    fence_barrier_init();
+  }
+  for (int j = threadIdx.x; j < p.t_new; j += blockDim.x) sValid[j] = bw_valid(p, __ldg(tab + j));
+  if (warp == 8) tmem_alloc2<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA signal (+ sValid)
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 9) {
+    // ---------------------------------------------------------------- TMA producer (both CTAs)
+    const bool leader = elect_one();
+    const uint64_t pol = policy_evict_last();
+    if (leader) {
+      if (rank == 0) mbar_arrive_expect_tx(qo_full, 4 * L::kTile);
+      for (int h = 0; h < 2; ++h) {
+        const int tok = bw_tok0(p, u[h] >= 0 ? u[h] : (u[0] >= 0 ? u[0] : p.sharp[bh * p.n_sharp]));
+        for (int pl = 0; pl < D / 64; ++pl) {
+          tma_load_4d_pair(smem + L::kQ + pl * 16384 + h * 8192, &tm_q, qo_full, pl * 64, tok, hh, bb, pol);
+          tma_load_4d_pair(smem + L::kO + pl * 16384 + h * 8192, &tm_do, qo_full, pl * 64, tok, hh, bb, pol);
+        }
+      }
+    }
+    int tok_nxt[2];
+    auto tile_tok = [&](int i, int (&t)[2]) {
+      const int u0 = __ldg(tab + 2 * i);
+      t[0] = bw_tok0(p, u0);
+      t[1] = 2 * i + 1 < p.t_new ? bw_tok0(p, __ldg(tab + 2 * i + 1)) : t[0];  // missing block: masked
+    };
+    tile_tok(0, tok_nxt);
+    for (int i = 0; i < n_kv; ++i) {
+      int tok[2] = {tok_nxt[0], tok_nxt[1]};
+      if (i + 1 < n_kv) tile_tok(i + 1, tok_nxt);  // next lookups in flight during the waits
+      const int ks = i % NK, vs = i % NV;
+      if (i >= NK) mbar_wait(&kf_empty[ks], ((i / NK) - 1) & 1);
+      if (leader) {
+        uint8_t* dk = smem + L::kK + ks * L::kKSlot;
+        if (rank == 0) mbar_arrive_expect_tx(&kf_full[ks], 2 * L::kKSlot);
+        for (int pl = 0; pl < D / 64; ++pl)  // S part: own block 2i + rank, both planes
+          tma_load_4d_pair(dk + pl * 8192, &tm_k, &kf_full[ks], pl * 64, tok[rank], hh, bb, pol);
+        for (int h = 0; h < 2; ++h)  // dQ part: plane `rank` of both blocks, [128 keys][64 d]
+          tma_load_4d_pair(dk + L::kHalf + h * 8192, &tm_k, &kf_full[ks], static_cast<int>(rank) * 64, tok[h], hh,
+                           bb, pol);
+      }
+      if (i >= NV) mbar_wait(&vf_empty[vs], ((i / NV) - 1) & 1);
+      if (leader) {
+        uint8_t* dv = smem + L::kV + vs * L::kVSlot;
+        if (rank == 0) mbar_arrive_expect_tx(&vf_full[vs], 2 * L::kVSlot);
+        for (int pl = 0; pl < D / 64; ++pl)
+          tma_load_4d_pair(dv + pl * 8192, &tm_v, &vf_full[vs], pl * 64, tok[rank], hh, bb, pol);
+      }
+      __syncwarp();
+    }
+    // drain: the leader's multicast releases of this CTA's slots have all landed
+    for (int e = n_kv > NK ? n_kv - NK : 0; e < n_kv; ++e) mbar_wait(&kf_empty[e % NK], (e / NK) & 1);
+    for (int e = n_kv > NV ? n_kv - NV : 0; e < n_kv; ++e) mbar_wait(&vf_empty[e % NV], (e / NV) & 1);
+  } else if (warp == 8) {
+    // ---------------------------------------------------------------- MMA issuer (leader CTA)
+    if (rank == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(256, 128, 0, 0);
+      constexpr uint32_t idesc_g = idesc_bf16_f32(256, D, 0, 1);
+      const bool leader = elect_one();
+      const uint64_t q_desc = sdesc_sw128_base(smem_u32(smem + L::kQ), 16, 1024);
+      const uint64_t do_desc = sdesc_sw128_base(smem_u32(smem + L::kO), 16, 1024);
+      const uint32_t kb0 = smem_u32(smem + L::kK), vb0 = smem_u32(smem + L::kV);
+      auto issue_s = [&](int j) {  // S of tile j into buffer j & 1
+        const int ks = j % NK;
+        mbar_wait(&kf_full[ks], (j / NK) & 1);
+        __syncwarp();
+        tc_fence_after();
+        if (leader) {
+          const uint64_t dk = sdesc_sw128_base(kb0 + ks * L::kKSlot, 16, 1024);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t oa = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;  // 128-row Q planes
+            const uint64_t ob = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;   // 64-key K planes
+            mma_ss2(tmem + (j & 1) * 128, q_desc + oa, dk + ob, idesc_s, kk > 0);
+          }
+          mma_commit_pair(&s_full[j & 1]);
+        }
+        __syncwarp();
+      };
+      auto issue_dp = [&](int j) {  // dP of tile j
+        const int vs = j % NV;
+        mbar_wait(&vf_full[vs], (j / NV) & 1);
+        __syncwarp();
+        tc_fence_after();
+        if (leader) {
+          const uint64_t dv = sdesc_sw128_base(vb0 + vs * L::kVSlot, 16, 1024);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t oa = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+            const uint64_t ob = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
+            mma_ss2(tmem + 256, do_desc + oa, dv + ob, idesc_s, kk > 0);
+          }
+          mma_commit_pair(dp_full);
+          mma_commit_pair(&vf_empty[vs]);
+        }
+        __syncwarp();
+      };
+      mbar_wait(qo_full, 0);
+      if (n_kv > 0) {
+        issue_s(0);
+        issue_dp(0);
+      }
+      for (int i = 0; i < n_kv; ++i) {
+        if (i + 1 < n_kv) {
+          issue_s(i + 1);
+          mbar_wait(dp_free, i & 1);  // tile i's dP is in both CTAs' softmax registers
+          issue_dp(i + 1);
+        }
+        if (leader) DQP_TSTAMP(i, 1, 2);
+        mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+        if (leader) DQP_TSTAMP(i, 1, 3);
+        __syncwarp();
+        tc_fence_after();
+        if (leader) {
+          const int ks = i % NK;
+          const uint64_t dkm = sdesc_sw128_base(kb0 + ks * L::kKSlot + L::kHalf, 16384, 1024);  // [128 keys][64 d]
+          const uint32_t ts = tmem + (i & 1) * 128;  // dS (bf16): keys 0-63 at cols [0,32), 64-127 at [64,96)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts2(tmem + 384, ts + (kk >> 2) * 64 + (kk & 3) * 8, dkm + (uint64_t)((kk * 2048) >> 4), idesc_g,
+                    (i > 0) || kk > 0);
+          mma_commit_pair(&kf_empty[ks]);
+        }
+        __syncwarp();
+      }
+      if (leader) mma_commit_pair(d_full);
+      __syncwarp();
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax (thread = query row x key half)
+    const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant; keys [64 half, 64 half + 64) = one block
+    const int row = quad * 32 + lane;
+    const int qh = row >> 6;
+    const int uq = u[qh];
+    const int vq = uq >= 0 ? bw_valid(p, uq) : 0;
+    const bool row_ok = (row & 63) < vq;
+    const long long grow = row_ok ? (long long)bh * p.S + bw_tok0(p, uq) + (row & 63) : 0;
+    const float lse = row_ok ? p.lse[grow] : -INFINITY;
+    const float rho = row_ok ? p.rho[grow] : 0.f;
+    const bool live = row_ok && lse > -INFINITY;
+    const float lse_eff = live ? lse : INFINITY;  // dead rows: exp2(-inf) = 0, no per-element predicate
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    const uint64_t sl2x2 = f32x2(p.sl2, p.sl2), nlse2 = f32x2(-lse_eff, -lse_eff), nrho2 = f32x2(-rho, -rho);
+    const uint32_t t_dp = tmem + lane_base + 256 + half * 64;
+    auto arrive_leader = [&](uint64_t* bar) {
+      if (rank)
+        mbar_arrive_leader(bar);
+      else
+        mbar_arrive(bar);
+    };
+    for (int i = 0; i < n_kv; ++i) {
+      // valid keys of this half's K_new block (warp-uniform), from shared memory: a
+      // dependent table load here sat on the softmax loop's critical path (~450 clk)
+      const int lc = 2 * i + half < p.t_new ? sValid[2 * i + half] : 0;
+      const uint32_t t_s = tmem + lane_base + (i & 1) * 128 + half * 64;
+      if (threadIdx.x == 0) DQP_TSTAMP(i, 0, 2);
+      mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+      mbar_wait(dp_full, i & 1);
+      if (threadIdx.x == 0) DQP_TSTAMP(i, 0, 1);
+      __syncwarp();
+      tc_fence_after();
+      if (lc <= 0) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader(dp_free);
+        uint32_t z[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) z[c] = 0u;
+        tmem_st16(t_s, z);
+        tmem_st16(t_s + 16, z);
+      } else {
+        uint32_t dr[2][32], srr[2][32];  // the whole 64-key half row of dP and S: one TMEM round trip
+        tmem_ld32(t_dp, dr[0]);
+        tmem_ld32(t_dp + 32, dr[1]);
+        tmem_ld32(t_s, srr[0]);
+        tmem_ld32(t_s + 32, srr[1]);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader(dp_free);  // the MMA warp may overwrite dP with tile i+1's
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t pk[16];
+          const uint32_t (&sr)[32] = srr[ch];
+          if (lc >= 64) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const uint64_t x =
+                  fma_f32x2(f32x2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sl2x2, nlse2);
+              float x0, x1;
+              f32x2_split(x, x0, x1);
+              uint64_t pr;
+              if (kEmuEvery > 0 && (c % kEmuEvery) == kEmuEvery - 1) {  // 1 in kEmuEvery pairs on the FMA pipe
+                const float2 e = ex2_emu2(make_float2(x0, x1));
+                pr = f32x2(e.x, e.y);
+              } else {
+                pr = f32x2(ex2_approx(x0), ex2_approx(x1));
+              }
+              const uint64_t dd =
+                  add_f32x2(f32x2(__uint_as_float(dr[ch][2 * c]), __uint_as_float(dr[ch][2 * c + 1])), nrho2);
+              float d0, d1;
+              f32x2_split(mul_f32x2(pr, dd), d0, d1);
+              pk[c] = pack_bf16x2(d0, d1);
+            }
+          } else {
+            const int lcc = lc - 32 * ch;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              float dvv[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int cc = 2 * c + e;
+                const float bias = cc < lcc ? 0.f : -INFINITY;
+                const float pr = ex2_approx(fmaf(__uint_as_float(sr[cc]), p.sl2, bias - lse_eff));
+                dvv[e] = pr * (__uint_as_float(dr[ch][cc]) - rho);
+              }
+              pk[c] = pack_bf16x2(dvv[0], dvv[1]);
+            }
+          }
+          tmem_st16(t_s + ch * 16, pk);  // over S columns this thread has already read
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (threadIdx.x == 0) DQP_TSTAMP(i, 0, 3);
+      if (lane == 0) arrive_leader(&p_full[i & 1]);
+    }
+    // ---------------------------------------------------------------- epilogue
+    mbar_wait(d_full, 0);
+    __syncwarp();
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = half * (D / 64); c < (half + 1) * (D / 64); ++c) {
+      uint32_t qr[32];
+      __syncwarp();
+      tmem_ld32(tmem + lane_base + 384 + c * 32, qr);
+      tmem_ld_wait();
+      if (row_ok) {
+        float* dst = p.dq + grow * D + c * 32;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) dst[e] = n_kv ? p.scale * __uint_as_float(qr[e]) : 0.f;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's MMAs / signals into this CTA are complete
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc2<512>(tmem);
   }
 }
 

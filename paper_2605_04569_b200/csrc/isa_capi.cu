@@ -949,11 +949,28 @@ int launch_bwd(const isa::BwdParams& bp, const Dims& d, const CUtensorMap* maps,
   ISA_LAUNCHED("bwd_dkv_tc_kernel");
   {
     using QL = isa::BwdDqSmem<D>;
-    if ((rc = ensure_smem((const void*)isa::bwd_dq_tc_kernel<D>, QL::kBytes))) return rc;
-    const int grid_x = (d.n_sharp + 1) / 2 + 2 * d.items_f;
-    isa::bwd_dq_tc_kernel<D><<<dim3(grid_x, d.BH), 320, QL::kBytes, st>>>(
-        maps[0], maps[1], maps[2], maps[3], tkc, tvc, bp, w.tiles, w.n_tiles, d.items_f, d.max_tiles);
-    ISA_LAUNCHED("bwd_dq_tc_kernel");
+    const int n_sp = (d.n_sharp + 1) / 2;  // sharp pairs (128 query rows each)
+    int x0 = 0;
+    if constexpr (D == 128) {
+      using PL = isa::BwdDqPairLayout<D>;
+      // sharp pairs on CTA pairs (same K_new stream), flat pairs below; the per-block
+      // valid-row table must fit next to the operand rings (t_new <= ~8K blocks)
+      if (d.n_sharp && pair_mode() && PL::bytes(d.t_new) <= 232448) {
+        const size_t bytes = PL::bytes(d.t_new);
+        if ((rc = ensure_smem((const void*)isa::bwd_dq_pair_kernel<D>, bytes))) return rc;
+        isa::bwd_dq_pair_kernel<D><<<dim3((n_sp + 1) & ~1, d.BH), 320, bytes, st>>>(maps[0], maps[1], maps[2], maps[3],
+                                                                                   bp);
+        ISA_LAUNCHED("bwd_dq_pair_kernel");
+        x0 = n_sp;
+      }
+    }
+    const int grid_x = n_sp - x0 + 2 * d.items_f;
+    if (grid_x > 0) {
+      if ((rc = ensure_smem((const void*)isa::bwd_dq_tc_kernel<D>, QL::kBytes))) return rc;
+      isa::bwd_dq_tc_kernel<D><<<dim3(grid_x, d.BH), 320, QL::kBytes, st>>>(
+          maps[0], maps[1], maps[2], maps[3], tkc, tvc, bp, w.tiles, w.n_tiles, d.items_f, d.max_tiles, x0);
+      ISA_LAUNCHED("bwd_dq_tc_kernel");
+    }
   }
   return ISA_OK;
 }

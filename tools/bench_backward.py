@@ -47,12 +47,14 @@ if "--kernels" in sys.argv:  # per-kernel device times of one backward (CUPTI vi
             r[1] += e.device_time_total / 1e3 if hasattr(e, "device_time_total") else e.cuda_time_total / 1e3
     for name, (n, ms) in sorted(rows.items(), key=lambda x: -x[1][1])[:14]:
         print(f"{ms:9.3f} ms  x{n:<3d} {name}")
-if "--gaps" in sys.argv:  # idle device time between consecutive kernels of one backward
+if "--gaps" in sys.argv:  # idle device time between consecutive kernels of one backward (3 calls)
     from torch.profiler import ProfilerActivity, profile
-    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as pr:
-        P.isa_backward(q, k, v, icl, cfg, do)
-        torch.cuda.synchronize()
-    ev = sorted((e for e in pr.events() if e.device_type.name == "CUDA"), key=lambda e: e.time_range.start)
+    for rep in range(3):
+        with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as pr:
+            P.isa_backward(q, k, v, icl, cfg, do)
+            torch.cuda.synchronize()
+        ev = sorted((e for e in pr.events() if e.device_type.name == "CUDA"), key=lambda e: e.time_range.start)
+        print(f"call {rep}: span {(ev[-1].time_range.end - ev[0].time_range.start) / 1e3:.3f} ms")
     prev = None
     for e in ev:
         if prev is not None and e.time_range.start - prev.time_range.end > 50:

@@ -11,7 +11,8 @@ LIB = os.path.join(ROOT, "paper_2605_04569_b200", "libisa_b200_tracedq.so")
 if "--build" in sys.argv:
     from paper_2605_04569_b200 import build as B
     cta = [a for a in sys.argv[1:] if not a.startswith("--")]
-    os.environ["ISA_EXTRA_DEFINES"] = f"ISA_TRACE={cta[0] if cta else 7},ISA_TRACE_DQ"
+    os.environ["ISA_EXTRA_DEFINES"] = f"ISA_TRACE={cta[0] if cta else 7}," + (
+        "ISA_TRACE_DQP" if "--pair" in sys.argv else "ISA_TRACE_DQ")
     r = subprocess.run(B.nvcc_command(out=LIB), capture_output=True, text=True)
     print("built" if r.returncode == 0 else r.stderr[-2000:])
     raise SystemExit
