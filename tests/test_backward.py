@@ -88,3 +88,41 @@ def test_backward_strided_inputs_and_fp32():
     assert g32.dq.dtype == torch.float32
     for n in ("dq", "dk", "dv"):  # same fp32 gradients; the bf16 call rounds them on return
         assert torch.equal(getattr(g32, n).to(torch.bfloat16), getattr(g, n))
+
+
+@pytest.mark.gpu
+def test_backward_cta_pair_matches_single_cta(tmp_path):
+    """The sharp-block dQ on CTA pairs (bwd_dq_pair_kernel, the default at D = 128)
+    against the single-CTA dQ kernel (ISA_PAIR=0 in a child process, which also
+    runs the forward recompute's K6 on single CTAs): same routing, gradients
+    equal up to accumulation rounding; odd sharp-pair counts included (a
+    padding CTA completes the last cluster)."""
+    import subprocess
+    import sys
+
+    import torch
+
+    import paper_2605_04569_b200 as P
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for S, ls in ((4096, 2048), (2048 + 640, 2048)):
+        out = tmp_path / f"single_{S}.npz"
+        code = (
+            "import sys, torch, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_2605_04569_b200 as P\n"
+            "g = torch.Generator(device='cuda').manual_seed(%d)\n"
+            "q, k, v, do = (torch.randn((1, 3, %d, 128), generator=g, device='cuda').to(torch.bfloat16) for _ in range(4))\n"
+            "r = P.isa_backward(q, k, v, P.IclLayout(%d, %d), P.IsaConfig(strict=False), do)\n"
+            "np.savez(%r, dq=r.dq.float().cpu().numpy(), dk=r.dk.float().cpu().numpy(), dv=r.dv.float().cpu().numpy())\n"
+        ) % (root, S, S, ls, S - ls, str(out))
+        env = dict(os.environ, ISA_PAIR="0")
+        subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+        ref = np.load(out)
+        g = torch.Generator(device="cuda").manual_seed(S)
+        q, k, v, do = (torch.randn((1, 3, S, 128), generator=g, device="cuda").to(torch.bfloat16) for _ in range(4))
+        r = P.isa_backward(q, k, v, P.IclLayout(ls, S - ls), P.IsaConfig(strict=False), do)
+        for name in ("dq", "dk", "dv"):
+            a = getattr(r, name).float().cpu().numpy().astype(np.float64)
+            b = ref[name].astype(np.float64)
+            scale = np.abs(b).max()
+            assert np.abs(a - b).max() <= 1e-2 * scale, (S, name, float(np.abs(a - b).max()), float(scale))
