@@ -537,6 +537,19 @@ def _extras(args, P, q, k, v, icl, cfg, ms, dev):
     d = P.IsaDims.derive(q.shape, icl, cfg)
     res["dense_tflops"] = d.flops().dense_equivalent_mas / (dense_ms * 1e-3) / 1e12
 
+    # §8f rank 2: isa_backward (pipeline.py:373-466) on the same inputs: forward
+    # recompute + tcgen05 dK/dV, dQ and centroid kernels; side measurement (not the metric)
+    try:
+        do = torch.randn(q.shape, device=q.device, dtype=torch.float32).to(q.dtype)
+        bwd_ms = timeit(lambda: P.isa_backward(q, k, v, icl, cfg, do))
+        f = d.flops()
+        res["backward"] = {"ms": bwd_ms, "alg_tflops": 2.5 * (f.exact_mas + f.taylor_mas) / (bwd_ms * 1e-3) / 1e12,
+                           "note": "CUDA events over 2 calls after one warm-up call, incl. the forward recompute; "
+                                   "TFLOP/s at the 2.5x-forward convention"}
+        del do
+    except Exception as exc:  # pragma: no cover
+        res["backward"] = {"error": str(exc)[:200]}
+
     res["e2e"] = _e2e(args, P, q, k, v, icl, cfg, 1)
     return res
 
