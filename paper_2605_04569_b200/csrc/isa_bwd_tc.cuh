@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(320, 1) bwd_dkv_tc_kernel(const __grid_constan
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[half]);
       if ((warp & 3) == 0 && lane == 0) ISA_TSTAMP(t, 0, 4);
+      if (lane == 0) ISA_TSTAMP(t, 1, warp & 3);  // P^T / dS^T stored, per lane quadrant of the group
     }
     // ---------------------------------------------------------------- epilogue
     mbar_wait(d_full, 0);

@@ -25,7 +25,8 @@ torch.cuda.synchronize()
 buf = np.zeros((96, 2, 8), dtype=np.int64)
 N.check(lib.isa_debug_trace_copy(buf.ctypes.data, buf.nbytes))
 t = buf - buf[1, 0, 0]
-print("tile | S_rdy  P_arr(w0) P_arr(w4) | mma: qo_full  p_seen  issued | tile_dt")
+print("unit | S_rdy  P_arr q0 q1 q2 q3 (group warps) | mma: qo_full  p_seen  issued | unit_dt(same group)")
 for i in range(2, 40):
     a = t[i]
-    print(f"{i:4d} | {a[0,0]:8d} {a[0,4]-a[0,0]:6d} {a[1,4]-a[0,0]:6d} | {a[0,5]-a[0,0]:6d} {a[0,6]-a[0,0]:6d} {a[0,7]-a[0,0]:6d} | {t[i+1,0,0]-a[0,0]:6d}")
+    q = " ".join(f"{a[1, w] - a[0, 0]:5d}" for w in range(4))
+    print(f"{i:4d} | {a[0,0]:8d} {q} | {a[0,5]-a[0,0]:6d} {a[0,6]-a[0,0]:6d} {a[0,7]-a[0,0]:6d} | {t[i+2,0,0]-a[0,0]:6d}")
