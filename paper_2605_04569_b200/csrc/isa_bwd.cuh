@@ -51,21 +51,26 @@ __device__ __forceinline__ int bw_valid(const BwdParams& p, int u) {
 __global__ void bwd_rho_kernel(const __nv_bfloat16* __restrict__ dout, long long db, long long dh, long long ds,
                                const __nv_bfloat16* __restrict__ o, int H, int S, int D, float* __restrict__ rho,
                                long long n_rows) {
-  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= n_rows) return;
-  const int bh = static_cast<int>(w / S), tok = static_cast<int>(w % S);
-  const __nv_bfloat16* a = dout + (bh / H) * db + (bh % H) * dh + tok * ds;
-  const __nv_bfloat16* b = o + w * D;
+  // D / 8 lanes per row, one 16-byte load of dO and of O per lane (D = 128: two rows per warp)
+  const int lpr = D >> 3;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long w = t / lpr;
+  const int sub = static_cast<int>(t % lpr);
   float acc = 0.f;
-  for (int d = lane * 2; d < D; d += 64) {
-    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + d));
-    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(b + d));
-    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
-  }
+  if (w < n_rows) {
+    const int bh = static_cast<int>(w / S), tok = static_cast<int>(w % S);
+    const uint4 x = *reinterpret_cast<const uint4*>(dout + (bh / H) * db + (bh % H) * dh + tok * ds + sub * 8);
+    const uint4 y = *reinterpret_cast<const uint4*>(o + w * D + sub * 8);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) rho[w] = acc;
+    for (int e = 0; e < 4; ++e) {
+      const float2 a2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[e]));
+      const float2 b2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ys[e]));
+      acc = fmaf(a2.x, b2.x, fmaf(a2.y, b2.y, acc));
+    }
+  }
+  for (int off = lpr >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (w < n_rows && sub == 0) rho[w] = acc;
 }
 
 }  // namespace isa

@@ -1071,7 +1071,7 @@ int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, co
   ISA_CUDA(cudaMemsetAsync(dk, 0, gbytes, st));  // rows of unselected context blocks get no gradient
   ISA_CUDA(cudaMemsetAsync(dv, 0, gbytes, st));
   const long long n_rows = (long long)d.BH * d.S;
-  isa::bwd_rho_kernel<<<grid1d(n_rows * 32, 256), 256, 0, st>>>(
+  isa::bwd_rho_kernel<<<grid1d(n_rows * (d.D / 8), 256), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(dout), shape->stride_b, shape->stride_h, shape->stride_s, b.o, d.H, d.S, d.D,
       b.rho, n_rows);
   ++launches;
