@@ -1067,9 +1067,13 @@ int isa_backward(const IsaShape* shape, const IsaKnobs* knobs, const void* q, co
   if ((rc = forward_impl(&os, &kf, df, q, k, v, b.o, b.fw, pinned, nullptr, err_word, nullptr, b.lse, st)))
     return rc;
   int launches = g_launches;
-  const size_t gbytes = 4ull * d.BH * d.S * d.D;
-  ISA_CUDA(cudaMemsetAsync(dk, 0, gbytes, st));  // rows of unselected context blocks get no gradient
-  ISA_CUDA(cudaMemsetAsync(dv, 0, gbytes, st));
+  // rows of unselected context blocks get no gradient: zero the context rows of every head
+  // (the dK/dV epilogue writes every source row and every selected context row)
+  if (d.l_ctx) {
+    const size_t pitch = 4ull * d.S * d.D, width = 4ull * d.l_ctx * d.D;
+    ISA_CUDA(cudaMemset2DAsync(static_cast<float*>(dk) + (size_t)d.l_src * d.D, pitch, 0, width, d.BH, st));
+    ISA_CUDA(cudaMemset2DAsync(static_cast<float*>(dv) + (size_t)d.l_src * d.D, pitch, 0, width, d.BH, st));
+  }
   const long long n_rows = (long long)d.BH * d.S;
   isa::bwd_rho_kernel<<<grid1d(n_rows * (d.D / 8), 256), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(dout), shape->stride_b, shape->stride_h, shape->stride_s, b.o, d.H, d.S, d.D,
