@@ -133,6 +133,11 @@ BWD_CASES = [
     ("bwd_gamma_s24", "clustered", 1, 2, 2048, 64, 1024, 1024, 24, {"gamma": 0.5}),
     ("bwd_gamma_raw_s25", "iid-gaussian", 1, 1, 1500, 128, 900, 600, 25,
      {"gamma": 0.05, "residual_softmax": False, "strict": False}),
+    # round 2: the D = 128 backward kernels one branch at a time (sharp dQ on CTA pairs, centroid
+    # adjoint + flat dQ), and batch 2 with ragged segments
+    ("bwd_allsharp_d128_s26", "iid-gaussian", 1, 2, 2048, 128, 1024, 1024, 26, {"alpha_s": 1.0, "alpha_f": 0.0}),
+    ("bwd_allflat_d128_s27", "clustered", 1, 1, 2048, 128, 1024, 1024, 27, {"alpha_s": 0.0, "alpha_f": 1.0}),
+    ("bwd_b2_ragged_d128_s28", "lowrank", 2, 1, 1700, 128, 1000, 700, 28, {"strict": False, "alpha_s": 0.25}),
 ]
 
 

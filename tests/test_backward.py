@@ -55,7 +55,7 @@ def test_backward_numpy_io_and_pinned_routing():
 
     import paper_2605_04569_b200 as P
 
-    m, (q, k, v, do), ref = _case(BWD_CASES[0])
+    m, (q, k, v, do), ref = _case("bwd_cfg1_iid_s20")
     icl, cfg = P.IclLayout(m["l_src"], m["l_ctx"]), P.IsaConfig(**m["cfg"])
     g = P.isa_backward(q, k, v, icl, cfg, do)
     assert isinstance(g.dq, np.ndarray) and g.dq.dtype == np.float32
@@ -75,7 +75,7 @@ def test_backward_strided_inputs_and_fp32():
 
     import paper_2605_04569_b200 as P
 
-    m, (q, k, v, do), ref = _case(BWD_CASES[0])
+    m, (q, k, v, do), ref = _case("bwd_cfg1_iid_s20")
     icl, cfg = P.IclLayout(m["l_src"], m["l_ctx"]), P.IsaConfig(**m["cfg"])
     dev = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k, v, do)]
     g = P.isa_backward(*dev[:3], icl, cfg, dev[3])
