@@ -138,6 +138,7 @@ BWD_CASES = [
     ("bwd_allsharp_d128_s26", "iid-gaussian", 1, 2, 2048, 128, 1024, 1024, 26, {"alpha_s": 1.0, "alpha_f": 0.0}),
     ("bwd_allflat_d128_s27", "clustered", 1, 1, 2048, 128, 1024, 1024, 27, {"alpha_s": 0.0, "alpha_f": 1.0}),
     ("bwd_b2_ragged_d128_s28", "lowrank", 2, 1, 1700, 128, 1000, 700, 28, {"strict": False, "alpha_s": 0.25}),
+    ("bwd_mid_d128_s29", "iid-gaussian", 1, 1, 4096, 128, 2048, 2048, 29, {}),  # longer K/V and query streams
 ]
 
 
